@@ -1,0 +1,143 @@
+/* thinkv_b200.h -- C ABI of the B200-native ThinKV decode path.
+ *
+ * The reference (arxiv 2510.01290 desk simulator, /root/reference/proj) has no
+ * FFI: its hot path is the private per-step driver ThinkvMethod
+ * (proj/src/sim.cpp:494-958) over the public C++ API in proj/include/thinkv/.
+ * This header is the drop-in boundary for that path: plain C types, device or
+ * host pointers plus sizes, status codes instead of exceptions.  Each entry
+ * point names the reference interface it replaces.
+ *
+ * Status codes mirror thinkv::Error::exit_code() (proj/include/thinkv/errors.hpp:31-46):
+ *   0 ok, 1 unexpected, 2 structural/config/parse, 3 calibration,
+ *   4 out-of-memory (block pool exhausted), 5 integrity.
+ * The message of the last failure on the calling thread is tkv_last_error().
+ *
+ * Threading: a run is single-threaded (SPEC.md:426 -- one pager per layer
+ * needs external mutual exclusion); distinct runs may be driven from distinct
+ * threads.  Device work is asynchronous on the run's stream; device-side
+ * failures (e.g. pool exhaustion inside the emission kernel) are sticky per
+ * unit and reported by the next synchronising call (tkv_synchronize,
+ * tkv_finish, tkv_dump_json).
+ */
+#ifndef THINKV_B200_H
+#define THINKV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TKV_ABI_VERSION 1
+
+enum tkv_status {
+  TKV_OK = 0,
+  TKV_ERR_UNEXPECTED = 1,
+  TKV_ERR_CONFIG = 2,
+  TKV_ERR_CALIBRATION = 3,
+  TKV_ERR_OOM = 4,
+  TKV_ERR_INTEGRITY = 5
+};
+
+enum tkv_dtype { TKV_DTYPE_BF16 = 0, TKV_DTYPE_F32 = 1, TKV_DTYPE_F64 = 2 };
+
+typedef struct tkv_ctx tkv_ctx;
+typedef struct tkv_run tkv_run;
+
+/* Run description: the hot-path fields of thinkv::SimConfig
+ * (proj/include/thinkv/sim.hpp:38-68) for num_seqs independent sequences of
+ * units_per_seq units each.  A unit is one (layer, kv-head) of a sequence --
+ * one reference "layer" (one BlockPager, segment list and buffer).  All units
+ * of a sequence share thought labels (sim.cpp:717-722). */
+typedef struct tkv_run_desc {
+  int32_t num_seqs;
+  int32_t units_per_seq;
+  int32_t num_q_heads;      /* G query heads sharing a unit's KV head */
+  int32_t gqa_maxpool;      /* 1: gqa_group_size = G (one max-pooled row, attention.cpp:110-122); 0: per-head rows */
+  int32_t head_dim;
+  int32_t tau;              /* refresh interval (thought.cpp:361-365) */
+  int32_t group_size;       /* emission window g (<= 64) */
+  int32_t block_size;       /* slots per block (<= 32) */
+  int32_t pool_blocks;      /* 0 = SimConfig::effective_pool_blocks() (sim.cpp:65-78) */
+  int64_t budget;
+  int32_t num_levels;
+  int64_t levels[16];       /* RetentionSchedule (evictor.hpp:19-27) */
+  int32_t psi_bits[8];      /* PrecisionMap bits per band: 2, 4, 8 or 16 */
+  int32_t num_thoughts;
+  double threshold_fraction;
+  int64_t prompt_len;
+  int64_t max_gen_len;
+  int32_t scripted;         /* 1: ScriptedTrace labels (sim.hpp:24-36) */
+  int32_t script_len;
+  const int32_t* script_bands;  /* [num_seqs][script_len], copied at create */
+  int32_t per_layer_thought;    /* must be 0 in this version */
+  int32_t num_thresholds;
+  double thresholds[8];     /* CalibrationResult::thresholds */
+  int32_t num_calib_units;
+  int32_t calib_units[64];  /* CalibrationResult::layers (unit indices within a sequence) */
+  int32_t input_dtype;      /* tkv_dtype of q/k/v */
+  int32_t record_events;    /* keep the evict/refresh/emit event log for tkv_dump_json("events") */
+  int32_t num_dump_positions;
+  const int64_t* dump_positions;  /* SimConfig::dump_positions, copied at create */
+} tkv_run_desc;
+
+typedef struct tkv_bytes_t {
+  int64_t live_slots;        /* live (unmasked) pager slots over all units */
+  int64_t resident_slots;    /* filled slots incl. soft-evicted */
+  int64_t live_code_bytes;   /* K+V code bytes of live slots */
+  int64_t live_scale_bytes;  /* live E4M3 key/value group scales + FP8 f32 scales (pager.cpp:321-323) */
+  int64_t buffer_bytes;      /* fp buffer + current token K/V bytes */
+  int64_t qo_bytes;          /* q read + output written */
+  int64_t meta_bytes;        /* block-table metadata read by the attention kernel */
+  int64_t algorithmic_bytes; /* sum of the above: the roofline numerator of one attention launch */
+} tkv_bytes_t;
+
+const char* tkv_last_error(void);
+int tkv_abi_version(void);
+
+int tkv_init(int device, tkv_ctx** out);
+int tkv_ctx_destroy(tkv_ctx* ctx);
+
+/* Replaces constructing ThinkvMethod (sim.cpp:494-508) + SimConfig::validate (sim.cpp:84-133). */
+int tkv_run_create(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run** out);
+int tkv_run_destroy(tkv_run* run);
+
+/* Replaces ThinkvMethod::process (sim.cpp:748-843) for every unit at once.
+ * q: [units][G][d], k/v: [units][d] in input_dtype, DEVICE pointers;
+ * out: [units][rows][d] fp32 DEVICE pointer, rows = 1 (max-pool) or G.
+ * stream: cudaStream_t (NULL = the run's own stream). */
+int tkv_step(tkv_run* run, const void* q, const void* k, const void* v, float* out, void* stream);
+
+/* Same with HOST buffers: copies q/k/v in, steps, copies out back (synchronous). */
+int tkv_step_host(tkv_run* run, const void* q, const void* k, const void* v, float* out);
+
+/* Replaces ThinkvMethod::finish (sim.cpp:871-958): final partial window,
+ * final budget pass, metrics. */
+int tkv_finish(tkv_run* run);
+
+/* Waits for the run's stream and reports sticky device-side errors. */
+int tkv_synchronize(tkv_run* run);
+int64_t tkv_position(const tkv_run* run);
+
+/* JSON views in the reference's own formats: "tables" (BlockPager::dump,
+ * pager.cpp:327-362, one per unit), "segments" (sim.cpp:919-937), "events"
+ * (JSON lines, sim.cpp:643-648/663-670/724-733), "metrics" (RunMetrics::to_json),
+ * "step_dumps".  Writes up to cap bytes (NUL-terminated) and the full length
+ * to *needed. */
+int tkv_dump_json(tkv_run* run, int seq, const char* what, char* buf, size_t cap, size_t* needed);
+
+/* Byte accounting of the attention view for the next step (FragmentationStats,
+ * pager.cpp:299-325, extended with buffer/q/out/metadata bytes). */
+int tkv_bytes(tkv_run* run, tkv_bytes_t* out);
+
+/* Last fp64 per-unit sparsity (layer_sparsity_average) computed on a refresh step. */
+int tkv_unit_sparsity(tkv_run* run, double* out, int64_t n);
+
+/* Deterministic synthetic bf16 inputs for step `step` (synth.h) on device. */
+int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t step, void* q, void* k, void* v, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* THINKV_B200_H */

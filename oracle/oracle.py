@@ -61,6 +61,7 @@ def lib():
             L.orc_dump.argtypes = [C.c_void_p, C.c_int, C.c_char_p]
             L.orc_toy_compare.restype = C.c_char_p
             L.orc_toy_compare.argtypes = [C.c_char_p]
+            L.orc_toy_stream.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.orc_synth_step.argtypes = [C.POINTER(SynthParams), C.c_int64, C.c_int32, C.c_int32,
                                          C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
             _lib = L
@@ -195,6 +196,22 @@ class OracleError(RuntimeError):
 
 def toy_compare(config: dict) -> dict:
     return json.loads(lib().orc_toy_compare(json.dumps(config).encode()).decode())
+
+
+def toy_stream(config: dict):
+    """ToyModel q/k/v stream of a reference SimConfig dict (doubles):
+    q [steps, layers, heads, d], k/v [steps, layers, d]."""
+    m = config["model"]
+    steps = config.get("prompt_len", 0) + config["max_gen_len"]
+    L, H, D = m["num_layers"], m["num_heads"], m["head_dim"]
+    q = np.zeros((steps, L, H, D))
+    k = np.zeros((steps, L, D))
+    v = np.zeros((steps, L, D))
+    rc = lib().orc_toy_stream(json.dumps(config).encode(), q.ctypes.data, k.ctypes.data,
+                              v.ctypes.data)
+    if rc != 0:
+        raise OracleError(rc, "toy stream failed")
+    return q, k, v
 
 
 def synth_step(seed: int, units_per_seq: int, tau: int, units: int, G: int, d: int, step: int,

@@ -656,6 +656,47 @@ const char* orc_toy_compare(const char* config_json) {
   return result.c_str();
 }
 
+int orc_toy_stream(const char* config_json, double* q, double* k, double* v) {
+  try {
+    const SimConfig cfg = SimConfig::from_json(json::parse(config_json));
+    ToyModel model(cfg.model);
+    const std::vector<TokenId> prompt = model.sample_prompt(cfg.seed, cfg.prompt_len);
+    Rng rng(Rng::mix(cfg.seed, 0xBEEF));
+    TokenId next = rng.uniform_int(0, cfg.model.embed_dim - 1);
+    const int L = cfg.model.num_layers, H = cfg.model.num_heads, D = cfg.model.head_dim;
+    const int groups = cfg.model.num_groups(), gs = cfg.model.gqa_group_size;
+    const double scale = 1.0 / std::sqrt(static_cast<double>(D));
+    std::vector<std::vector<Vec>> ck(L), cv(L);
+    const std::int64_t steps = cfg.prompt_len + cfg.max_gen_len;
+    for (std::int64_t pos = 0; pos < steps; ++pos) {
+      const TokenId tok = pos < cfg.prompt_len ? prompt[pos] : next;
+      Vec hidden = model.embed(tok);
+      for (int l = 0; l < L; ++l) {
+        ToyModel::LayerProjection pr = model.project(l, hidden, pos);
+        ck[l].push_back(pr.key);
+        cv[l].push_back(pr.value);
+        for (int h = 0; h < H; ++h)
+          std::copy(pr.queries[h].begin(), pr.queries[h].end(), q + ((pos * L + l) * H + h) * D);
+        std::copy(pr.key.begin(), pr.key.end(), k + (pos * L + l) * D);
+        std::copy(pr.value.begin(), pr.value.end(), v + (pos * L + l) * D);
+        std::vector<const Vec*> kp, vp;
+        for (const Vec& x : ck[l]) kp.push_back(&x);
+        for (const Vec& x : cv[l]) vp.push_back(&x);
+        std::vector<Vec> gouts;
+        for (int g = 0; g < groups; ++g) {
+          std::span<const Vec> qs(pr.queries.data() + g * gs, gs);
+          gouts.push_back(gqa_attend(qs, std::span<const Vec* const>(kp), std::span<const Vec* const>(vp), scale).output);
+        }
+        hidden = model.combine(l, hidden, gouts);
+      }
+      next = model.readout(hidden);
+    }
+    return 0;
+  } catch (...) {
+    return 2;
+  }
+}
+
 void orc_synth_step(const tkv_synth_params* p, int64_t unit0, int32_t units, int32_t G, int32_t d,
                     int64_t step, uint16_t* q, uint16_t* k, uint16_t* v) {
   for (int32_t i = 0; i < units; ++i) {

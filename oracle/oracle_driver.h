@@ -71,6 +71,11 @@ const char* orc_dump(orc_run* run, int seq, const char* what);
 // step_dumps for each.  Used to pin the restatement (tests/test_oracle.py).
 const char* orc_toy_compare(const char* config_json);
 
+// The ToyModel input stream of a SimConfig (ShadowStream restatement,
+// sim.cpp:383-447): q [steps][layers][heads][d], k/v [steps][layers][d].
+// Arrays must be sized by the caller (see oracle.py toy_stream).
+int orc_toy_stream(const char* config_json, double* q, double* k, double* v);
+
 // Synthetic bf16 inputs for `units` units starting at unit index unit0.
 void orc_synth_step(const tkv_synth_params* p, int64_t unit0, int32_t units,
                     int32_t G, int32_t d, int64_t step, uint16_t* q,

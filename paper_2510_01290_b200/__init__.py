@@ -1,0 +1,200 @@
+"""B200-native ThinKV decode path (arxiv 2510.01290).
+
+Host-side mirror of the reference's per-step interface over the C ABI in
+include/thinkv_b200.h:
+
+  reference (proj/src/sim.cpp, proj/include/thinkv/sim.hpp)   here
+  --------------------------------------------------------    ---------------------------
+  SimConfig (hot-path fields)                                  ThinkvConfig
+  ThinkvMethod(cfg)            (sim.cpp:494-508)               DecodeRun(cfg)
+  ThinkvMethod::process(sv)    (sim.cpp:748-843)               DecodeRun.step(q, k, v, out)
+  ThinkvMethod::finish()       (sim.cpp:871-958)               DecodeRun.finish()
+  RunOutput.final_block_tables / final_segments / events_jsonl DecodeRun.tables()/segments()/events()
+  RunOutput.metrics / step_dumps                               DecodeRun.metrics()/step_dumps()
+  thinkv::Error{kind}.exit_code()                              TkvError.code (same numbers)
+
+Inputs q/k/v are torch CUDA tensors (device memory and streams come from
+PyTorch; all compute is in the library's sm_100a kernels).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+from . import _abi
+from ._abi import TkvError, check, lib
+
+__all__ = ["ThinkvConfig", "DecodeRun", "TkvError", "Context"]
+
+
+@dataclass
+class ThinkvConfig:
+    num_seqs: int = 1
+    units_per_seq: int = 1
+    num_q_heads: int = 1
+    gqa_maxpool: bool = False
+    head_dim: int = 16
+    tau: int = 128
+    group_size: int = 16
+    block_size: int = 8
+    pool_blocks: int = 0
+    budget: int = 1024
+    levels: Sequence[int] = (64, 32, 16, 8, 4)
+    psi_bits: Sequence[int] = (4, 4, 2)  # per band: E, R, T (R4E4T2)
+    num_thoughts: int = 3
+    threshold_fraction: float = 0.01
+    prompt_len: int = 0
+    max_gen_len: int = 1024
+    scripted: bool = True
+    script: Optional[List[List[int]]] = None
+    per_layer_thought: bool = False
+    thresholds: Sequence[float] = ()
+    calib_units: Sequence[int] = ()
+    input_dtype: str = "bf16"
+    record_events: bool = False
+    dump_positions: Sequence[int] = ()
+
+    @property
+    def units(self) -> int:
+        return self.num_seqs * self.units_per_seq
+
+    @property
+    def out_rows(self) -> int:
+        return 1 if self.gqa_maxpool else self.num_q_heads
+
+    def to_desc(self):
+        import numpy as np
+        d = _abi.RunDesc()
+        keep = []
+        for name in ("num_seqs", "units_per_seq", "num_q_heads", "head_dim", "tau", "group_size",
+                     "block_size", "pool_blocks", "budget", "num_thoughts", "threshold_fraction",
+                     "prompt_len", "max_gen_len"):
+            setattr(d, name, getattr(self, name))
+        d.gqa_maxpool = int(self.gqa_maxpool)
+        d.num_levels = len(self.levels)
+        for i, x in enumerate(self.levels):
+            d.levels[i] = int(x)
+        for i, b in enumerate(self.psi_bits):
+            d.psi_bits[i] = int(b)
+        d.scripted = int(self.scripted)
+        if self.scripted:
+            script = self.script or [[1]] * self.num_seqs
+            n = max(len(s) for s in script)
+            arr = np.array([list(s) + [s[-1]] * (n - len(s)) for s in script], dtype=np.int32)
+            keep.append(arr)
+            d.script_len = n
+            d.script_bands = arr.ctypes.data_as(C.POINTER(C.c_int32))
+        d.per_layer_thought = int(self.per_layer_thought)
+        d.num_thresholds = len(self.thresholds)
+        for i, t in enumerate(self.thresholds):
+            d.thresholds[i] = t
+        d.num_calib_units = len(self.calib_units)
+        for i, u in enumerate(self.calib_units):
+            d.calib_units[i] = u
+        d.input_dtype = _abi.DTYPES[self.input_dtype]
+        d.record_events = int(self.record_events)
+        if self.dump_positions:
+            dp = np.array(self.dump_positions, dtype=np.int64)
+            keep.append(dp)
+            d.num_dump_positions = len(dp)
+            d.dump_positions = dp.ctypes.data_as(C.POINTER(C.c_int64))
+        return d, keep
+
+
+class Context:
+    """One CUDA device (tkv_init)."""
+
+    _by_device = {}
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib.tkv_init(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @classmethod
+    def get(cls, device: int = 0) -> "Context":
+        if device not in cls._by_device:
+            cls._by_device[device] = cls(device)
+        return cls._by_device[device]
+
+
+class DecodeRun:
+    """The ThinKV decode path for a batch of sequences on one GPU."""
+
+    def __init__(self, cfg: ThinkvConfig, device: int = 0):
+        self.cfg = cfg
+        self.ctx = Context.get(device)
+        desc, keep = cfg.to_desc()
+        h = C.c_void_p()
+        check(lib.tkv_run_create(self.ctx._h, C.byref(desc), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.tkv_run_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    # -- stepping ---------------------------------------------------------
+    def step(self, q, k, v, out, stream=None):
+        """q [units,G,d], k/v [units,d] (input dtype), out [units,rows,d] fp32: CUDA tensors."""
+        s = stream.cuda_stream if stream is not None else None
+        check(lib.tkv_step(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), s))
+
+    def step_host(self, q, k, v, out):
+        """Same with host (numpy / pinned CPU tensor) buffers, synchronous."""
+        ptr = (lambda a: a.ctypes.data) if hasattr(q, "ctypes") else (lambda a: a.data_ptr())
+        check(lib.tkv_step_host(self._h, ptr(q), ptr(k), ptr(v), ptr(out)))
+
+    def synth_inputs(self, seed: int, step: int, q, k, v, stream=None):
+        s = stream.cuda_stream if stream is not None else None
+        check(lib.tkv_synth_inputs(self._h, seed, step, q.data_ptr(), k.data_ptr(), v.data_ptr(), s))
+
+    def finish(self):
+        check(lib.tkv_finish(self._h))
+
+    def synchronize(self):
+        check(lib.tkv_synchronize(self._h))
+
+    @property
+    def position(self) -> int:
+        return lib.tkv_position(self._h)
+
+    # -- views in the reference's JSON shapes -------------------------------
+    def _dump(self, seq: int, what: str) -> str:
+        need = C.c_size_t(0)
+        check(lib.tkv_dump_json(self._h, seq, what.encode(), None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        check(lib.tkv_dump_json(self._h, seq, what.encode(), buf, need.value, C.byref(need)))
+        return buf.value.decode()
+
+    def tables(self, seq: int = 0):
+        return json.loads(self._dump(seq, "tables"))
+
+    def segments(self, seq: int = 0):
+        return json.loads(self._dump(seq, "segments"))
+
+    def events(self, seq: int = 0) -> str:
+        return self._dump(seq, "events")
+
+    def metrics(self, seq: int = 0):
+        return json.loads(self._dump(seq, "metrics"))
+
+    def step_dumps(self, seq: int = 0):
+        return json.loads(self._dump(seq, "step_dumps"))
+
+    def bytes(self) -> dict:
+        b = _abi.Bytes()
+        check(lib.tkv_bytes(self._h, C.byref(b)))
+        return {n: getattr(b, n) for n, _ in _abi.Bytes._fields_}
+
+    def unit_sparsity(self):
+        import numpy as np
+        out = np.zeros(self.cfg.units, dtype=np.float64)
+        check(lib.tkv_unit_sparsity(self._h, out.ctypes.data, out.size))
+        return out

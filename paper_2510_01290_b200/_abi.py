@@ -1,0 +1,88 @@
+"""ctypes binding of include/thinkv_b200.h (libthinkv_b200.so, built in-tree).
+
+The library is the product: there is no Python or CPU fallback.  Importing
+this module loads the shared library eagerly and raises if it is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libthinkv_b200.so")
+
+# Every symbol include/thinkv_b200.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "tkv_last_error", "tkv_abi_version", "tkv_init", "tkv_ctx_destroy", "tkv_run_create",
+    "tkv_run_destroy", "tkv_step", "tkv_step_host", "tkv_finish", "tkv_synchronize",
+    "tkv_position", "tkv_dump_json", "tkv_bytes", "tkv_unit_sparsity", "tkv_synth_inputs",
+)
+
+STATUS = {0: "ok", 1: "unexpected", 2: "config", 3: "calibration", 4: "out_of_memory",
+          5: "integrity"}
+
+DTYPES = {"bf16": 0, "f32": 1, "f64": 2}
+
+
+class RunDesc(C.Structure):
+    _fields_ = [
+        ("num_seqs", C.c_int32), ("units_per_seq", C.c_int32), ("num_q_heads", C.c_int32),
+        ("gqa_maxpool", C.c_int32), ("head_dim", C.c_int32), ("tau", C.c_int32),
+        ("group_size", C.c_int32), ("block_size", C.c_int32), ("pool_blocks", C.c_int32),
+        ("budget", C.c_int64), ("num_levels", C.c_int32), ("levels", C.c_int64 * 16),
+        ("psi_bits", C.c_int32 * 8), ("num_thoughts", C.c_int32),
+        ("threshold_fraction", C.c_double), ("prompt_len", C.c_int64),
+        ("max_gen_len", C.c_int64), ("scripted", C.c_int32), ("script_len", C.c_int32),
+        ("script_bands", C.POINTER(C.c_int32)), ("per_layer_thought", C.c_int32),
+        ("num_thresholds", C.c_int32), ("thresholds", C.c_double * 8),
+        ("num_calib_units", C.c_int32), ("calib_units", C.c_int32 * 64),
+        ("input_dtype", C.c_int32), ("record_events", C.c_int32),
+        ("num_dump_positions", C.c_int32), ("dump_positions", C.POINTER(C.c_int64)),
+    ]
+
+
+class Bytes(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "live_slots", "resident_slots", "live_code_bytes", "live_scale_bytes", "buffer_bytes",
+        "qo_bytes", "meta_bytes", "algorithmic_bytes")]
+
+
+class TkvError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{STATUS.get(code, code)}] {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the ThinKV decode path)")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    L.tkv_last_error.restype = C.c_char_p
+    L.tkv_abi_version.restype = C.c_int
+    L.tkv_init.argtypes = [C.c_int, C.POINTER(vp)]
+    L.tkv_ctx_destroy.argtypes = [vp]
+    L.tkv_run_create.argtypes = [vp, C.POINTER(RunDesc), C.POINTER(vp)]
+    L.tkv_run_destroy.argtypes = [vp]
+    L.tkv_step.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.tkv_step_host.argtypes = [vp, vp, vp, vp, vp]
+    L.tkv_finish.argtypes = [vp]
+    L.tkv_synchronize.argtypes = [vp]
+    L.tkv_position.argtypes = [vp]
+    L.tkv_position.restype = C.c_int64
+    L.tkv_dump_json.argtypes = [vp, C.c_int, C.c_char_p, C.c_char_p, C.c_size_t,
+                                C.POINTER(C.c_size_t)]
+    L.tkv_bytes.argtypes = [vp, C.POINTER(Bytes)]
+    L.tkv_unit_sparsity.argtypes = [vp, vp, C.c_int64]
+    L.tkv_synth_inputs.argtypes = [vp, C.c_uint64, C.c_int64, vp, vp, vp, vp]
+    return L
+
+
+lib = _load()
+
+
+def check(rc: int):
+    if rc != 0:
+        raise TkvError(rc, lib.tkv_last_error().decode(errors="replace"))

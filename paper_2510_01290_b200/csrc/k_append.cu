@@ -1,0 +1,329 @@
+// K2: quantize-on-append.  One CTA per unit emits the unit's buffered window:
+//   phase A  window quantization (quantize_window, proj/src/quant.cpp:486-580)
+//            in fp64, bit-exact; keys grouped per channel across the window's
+//            tokens, values per token in g-channel chunks, FP8 with one fp32
+//            scale per side per window;
+//   phase B  ordered slot claim and block-table bookkeeping
+//            (BlockPager::append_tokens, proj/src/pager.cpp:114-219): soft-
+//            evicted slots of same-thought blocks in physical order, then
+//            unfilled tail slots, then the lowest free block ids; the OOM check
+//            happens before any mutation (pager.cpp:147-159);
+//   phase C  packed code / scale stores into the claimed slots (no compaction:
+//            slots never move) and token -> slot index updates.
+#include <cuda_runtime.h>
+
+#include "tkv_codec.cuh"
+#include "tkv_kernels.h"
+#include "tkv_state.h"
+
+namespace {
+
+__device__ __forceinline__ double load_in(const uint8_t* p, int dtype, int64_t idx) {
+  if (dtype == TKV_IN_BF16) {
+    const uint16_t b = reinterpret_cast<const uint16_t*>(p)[idx];
+    return (double)__uint_as_float(((uint32_t)b) << 16);
+  }
+  if (dtype == TKV_IN_F32) return (double)reinterpret_cast<const float*>(p)[idx];
+  return reinterpret_cast<const double*>(p)[idx];
+}
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+  // max is order-independent, so a tree reduction is exact.
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = fmax(r, red[i]);
+  return r;
+}
+
+struct FlushSmem {
+  int32_t claim[64];
+  int8_t reuse[64];
+  int32_t win;
+  int32_t abort_code;
+  int32_t bad;
+  float kf, vf;
+  double red[32];
+};
+
+__global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n, int pos0,
+                                                    const TkvFlushCtl* __restrict__ ctl,
+                                                    int units_per_group) {
+  const TkvDims& dm = st.dm;
+  const int u = blockIdx.x;
+  if (u >= dm.U) return;
+  const int D = dm.D, g = dm.g, bs = dm.bs, P = dm.P;
+  const TkvFlushCtl c = ctl[u / units_per_group];
+  const int fmt = dm.band_fmt[c.band];
+  const int kbytes = dm.band_bytes[c.band];
+  extern __shared__ __align__(16) uint8_t dyn[];
+  __shared__ FlushSmem sm;
+  uint8_t* kc = dyn;                         // [n][D] key codes
+  uint8_t* vc = kc + 64 * D;                 // [n][D] value codes
+  uint8_t* ksc = vc + 64 * D;                // [D] key scale codes
+  uint8_t* vsc = ksc + D;                    // [n][vchunks] value scale codes
+  const int64_t buf_elems = (int64_t)g * D;
+  const uint8_t* bufk = st.buf + ((int64_t)u * 4 + half * 2 + 0) * buf_elems * dm.in_bytes;
+  const uint8_t* bufv = st.buf + ((int64_t)u * 4 + half * 2 + 1) * buf_elems * dm.in_bytes;
+  if (threadIdx.x == 0) { sm.abort_code = 0; sm.bad = 0; }
+  __syncthreads();
+
+  // ---- phase A: quantization -------------------------------------------
+  if (fmt != TKV_FMT_RAW) {
+    bool bad = false;
+    for (int i = threadIdx.x; i < n * D; i += blockDim.x) {
+      if (!isfinite(load_in(bufk, dm.in_dtype, i)) || !isfinite(load_in(bufv, dm.in_dtype, i))) bad = true;
+    }
+    if (bad) atomicExch(&sm.bad, 1);
+    if (fmt == TKV_FMT_FP8) {
+      double ak = 0.0, av = 0.0;
+      for (int i = threadIdx.x; i < n * D; i += blockDim.x) {
+        ak = fmax(ak, fabs(load_in(bufk, dm.in_dtype, i)));
+        av = fmax(av, fabs(load_in(bufv, dm.in_dtype, i)));
+      }
+      ak = block_max(ak, sm.red);
+      av = block_max(av, sm.red);
+      const float kf = __double2float_rn(ak / 448.0);  // fp8_tensor_scale (quant.cpp:176-178)
+      const float vf = __double2float_rn(av / 448.0);
+      for (int i = threadIdx.x; i < n * D; i += blockDim.x) {
+        bool b2 = false;
+        kc[i] = kf > 0.0f ? tkv_e4m3_encode(load_in(bufk, dm.in_dtype, i) / (double)kf, &b2) : 0;
+        vc[i] = vf > 0.0f ? tkv_e4m3_encode(load_in(bufv, dm.in_dtype, i) / (double)vf, &b2) : 0;
+        if (b2) atomicExch(&sm.bad, 1);
+      }
+      if (threadIdx.x == 0) { sm.kf = kf; sm.vf = vf; }
+    } else {
+      bool b2 = false;
+      // keys: one group per channel over the window's tokens (zero padding
+      // never changes the absmax).
+      for (int ch = threadIdx.x; ch < D; ch += blockDim.x) {
+        double am = 0.0;
+        for (int t = 0; t < n; ++t) am = fmax(am, fabs(load_in(bufk, dm.in_dtype, (int64_t)t * D + ch)));
+        uint8_t sc;
+        if (fmt == TKV_FMT_TERNARY) {
+          sc = tkv_e4m3_encode(am, &b2);                       // quant.cpp:141-158
+          const double delta = tkv_e4m3_decode(sc);
+          for (int t = 0; t < n; ++t) {
+            uint8_t code = 0;
+            if (delta > 0.0) {
+              const double r = rint(load_in(bufk, dm.in_dtype, (int64_t)t * D + ch) / delta);
+              code = tkv_ternary_bits((int)fmin(fmax(r, -1.0), 1.0));
+            }
+            kc[t * D + ch] = code;
+          }
+        } else {
+          sc = tkv_e4m3_encode(am / 6.0, &b2);                 // quant.cpp:160-174
+          const double s = tkv_e4m3_decode(sc);
+          for (int t = 0; t < n; ++t)
+            kc[t * D + ch] = s > 0.0 ? tkv_nvfp4_encode(load_in(bufk, dm.in_dtype, (int64_t)t * D + ch) / s) : 0;
+        }
+        ksc[ch] = sc;
+      }
+      // values: per token, chunks of g consecutive channels.
+      const int vch = dm.vchunks;
+      for (int it = threadIdx.x; it < n * vch; it += blockDim.x) {
+        const int t = it / vch, j = it % vch;
+        const int base = j * g, len = min(g, D - base);
+        double am = 0.0;
+        for (int q = 0; q < len; ++q) am = fmax(am, fabs(load_in(bufv, dm.in_dtype, (int64_t)t * D + base + q)));
+        uint8_t sc;
+        if (fmt == TKV_FMT_TERNARY) {
+          sc = tkv_e4m3_encode(am, &b2);
+          const double delta = tkv_e4m3_decode(sc);
+          for (int q = 0; q < len; ++q) {
+            uint8_t code = 0;
+            if (delta > 0.0) {
+              const double r = rint(load_in(bufv, dm.in_dtype, (int64_t)t * D + base + q) / delta);
+              code = tkv_ternary_bits((int)fmin(fmax(r, -1.0), 1.0));
+            }
+            vc[t * D + base + q] = code;
+          }
+        } else {
+          sc = tkv_e4m3_encode(am / 6.0, &b2);
+          const double s = tkv_e4m3_decode(sc);
+          for (int q = 0; q < len; ++q)
+            vc[t * D + base + q] =
+                s > 0.0 ? tkv_nvfp4_encode(load_in(bufv, dm.in_dtype, (int64_t)t * D + base + q) / s) : 0;
+        }
+        vsc[t * vch + j] = sc;
+      }
+      if (b2) atomicExch(&sm.bad, 1);
+    }
+  }
+  __syncthreads();
+
+  // ---- phase B: ordered claim + block-table bookkeeping (one thread) -----
+  if (threadIdx.x == 0) {
+    int* err = st.err + u;
+    if (sm.bad) {
+      sm.abort_code = TKV_E_STRUCTURAL;
+    } else if (*err != 0) {
+      sm.abort_code = *err;  // sticky: a failed unit stops mutating
+    }
+    int8_t* th = st.blk_thought + (int64_t)u * P;
+    uint8_t* fl = st.blk_filled + (int64_t)u * P;
+    uint32_t* ev = st.blk_evict + (int64_t)u * P;
+    uint8_t* ns = st.blk_nstart + (int64_t)u * P;
+    int32_t* sstart = st.blk_start + (int64_t)u * P * (bs + 1);
+    uint32_t* smask = st.blk_segmask + (int64_t)u * P * bs;
+    int claims = 0;
+    if (sm.abort_code == 0) {
+      // (1) soft-evicted slots of same-thought blocks, physical order.
+      for (int b = 0; b < P && claims < n; ++b) {
+        if (th[b] != c.band) continue;
+        uint32_t m = ev[b] & (fl[b] >= 32 ? 0xffffffffu : ((1u << fl[b]) - 1u));
+        while (m && claims < n) {
+          const int s = __ffs(m) - 1;
+          m &= m - 1;
+          sm.claim[claims] = b * bs + s;
+          sm.reuse[claims] = 1;
+          ++claims;
+        }
+      }
+      // (2) unfilled tail slots of same-thought blocks.
+      for (int b = 0; b < P && claims < n; ++b) {
+        if (th[b] != c.band) continue;
+        for (int s = fl[b]; s < bs && claims < n; ++s) {
+          sm.claim[claims] = b * bs + s;
+          sm.reuse[claims] = 0;
+          ++claims;
+        }
+      }
+      // (3) fresh blocks, lowest free id first; capacity checked up front.
+      const int remaining = n - claims;
+      const int fresh = (remaining + bs - 1) / bs;
+      if (fresh > st.unit_nfree[u]) {
+        sm.abort_code = TKV_E_OOM;
+      } else {
+        for (int b = 0, got = 0; b < P && got < fresh; ++b) {
+          if (th[b] != -1) continue;
+          th[b] = (int8_t)c.band;  // allocate_block (pager.cpp:28-47)
+          fl[b] = 0;
+          ev[b] = 0;
+          ns[b] = 0;
+          ++got;
+          for (int s = 0; s < bs && claims < n; ++s) {
+            sm.claim[claims] = b * bs + s;
+            sm.reuse[claims] = 0;
+            ++claims;
+          }
+        }
+        st.unit_nfree[u] -= fresh;
+      }
+    }
+    if (sm.abort_code != 0) {
+      *err = sm.abort_code;
+    } else {
+      int w = -1;
+      if (fmt != TKV_FMT_RAW) {
+        const int nf = st.win_nfree[u];
+        if (nf <= 0) {
+          sm.abort_code = TKV_E_INTEGRITY;
+          *err = TKV_E_INTEGRITY;
+        } else {
+          w = st.win_free[(int64_t)u * dm.NW + nf - 1];
+          st.win_nfree[u] = nf - 1;
+        }
+      }
+      sm.win = w;
+      for (int i = 0; i < n && sm.abort_code == 0; ++i) {
+        const int b = sm.claim[i] / bs, s = sm.claim[i] % bs;
+        const uint32_t bit = 1u << s;
+        int32_t* starts = sstart + (int64_t)b * (bs + 1);
+        uint32_t* masks = smask + (int64_t)b * bs;
+        if (sm.reuse[i]) {
+          ev[b] &= ~bit;
+          for (int k = 0; k + 1 < ns[b]; ++k) masks[k] &= ~bit;
+        } else {
+          fl[b] += 1;
+        }
+        // Segment bookkeeping: first segment implicit, later ones carry masks.
+        int found = -1;
+        for (int k = 0; k < ns[b]; ++k)
+          if (starts[k] == c.seg_start) { found = k; break; }
+        if (found < 0) {
+          starts[ns[b]] = c.seg_start;
+          if (ns[b] > 0) masks[ns[b] - 1] = bit;
+          ns[b] += 1;
+        } else if (found > 0) {
+          masks[found - 1] |= bit;
+        }
+        // Prune later segments whose masks emptied after reuse.
+        for (int k = ns[b] - 2; k >= 0; --k) {
+          if (masks[k] != 0) continue;
+          for (int j = k; j + 1 < ns[b] - 1; ++j) masks[j] = masks[j + 1];
+          for (int j = k + 1; j + 1 < ns[b]; ++j) starts[j] = starts[j + 1];
+          ns[b] -= 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (sm.abort_code != 0) return;
+
+  // ---- phase C: slot payload stores ----------------------------------------
+  const int w = sm.win;
+  const int vch = dm.vchunks;
+  const int ks = dm.kstride;
+  for (int i = 0; i < n; ++i) {
+    const int64_t slot = (int64_t)u * dm.NS + sm.claim[i];
+    uint8_t* kd = st.slot_k + slot * ks;
+    uint8_t* vd = st.slot_v + slot * ks;
+    if (fmt == TKV_FMT_RAW) {
+      const int64_t bytes = (int64_t)D * dm.in_bytes;
+      for (int64_t q = threadIdx.x; q < bytes; q += blockDim.x) {
+        kd[q] = bufk[(int64_t)i * bytes + q];
+        vd[q] = bufv[(int64_t)i * bytes + q];
+      }
+    } else {
+      for (int q = threadIdx.x; q < kbytes; q += blockDim.x) {
+        uint32_t kb = 0, vb = 0;
+        if (fmt == TKV_FMT_TERNARY) {
+          for (int e = 0; e < 4; ++e) {
+            const int ch = q * 4 + e;
+            if (ch < D) { kb |= (uint32_t)kc[i * D + ch] << (2 * e); vb |= (uint32_t)vc[i * D + ch] << (2 * e); }
+          }
+        } else if (fmt == TKV_FMT_NVFP4) {
+          for (int e = 0; e < 2; ++e) {
+            const int ch = q * 2 + e;
+            if (ch < D) { kb |= (uint32_t)kc[i * D + ch] << (4 * e); vb |= (uint32_t)vc[i * D + ch] << (4 * e); }
+          }
+        } else {
+          kb = kc[i * D + q];
+          vb = vc[i * D + q];
+        }
+        kd[q] = (uint8_t)kb;
+        vd[q] = (uint8_t)vb;
+      }
+      if (fmt != TKV_FMT_FP8)
+        for (int j = threadIdx.x; j < vch; j += blockDim.x) st.slot_vs[slot * vch + j] = vsc[i * vch + j];
+    }
+    if (threadIdx.x == 0) {
+      st.slot_win[slot] = w;
+      st.slot_id[slot] = pos0 + i;
+      st.tok_slot[(int64_t)u * dm.T + pos0 + i] = sm.claim[i];
+    }
+  }
+  if (w >= 0) {
+    const int64_t wi = (int64_t)u * dm.NW + w;
+    if (fmt == TKV_FMT_FP8) {
+      if (threadIdx.x == 0) { st.win_kf[wi] = sm.kf; st.win_vf[wi] = sm.vf; }
+    } else {
+      for (int ch = threadIdx.x; ch < D; ch += blockDim.x) st.win_ks[wi * D + ch] = ksc[ch];
+    }
+    if (threadIdx.x == 0) st.win_refs[wi] = n;
+  }
+}
+
+}  // namespace
+
+cudaError_t tkv_launch_flush(const TkvState& st, int half, int n, int pos0, const TkvFlushCtl* ctl,
+                             int units_per_group, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = (size_t)64 * st.dm.D * 2 + st.dm.D + (size_t)64 * st.dm.vchunks;
+  flush_kernel<<<st.dm.U, 128, smem, stream>>>(st, half, n, pos0, ctl, units_per_group);
+  return cudaGetLastError();
+}

@@ -1,0 +1,1218 @@
+// Host control plane + C ABI (include/thinkv_b200.h).
+//
+// The reference's per-step driver ThinkvMethod (proj/src/sim.cpp:494-958)
+// mixes three kinds of work.  Here they are split by where they belong:
+//   * schedule arithmetic that depends only on segment *sizes* (refresh
+//     boundaries, emission points, transition/overflow victim choice and
+//     retention targets -- evictor.cpp:348-433) is identical for every unit of
+//     a sequence, because all units share the sequence's thought labels
+//     (sim.cpp:717-722) and sizes evolve deterministically
+//     (target = min(size, R_level)).  The host runs it once per sequence.
+//   * everything that depends on cache *contents* -- codes, scales, slot
+//     placement, K-means medoids, soft-eviction masks, block release,
+//     attention -- runs on the GPU, one CTA per unit, in stream order.
+//   * reporting (events, dumps, metrics) is reconstructed on demand from
+//     device state plus the host's op records.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "json.hpp"
+#include "../../include/thinkv_b200.h"
+#include "synth.h"
+#include "tkv_kernels.h"
+#include "tkv_state.h"
+
+using nlohmann::json;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct TkvError : std::runtime_error {
+  int code;
+  TkvError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_OK(expr)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw TkvError(TKV_ERR_UNEXPECTED, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                             " at " #expr);                                   \
+  } while (0)
+
+int fail(const TkvError& e) {
+  g_last_error = e.what();
+  return e.code;
+}
+
+// Thought taxonomy helpers (proj/src/common.cpp:13-61).
+std::string thought_name(int band, int num_thoughts) {
+  if (num_thoughts == 3) {
+    if (band == 0) return "E";
+    if (band == 1) return "R";
+    if (band == 2) return "T";
+  }
+  return "B" + std::to_string(band);
+}
+int importance(int band, int num_thoughts) {
+  if (num_thoughts == 3) return band == 0 ? 1 : (band == 1 ? 2 : 0);
+  return num_thoughts - 1 - band;
+}
+bool is_transition(int band, int num_thoughts) { return num_thoughts >= 3 && band == num_thoughts - 1; }
+int prefill_band(int num_thoughts) { return num_thoughts == 3 ? 1 : 0; }
+const char* format_name(int fmt) {
+  switch (fmt) {
+    case TKV_FMT_TERNARY: return "TERNARY2";
+    case TKV_FMT_NVFP4: return "NVFP4";
+    case TKV_FMT_FP8: return "FP8E4M3";
+    default: return "RAW16";
+  }
+}
+
+struct HSeg {
+  int id = 0;
+  int band = 0;
+  int64_t start = 0;
+  int64_t size = 0;
+  int level = 0;
+  bool open = false;
+  int64_t initial = 0;
+  int dev = 0;
+};
+
+struct EvSeg {
+  int seg_id;
+  int64_t seg_start;
+  int64_t retained;
+  std::vector<int64_t> log_offs;  // one per op on this segment in this call
+};
+
+struct EventRec {
+  int kind = 0;  // 0 emit, 1 evict, 2 refresh
+  int64_t step = 0;
+  // emit
+  int fmt = 0, tokens = 0, pad = 0;
+  // evict
+  int trigger = 0;  // 0 transition_end, 1 budget_overflow
+  bool infeasible = false;
+  std::vector<EvSeg> segs;
+  int64_t after = 0, evicted = 0;
+  // refresh
+  int64_t dstep = 0;
+  double sparsity = 0.0;
+  int band = 0;
+};
+
+struct Group {
+  int seq = 0, unit0 = 0, nunits = 0;
+  std::vector<HSeg> segs;
+  int open = -1;
+  int next_seg_id = 0;
+  int64_t total = 0;
+  std::vector<EventRec> events;
+  int64_t eviction_steps = 0, transition_calls = 0, overflow_calls = 0, infeasible_events = 0;
+  std::map<std::string, int64_t> gen_by_thought;
+  json step_dumps = json::object();
+};
+
+// One anneal of one segment of one group (identical across its units).
+struct PlanOp {
+  int seg_idx;
+  int64_t m, K;
+};
+struct GroupPlan {
+  int group;
+  int trigger;
+  bool infeasible = false;
+  std::vector<PlanOp> ops;
+};
+
+}  // namespace
+
+struct tkv_ctx {
+  int device = 0;
+};
+
+struct tkv_run {
+  tkv_ctx* ctx = nullptr;
+  tkv_run_desc desc{};
+  std::vector<int32_t> script;
+  std::set<int64_t> dump_at;
+  std::vector<int64_t> levels;
+  TkvState st{};
+  cudaStream_t stream = nullptr;
+  std::vector<Group> groups;
+  int64_t pos = 0;
+  int cur_half = 0;
+  int buf_len = 0;
+  int64_t buf_pos0 = 0;
+  int64_t total_steps = 0;
+  bool finished = false;
+  // device arenas
+  uint8_t* d_arena = nullptr;
+  size_t arena_cap = 0, arena_used = 0;
+  uint8_t* h_pinned[2] = {nullptr, nullptr};
+  cudaEvent_t pinned_ev[2]{};
+  int phase = 0;
+  uint32_t* d_log = nullptr;
+  int64_t log_cap = 0, log_used = 0;
+  double* d_scratch = nullptr;
+  int scratch_ctas = 0;
+  int64_t scratch_per_cta = 0;
+  int max_m = 0;
+  TkvFlushCtl* d_ctl = nullptr;
+  std::vector<double> last_sparsity;
+  std::vector<std::vector<double>> refresh_sparsity;  // per refresh (record mode)
+  std::vector<json> metrics;
+  // host-pointer step staging
+  void* d_q = nullptr;
+  void* d_k = nullptr;
+  void* d_v = nullptr;
+  float* d_out = nullptr;
+  std::vector<void*> allocations;
+};
+
+namespace {
+
+template <typename T>
+T* dalloc(tkv_run* r, size_t n, int fill = -2) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CUDA_OK(cudaMalloc(&p, n * sizeof(T)));
+  r->allocations.push_back(p);
+  if (fill != -2) CUDA_OK(cudaMemsetAsync(p, fill, n * sizeof(T), r->stream));
+  return static_cast<T*>(p);
+}
+
+int fmt_for_bits(int bits) {
+  switch (bits) {
+    case 2: return TKV_FMT_TERNARY;
+    case 4: return TKV_FMT_NVFP4;
+    case 8: return TKV_FMT_FP8;
+    case 16: return TKV_FMT_RAW;
+  }
+  throw TkvError(TKV_ERR_CONFIG, "unsupported precision " + std::to_string(bits) + " bits");
+}
+
+int64_t effective_pool(const tkv_run_desc& d) {  // SimConfig::effective_pool_blocks (sim.cpp:65-78)
+  if (d.pool_blocks > 0) return d.pool_blocks;
+  const int64_t segments = (d.prompt_len + d.max_gen_len + d.tau - 1) / d.tau;
+  const int64_t floor = d.num_levels > 0 ? d.levels[d.num_levels - 1] : 1;
+  const int64_t closed = std::max<int64_t>(d.budget, segments * floor);
+  const int64_t resident = closed + d.tau + d.group_size + d.prompt_len;
+  return std::max<int64_t>(1, (2 * resident + d.block_size - 1) / d.block_size);
+}
+
+void validate(const tkv_run_desc& d) {
+  std::vector<std::string> errs;  // SimConfig::validate (sim.cpp:84-133) + device limits
+  if (d.num_seqs < 1 || d.units_per_seq < 1) errs.push_back("num_seqs and units_per_seq must be >= 1");
+  if (d.num_q_heads < 1 || d.num_q_heads > TKV_MAX_G) errs.push_back("num_q_heads must lie in [1, 16]");
+  if (d.head_dim < 1 || d.head_dim > 256) errs.push_back("head_dim must lie in [1, 256]");
+  if (d.num_thoughts < 1 || d.num_thoughts > TKV_MAX_BANDS) errs.push_back("num_thoughts must lie in [1, 8]");
+  if (d.tau < 1 || d.tau > 256) errs.push_back("tau must lie in [1, 256]");
+  if (d.group_size < 1 || d.group_size > 64) errs.push_back("group_size must lie in [1, 64]");
+  if (d.block_size < 1 || d.block_size > 32) errs.push_back("block_size must lie in [1, 32]");
+  if (d.max_gen_len < 1) errs.push_back("max_gen_len must be >= 1");
+  if (d.prompt_len < 0) errs.push_back("prompt_len must be >= 0");
+  if (d.pool_blocks < 0) errs.push_back("pool_blocks must be >= 0");
+  if (!(d.threshold_fraction > 0.0) || d.threshold_fraction > 1.0)
+    errs.push_back("threshold_fraction must lie in (0, 1]");
+  if (d.num_levels < 1 || d.num_levels > 16) {
+    errs.push_back("retention schedule must not be empty");
+  } else {
+    for (int i = 0; i < d.num_levels; ++i) {
+      if (d.levels[i] <= 0) errs.push_back("retention levels must be positive");
+      if (i > 0 && d.levels[i] >= d.levels[i - 1]) errs.push_back("retention levels must be strictly descending");
+    }
+    if (errs.empty() && d.budget < d.num_thoughts * d.levels[d.num_levels - 1])
+      errs.push_back("budget must be >= num_thoughts * retention floor");
+  }
+  if (d.per_layer_thought) errs.push_back("per_layer_thought is not supported by this version");
+  if (d.scripted) {
+    if (d.script_len < 1 || !d.script_bands) errs.push_back("scripted trace has no labels");
+    else
+      for (int64_t i = 0; i < (int64_t)d.num_seqs * d.script_len; ++i)
+        if (d.script_bands[i] < 0 || d.script_bands[i] >= d.num_thoughts) errs.push_back("scripted band out of range");
+  } else {
+    if (d.num_thresholds != d.num_thoughts - 1) errs.push_back("calibration must carry num_thoughts - 1 thresholds");
+    if (d.num_calib_units < 1) errs.push_back("calibration layer subset is empty");
+    for (int i = 0; i < d.num_calib_units; ++i)
+      if (d.calib_units[i] < 0 || d.calib_units[i] >= d.units_per_seq)
+        errs.push_back("calibration layer index out of range");
+  }
+  if (d.input_dtype < 0 || d.input_dtype > 2) errs.push_back("input_dtype must be bf16, f32 or f64");
+  if (!errs.empty()) {
+    std::string what = "invalid run config:";
+    for (const auto& e : errs) what += "\n  - " + e;
+    throw TkvError(TKV_ERR_CONFIG, what);
+  }
+  for (int b = 0; b < d.num_thoughts; ++b) fmt_for_bits(d.psi_bits[b]);
+}
+
+// -------------------------------------------------------------------------
+// uploads: pinned double buffer (by call phase) -> device arena
+// -------------------------------------------------------------------------
+void begin_phase(tkv_run* r) {
+  r->phase ^= 1;
+  CUDA_OK(cudaEventSynchronize(r->pinned_ev[r->phase]));
+  r->arena_used = 0;
+}
+void end_phase(tkv_run* r) { CUDA_OK(cudaEventRecord(r->pinned_ev[r->phase], r->stream)); }
+
+template <typename T>
+T* upload(tkv_run* r, const T* data, size_t n) {
+  const size_t bytes = std::max<size_t>(n * sizeof(T), 1);
+  const size_t off = (r->arena_used + 255) & ~size_t(255);
+  if (off + bytes > r->arena_cap) throw TkvError(TKV_ERR_UNEXPECTED, "upload arena exhausted");
+  std::memcpy(r->h_pinned[r->phase] + off, data, n * sizeof(T));
+  CUDA_OK(cudaMemcpyAsync(r->d_arena + off, r->h_pinned[r->phase] + off, bytes, cudaMemcpyHostToDevice, r->stream));
+  r->arena_used = off + bytes;
+  return reinterpret_cast<T*>(r->d_arena + off);
+}
+
+void check_launch(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw TkvError(TKV_ERR_UNEXPECTED, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// -------------------------------------------------------------------------
+// schedule arithmetic (sizes only): evictor.cpp:348-433
+// -------------------------------------------------------------------------
+int64_t anneal_size(const tkv_run* r, int level) {
+  return level < (int)r->levels.size() ? r->levels[level] : r->levels.back();
+}
+
+// anneal_one on sizes: advances the level, returns an op if tokens leave.
+void anneal_one(const tkv_run* r, Group& g, int si, GroupPlan& plan) {
+  HSeg& s = g.segs[si];
+  const int64_t target = std::min(s.size, anneal_size(r, s.level));
+  s.level += 1;
+  if (target >= s.size) return;
+  plan.ops.push_back(PlanOp{si, s.size, target});
+  g.total -= s.size - target;
+  s.size = target;
+}
+
+GroupPlan plan_transition(const tkv_run* r, Group& g, int gi, int64_t closing_start) {
+  GroupPlan p{gi, 0, false, {}};
+  for (int si = 0; si < (int)g.segs.size(); ++si) {
+    const HSeg& s = g.segs[si];
+    if (s.open || s.start >= closing_start) continue;
+    anneal_one(r, g, si, p);
+  }
+  return p;
+}
+
+GroupPlan plan_overflow(const tkv_run* r, Group& g, int gi) {
+  GroupPlan p{gi, 1, false, {}};
+  const int64_t floor = r->levels.back();
+  const int64_t budget = r->desc.budget;
+  const int nt = r->desc.num_thoughts;
+  const size_t max_passes = g.segs.size() * (r->levels.size() + 2) + 1;
+  for (size_t pass = 0; g.total > budget && pass < max_passes; ++pass) {
+    int victim = -1;
+    for (int si = 0; si < (int)g.segs.size(); ++si) {
+      const HSeg& s = g.segs[si];
+      if (s.open || s.size <= floor) continue;
+      if (victim < 0) { victim = si; continue; }
+      const int rs = importance(s.band, nt), rv = importance(g.segs[victim].band, nt);
+      if (rs < rv || (rs == rv && s.start < g.segs[victim].start)) victim = si;
+    }
+    if (victim < 0) {
+      p.infeasible = true;
+      break;
+    }
+    anneal_one(r, g, victim, p);
+  }
+  return p;
+}
+
+// Launch the K-means anneals (in waves: an op that re-anneals a segment
+// already annealed in this call waits for the previous wave) and the apply
+// kernel, and record the evict events (sim.cpp:652-671).
+void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
+  const int W = r->st.dm.W;
+  std::vector<std::vector<TkvAnnealOp>> waves;
+  std::vector<std::vector<std::pair<int, TkvAnnealOp>>> per_group(plans.size());
+  for (size_t pi = 0; pi < plans.size(); ++pi) {
+    GroupPlan& p = plans[pi];
+    Group& g = r->groups[p.group];
+    std::map<int, int> seen;
+    for (const PlanOp& o : p.ops) {
+      const int wave = seen[o.seg_idx]++;
+      const HSeg& s = g.segs[o.seg_idx];
+      TkvAnnealOp op{};
+      op.unit0 = g.unit0;
+      op.nunits = g.nunits;
+      op.seg = s.dev;
+      op.seg_start = (int32_t)s.start;
+      op.span = (int32_t)s.initial;
+      op.m = (int32_t)o.m;
+      op.K = (int32_t)o.K;
+      const int64_t need = (int64_t)g.nunits * W;
+      if (r->log_used + need > r->log_cap) throw TkvError(TKV_ERR_UNEXPECTED, "eviction log capacity exceeded");
+      op.log_off = (int32_t)r->log_used;
+      r->log_used += need;
+      if ((int)waves.size() <= wave) waves.resize(wave + 1);
+      waves[wave].push_back(op);
+      per_group[pi].push_back({o.seg_idx, op});
+    }
+  }
+  for (auto& wv : waves) {
+    std::vector<int32_t> prefix(wv.size());
+    int32_t items = 0;
+    for (size_t i = 0; i < wv.size(); ++i) { prefix[i] = items; items += wv[i].nunits; }
+    TkvAnnealOp* d_ops = upload(r, wv.data(), wv.size());
+    int32_t* d_pre = upload(r, prefix.data(), prefix.size());
+    check_launch(tkv_launch_anneal(r->st, d_ops, (int)wv.size(), d_pre, items, r->d_log, r->d_scratch,
+                                   r->scratch_ctas, r->scratch_per_cta, r->max_m, r->stream),
+                 "anneal kernel");
+  }
+  std::vector<TkvAnnealOp> aops;
+  std::vector<TkvApplyGroup> ag;
+  std::vector<int32_t> aprefix;
+  int32_t aitems = 0;
+  for (size_t pi = 0; pi < plans.size(); ++pi) {
+    if (per_group[pi].empty()) continue;
+    const Group& g = r->groups[plans[pi].group];
+    TkvApplyGroup a{g.unit0, g.nunits, (int32_t)aops.size(), 0};
+    for (auto& x : per_group[pi]) aops.push_back(x.second);
+    a.op_end = (int32_t)aops.size();
+    ag.push_back(a);
+    aprefix.push_back(aitems);
+    aitems += g.nunits;
+  }
+  if (!ag.empty()) {
+    TkvAnnealOp* d_aops = upload(r, aops.data(), aops.size());
+    TkvApplyGroup* d_ag = upload(r, ag.data(), ag.size());
+    int32_t* d_apre = upload(r, aprefix.data(), aprefix.size());
+    check_launch(tkv_launch_apply(r->st, d_aops, d_ag, (int)ag.size(), d_apre, aitems, r->d_log, r->stream),
+                 "apply kernel");
+  }
+  // events
+  for (size_t pi = 0; pi < plans.size(); ++pi) {
+    GroupPlan& p = plans[pi];
+    Group& g = r->groups[p.group];
+    if (p.ops.empty() && !p.infeasible) continue;
+    EventRec ev;
+    ev.kind = 1;
+    ev.step = step;
+    ev.trigger = p.trigger;
+    ev.infeasible = p.infeasible;
+    for (auto& x : per_group[pi]) {
+      const HSeg& s = g.segs[x.first];
+      auto it = std::find_if(ev.segs.begin(), ev.segs.end(), [&](const EvSeg& e) { return e.seg_id == s.id; });
+      if (it == ev.segs.end()) {
+        ev.segs.push_back(EvSeg{s.id, s.start, s.size, {}});
+        it = ev.segs.end() - 1;
+      }
+      it->log_offs.push_back(x.second.log_off);
+      it->retained = s.size;
+      ev.evicted += x.second.m - x.second.K;
+    }
+    ev.after = g.total;
+    if (r->desc.record_events) g.events.push_back(std::move(ev));
+  }
+}
+
+// -------------------------------------------------------------------------
+// emission (flush_layer, sim.cpp:565-650) for every unit
+// -------------------------------------------------------------------------
+void flush_all(tkv_run* r, int64_t step) {
+  if (r->buf_len <= 0) return;
+  std::vector<TkvFlushCtl> ctl(r->groups.size());
+  for (size_t gi = 0; gi < r->groups.size(); ++gi) {
+    const Group& g = r->groups[gi];
+    const HSeg& s = g.segs[g.open];
+    ctl[gi].band = s.band;
+    ctl[gi].seg_start = (int32_t)s.start;
+  }
+  TkvFlushCtl* d_ctl = upload(r, ctl.data(), ctl.size());
+  check_launch(tkv_launch_flush(r->st, r->cur_half, r->buf_len, (int)r->buf_pos0, d_ctl, r->desc.units_per_seq,
+                                r->stream),
+               "flush kernel");
+  if (r->desc.record_events) {
+    for (size_t gi = 0; gi < r->groups.size(); ++gi) {
+      Group& g = r->groups[gi];
+      EventRec ev;
+      ev.kind = 0;
+      ev.step = step;
+      ev.fmt = r->st.dm.band_fmt[g.segs[g.open].band];
+      ev.tokens = r->buf_len;
+      ev.pad = r->desc.group_size - r->buf_len;
+      g.events.push_back(ev);
+    }
+  }
+  r->cur_half ^= 1;
+  r->buf_len = 0;
+}
+
+std::vector<double> download_sparsity(tkv_run* r) {
+  std::vector<double> sp(r->st.dm.U);
+  CUDA_OK(cudaMemcpyAsync(sp.data(), r->st.sparsity, sp.size() * sizeof(double), cudaMemcpyDeviceToHost, r->stream));
+  CUDA_OK(cudaStreamSynchronize(r->stream));
+  return sp;
+}
+
+// boundary (sim.cpp:673-746)
+void boundary(tkv_run* r, int64_t pos, bool decode) {
+  const tkv_run_desc& d = r->desc;
+  flush_all(r, pos);
+  std::vector<GroupPlan> plans;
+  std::vector<bool> fired(r->groups.size(), false);
+  for (size_t gi = 0; gi < r->groups.size(); ++gi) {
+    Group& g = r->groups[gi];
+    if (g.open < 0) continue;
+    HSeg& open = g.segs[g.open];
+    open.open = false;
+    if (decode && is_transition(open.band, d.num_thoughts)) {
+      const int64_t closing = open.start;
+      plans.push_back(plan_transition(r, g, (int)gi, closing));
+      bool pred = false;
+      for (const HSeg& s : g.segs) pred = pred || s.start < closing;
+      fired[gi] = pred;
+    }
+    g.open = -1;
+  }
+  if (!plans.empty()) execute_plans(r, plans, pos);
+  for (size_t gi = 0; gi < r->groups.size(); ++gi) {
+    if (!fired[gi]) continue;
+    r->groups[gi].transition_calls += 1;
+    r->groups[gi].eviction_steps += 1;
+  }
+  // labels for the next interval
+  const int U = d.units_per_seq;
+  std::vector<double> sp;
+  const bool need_sp = decode && (!d.scripted || d.record_events);
+  if (need_sp) sp = download_sparsity(r);
+  for (size_t gi = 0; gi < r->groups.size(); ++gi) {
+    Group& g = r->groups[gi];
+    int band = prefill_band(d.num_thoughts);
+    double mean = 0.0;
+    if (decode) {
+      const int64_t dstep = pos - d.prompt_len;
+      const int64_t interval = dstep / d.tau;
+      if (d.scripted) {
+        const int64_t i = std::min<int64_t>(interval, d.script_len - 1);
+        band = r->script[(size_t)g.seq * d.script_len + i];
+        if (need_sp) {
+          for (int u = 0; u < U; ++u) mean += sp[(size_t)g.unit0 + u];
+          mean /= (double)U;
+        }
+      } else {
+        for (int i = 0; i < d.num_calib_units; ++i) mean += sp[(size_t)g.unit0 + d.calib_units[i]];
+        mean /= (double)d.num_calib_units;
+        band = 0;
+        for (int i = 0; i < d.num_thresholds; ++i)
+          if (mean > d.thresholds[i]) ++band;  // classify (thought.cpp:353-359)
+      }
+      if (d.record_events) {
+        EventRec ev;
+        ev.kind = 2;
+        ev.step = pos;
+        ev.dstep = dstep;
+        ev.sparsity = mean;
+        ev.band = band;
+        g.events.push_back(ev);
+      }
+    }
+    HSeg s;
+    s.id = g.next_seg_id++;
+    s.band = band;
+    s.start = pos;
+    s.open = true;
+    s.dev = (int)g.segs.size();
+    if (s.dev >= r->st.dm.NSEG) throw TkvError(TKV_ERR_UNEXPECTED, "segment capacity exceeded");
+    g.segs.push_back(s);
+    g.open = s.dev;
+  }
+}
+
+void overflow_pass(tkv_run* r, int64_t step, bool decode, bool final_pass) {
+  std::vector<GroupPlan> plans;
+  for (size_t gi = 0; gi < r->groups.size(); ++gi) {
+    Group& g = r->groups[gi];
+    if (g.total <= r->desc.budget) continue;
+    plans.push_back(plan_overflow(r, g, (int)gi));
+  }
+  if (plans.empty()) return;
+  execute_plans(r, plans, step);
+  for (const GroupPlan& p : plans) {
+    Group& g = r->groups[p.group];
+    // process() counts one infeasible event per step; finish() counts one per
+    // layer whose final plan is infeasible (sim.cpp:835-837 vs :879).
+    if (p.infeasible) g.infeasible_events += final_pass ? g.nunits : 1;
+    g.overflow_calls += 1;  // any_overflow / final_overflow per sequence
+    if (decode && !final_pass) g.eviction_steps += 1;
+  }
+}
+
+// -------------------------------------------------------------------------
+// dumps (device -> host) in the reference's JSON shapes
+// -------------------------------------------------------------------------
+struct UnitSnap {
+  std::vector<int8_t> th;
+  std::vector<uint8_t> fl, ns;
+  std::vector<uint32_t> ev, smask, segm;
+  std::vector<int32_t> start, sid, swin, wrefs;
+};
+
+template <typename T>
+void d2h(tkv_run* r, std::vector<T>& v, const T* src, size_t n) {
+  v.resize(n);
+  CUDA_OK(cudaMemcpyAsync(v.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost, r->stream));
+}
+
+std::vector<UnitSnap> snapshot(tkv_run* r, int u0, int n) {
+  const TkvDims& dm = r->st.dm;
+  std::vector<UnitSnap> out(n);
+  for (int i = 0; i < n; ++i) {
+    const int64_t u = u0 + i;
+    UnitSnap& s = out[i];
+    d2h(r, s.th, r->st.blk_thought + u * dm.P, dm.P);
+    d2h(r, s.fl, r->st.blk_filled + u * dm.P, dm.P);
+    d2h(r, s.ns, r->st.blk_nstart + u * dm.P, dm.P);
+    d2h(r, s.ev, r->st.blk_evict + u * dm.P, dm.P);
+    d2h(r, s.smask, r->st.blk_segmask + u * dm.P * dm.bs, (size_t)dm.P * dm.bs);
+    d2h(r, s.start, r->st.blk_start + u * dm.P * (dm.bs + 1), (size_t)dm.P * (dm.bs + 1));
+    d2h(r, s.sid, r->st.slot_id + u * dm.NS, dm.NS);
+    d2h(r, s.swin, r->st.slot_win + u * dm.NS, dm.NS);
+    d2h(r, s.wrefs, r->st.win_refs + u * dm.NW, dm.NW);
+    d2h(r, s.segm, r->st.seg_mask + u * dm.NSEG * dm.W, (size_t)dm.NSEG * dm.W);
+  }
+  CUDA_OK(cudaStreamSynchronize(r->stream));
+  return out;
+}
+
+std::string mask_string(uint32_t m, int bs) {
+  std::string s(bs, '0');
+  for (int i = 0; i < bs; ++i)
+    if ((m >> i) & 1u) s[i] = '1';
+  return s;
+}
+
+json table_json(const tkv_run* r, const UnitSnap& s) {  // BlockPager::dump (pager.cpp:327-362)
+  const TkvDims& dm = r->st.dm;
+  json j;
+  j["block_size"] = dm.bs;
+  j["pool_blocks"] = dm.P;
+  json blocks = json::array();
+  std::vector<int> free_ids;
+  for (int b = 0; b < dm.P; ++b) {
+    if (s.th[b] < 0) {
+      free_ids.push_back(b);
+      continue;
+    }
+    json e;
+    e["physical_block"] = b;
+    e["filled"] = (int)s.fl[b];
+    e["thought"] = (int)s.th[b];
+    std::vector<int64_t> starts;
+    for (int k = 0; k < s.ns[b]; ++k) starts.push_back(s.start[(size_t)b * (dm.bs + 1) + k]);
+    e["start_indices"] = starts;
+    json masks = json::array();
+    for (int k = 0; k + 1 < s.ns[b]; ++k) masks.push_back(mask_string(s.smask[(size_t)b * dm.bs + k], dm.bs));
+    e["segment_masks"] = masks;
+    e["eviction_mask"] = mask_string(s.ev[b], dm.bs);
+    json toks = json::array();
+    for (int sl = 0; sl < dm.bs; ++sl) {
+      if (sl < s.fl[b]) toks.push_back((int64_t)s.sid[(size_t)b * dm.bs + sl]);
+      else toks.push_back(nullptr);
+    }
+    e["tokens"] = toks;
+    blocks.push_back(std::move(e));
+  }
+  j["blocks"] = std::move(blocks);
+  j["free_blocks"] = free_ids;
+  return j;
+}
+
+std::vector<int64_t> members_of(const tkv_run* r, const UnitSnap& s, const HSeg& seg) {
+  std::vector<int64_t> m;
+  if (seg.open) {
+    for (int64_t i = 0; i < seg.size; ++i) m.push_back(seg.start + i);
+    return m;
+  }
+  const int W = r->st.dm.W;
+  for (int64_t b = 0; b < seg.initial; ++b)
+    if ((s.segm[(size_t)seg.dev * W + (b >> 5)] >> (b & 31)) & 1u) m.push_back(seg.start + b);
+  return m;
+}
+
+json segments_json(const tkv_run* r, const Group& g, const std::vector<UnitSnap>& snaps) {  // sim.cpp:919-937
+  json units = json::array();
+  for (int i = 0; i < g.nunits; ++i) {
+    json arr = json::array();
+    for (const HSeg& s : g.segs) {
+      const auto mem = members_of(r, snaps[i], s);
+      if ((int64_t)mem.size() != s.size)
+        throw TkvError(TKV_ERR_INTEGRITY, "device member mask disagrees with the host segment size");
+      arr.push_back(json{{"id", s.id},
+                         {"band", s.band},
+                         {"thought", thought_name(s.band, r->desc.num_thoughts)},
+                         {"start", s.start},
+                         {"anneal_level", s.level},
+                         {"open", s.open},
+                         {"initial_size", s.initial},
+                         {"size", s.size},
+                         {"members", mem}});
+    }
+    units.push_back(std::move(arr));
+  }
+  return units;
+}
+
+json tables_json(const tkv_run* r, const std::vector<UnitSnap>& snaps) {
+  json arr = json::array();
+  for (const auto& s : snaps) arr.push_back(table_json(r, s));
+  return arr;
+}
+
+void check_device_errors(tkv_run* r) {
+  CUDA_OK(cudaStreamSynchronize(r->stream));
+  std::vector<int32_t> err(r->st.dm.U);
+  CUDA_OK(cudaMemcpy(err.data(), r->st.err, err.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  for (size_t u = 0; u < err.size(); ++u) {
+    if (err[u] == 0) continue;
+    const char* what = err[u] == TKV_ERR_OOM ? "physical block pool exhausted"
+                       : err[u] == TKV_ERR_INTEGRITY ? "integrity failure (unknown token id / bookkeeping)"
+                       : err[u] == TKV_ERR_CONFIG ? "structural error (non-finite input element)"
+                                                  : "device error";
+    throw TkvError(err[u], std::string(what) + " in unit " + std::to_string(u));
+  }
+}
+
+json events_json_lines(tkv_run* r, const Group& g, std::string* out) {
+  // evicted ids come from the device log
+  std::vector<uint32_t> log;
+  if (r->log_used > 0) {
+    log.resize(r->log_used);
+    CUDA_OK(cudaMemcpy(log.data(), r->d_log, log.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  }
+  const int W = r->st.dm.W;
+  std::string s;
+  for (const EventRec& e : g.events) {
+    for (int i = 0; i < g.nunits; ++i) {
+      if (e.kind == 2) {
+        if (i > 0) break;
+        json ev{{"type", "refresh"}, {"step", e.step}, {"dstep", e.dstep}, {"sparsity", e.sparsity}, {"band", e.band}};
+        s += ev.dump() + "\n";
+        continue;
+      }
+      if (e.kind == 0) {
+        json ev{{"type", "emit"}, {"step", e.step}, {"layer", i}, {"format", format_name(e.fmt)},
+                {"tokens", e.tokens}, {"pad", e.pad}};
+        s += ev.dump() + "\n";
+        continue;
+      }
+      json segs = json::array();
+      for (const EvSeg& es : e.segs) {
+        std::vector<int64_t> ids;
+        for (int64_t off : es.log_offs)
+          for (int w = 0; w < W; ++w) {
+            uint32_t bits = log[(size_t)off + (size_t)i * W + w];
+            while (bits) {
+              const int b = __builtin_ctz(bits);
+              bits &= bits - 1;
+              ids.push_back(es.seg_start + w * 32 + b);
+            }
+          }
+        std::sort(ids.begin(), ids.end());
+        segs.push_back(json{{"segment", es.seg_id}, {"retained", es.retained}, {"evicted", ids}});
+      }
+      json ev{{"type", "evict"},
+              {"trigger", e.trigger == 0 ? "transition_end" : "budget_overflow"},
+              {"step", e.step},
+              {"layer", i},
+              {"segments", segs},
+              {"infeasible", e.infeasible},
+              {"retained_before", e.after + e.evicted},
+              {"retained_total", e.after}};
+      s += ev.dump() + "\n";
+    }
+  }
+  *out = s;
+  return json();
+}
+
+// Metrics (ThinkvMethod::finish, sim.cpp:889-957) from device state.
+json metrics_json(tkv_run* r, const Group& g, const std::vector<UnitSnap>& snaps) {
+  const TkvDims& dm = r->st.dm;
+  const tkv_run_desc& d = r->desc;
+  int64_t bits = 0, slots = 0;
+  for (const UnitSnap& s : snaps) {
+    for (int b = 0; b < dm.P; ++b) {
+      if (s.th[b] < 0) continue;
+      const int fmt = dm.band_fmt[s.th[b]];
+      const int64_t per = (int64_t)(fmt == TKV_FMT_RAW ? 16 : (fmt == TKV_FMT_TERNARY ? 2 : (fmt == TKV_FMT_NVFP4 ? 4 : 8))) * dm.D * 2;
+      for (int sl = 0; sl < s.fl[b]; ++sl)
+        if (!((s.ev[b] >> sl) & 1u)) { bits += per; slots += 1; }
+    }
+  }
+  int64_t live_prompt = 0, live_gen = 0;
+  std::map<std::string, int64_t> live_by;
+  const UnitSnap& s0 = snaps[0];
+  for (int b = 0; b < dm.P; ++b) {
+    if (s0.th[b] < 0) continue;
+    for (int sl = 0; sl < s0.fl[b]; ++sl) {
+      if ((s0.ev[b] >> sl) & 1u) continue;
+      const int64_t id = s0.sid[(size_t)b * dm.bs + sl];
+      (id < d.prompt_len ? live_prompt : live_gen) += 1;
+      live_by[thought_name(s0.th[b], d.num_thoughts)] += 1;
+    }
+  }
+  const int64_t total = d.prompt_len + d.max_gen_len;
+  json m;
+  m["method"] = "thinkv";
+  m["generated_length"] = d.max_gen_len;
+  m["prompt_length"] = d.prompt_len;
+  m["live_tokens_final"] = live_prompt + live_gen;
+  m["live_prompt_final"] = live_prompt;
+  m["live_generated_final"] = live_gen;
+  m["live_by_thought"] = live_by;
+  m["generated_by_thought"] = g.gen_by_thought;
+  const double avg = slots > 0 ? (double)bits / ((double)slots * 2.0 * dm.D) : 16.0;
+  m["avg_bits_per_token"] = avg;
+  m["a"] = avg / 16.0;
+  m["b"] = d.max_gen_len > 0 ? (double)live_gen / (double)d.max_gen_len : 1.0;
+  const double denom = (double)g.nunits * (double)total * 2.0 * dm.D * 16.0;
+  const double mf = (double)bits / denom;
+  m["memory_footprint_fraction"] = mf;
+  m["compression_ratio"] = mf > 0.0 ? 1.0 / mf : 0.0;
+  m["eviction_call_fraction"] = (double)g.eviction_steps / (double)d.max_gen_len;
+  m["recall_at_10_mean"] = 1.0;
+  m["attention_output_error_mean"] = 0.0;
+  m["recall_at_10"] = json::array();
+  m["attention_output_error"] = json::array();
+  m["eviction_steps"] = g.eviction_steps;
+  m["transition_calls"] = g.transition_calls;
+  m["overflow_calls"] = g.overflow_calls;
+  m["budget_infeasible_events"] = g.infeasible_events;
+  m["moved_token_slots"] = 0;
+  return m;
+}
+
+// the step (ThinkvMethod::process, sim.cpp:748-843)
+void do_step(tkv_run* r, const void* q, const void* k, const void* v, float* out) {
+  const tkv_run_desc& d = r->desc;
+  if (r->finished) throw TkvError(TKV_ERR_CONFIG, "run already finished");
+  if (r->pos >= r->total_steps) throw TkvError(TKV_ERR_CONFIG, "step beyond prompt_len + max_gen_len");
+  begin_phase(r);
+  if (!d.record_events) r->log_used = 0;
+  const int64_t pos = r->pos;
+  const bool decode = pos >= d.prompt_len;
+  const int64_t bstep = decode ? pos - d.prompt_len : pos;
+  const bool refresh = bstep % d.tau == 0;
+  const bool flush_first = refresh && r->buf_len > 0;
+  const int put_half = flush_first ? (r->cur_half ^ 1) : r->cur_half;
+  const int put_slot = flush_first ? 0 : r->buf_len;
+  // 1. attention (+ exact sparsity on refresh steps, where it is consumed)
+  if (refresh && decode)
+    check_launch(tkv_launch_score(r->st, q, k, r->cur_half, r->buf_len, r->stream), "score kernel");
+  check_launch(tkv_launch_attend(r->st, q, k, v, out, r->cur_half, r->buf_len, put_half, put_slot, r->stream),
+               "attend kernel");
+  // 2. refresh boundary
+  if (refresh) boundary(r, pos, decode);
+  // 3. buffer the token under the open segment
+  if (r->buf_len == 0) r->buf_pos0 = pos;
+  r->buf_len += 1;
+  for (Group& g : r->groups) {
+    HSeg& open = g.segs[g.open];
+    open.size += 1;
+    open.initial += 1;
+    g.total += 1;
+    if (decode) g.gen_by_thought[thought_name(open.band, d.num_thoughts)] += 1;
+  }
+  // 4. emission at g tokens
+  if (r->buf_len >= d.group_size) flush_all(r, pos);
+  // 5. Case-2 budget enforcement
+  overflow_pass(r, pos, decode, false);
+  end_phase(r);
+  if (r->dump_at.count(pos)) {
+    check_device_errors(r);
+    for (Group& g : r->groups) {
+      const auto snaps = snapshot(r, g.unit0, g.nunits);
+      g.step_dumps[std::to_string(pos)] = json{{"block_tables", tables_json(r, snaps)},
+                                               {"segments", segments_json(r, g, snaps)}};
+    }
+  }
+  r->pos += 1;
+}
+
+void do_finish(tkv_run* r) {
+  if (r->finished) return;
+  begin_phase(r);
+  if (!r->desc.record_events) r->log_used = 0;
+  const int64_t total = r->desc.prompt_len + r->desc.max_gen_len;
+  flush_all(r, total);
+  for (Group& g : r->groups)
+    if (g.open >= 0) g.segs[g.open].open = false;
+  overflow_pass(r, total, true, true);
+  end_phase(r);
+  check_device_errors(r);
+  r->metrics.clear();
+  for (Group& g : r->groups) {
+    const auto snaps = snapshot(r, g.unit0, g.nunits);
+    r->metrics.push_back(metrics_json(r, g, snaps));
+  }
+  r->finished = true;
+}
+
+void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
+  if (!desc) throw TkvError(TKV_ERR_CONFIG, "null run description");
+  validate(*desc);
+  if (!ctx) throw TkvError(TKV_ERR_CONFIG, "null context");
+  r->ctx = ctx;
+  r->desc = *desc;
+  const tkv_run_desc& d = r->desc;
+  if (d.scripted) r->script.assign(d.script_bands, d.script_bands + (size_t)d.num_seqs * d.script_len);
+  r->desc.script_bands = nullptr;
+  for (int i = 0; i < d.num_dump_positions; ++i) r->dump_at.insert(d.dump_positions[i]);
+  r->desc.dump_positions = nullptr;
+  r->levels.assign(d.levels, d.levels + d.num_levels);
+  r->total_steps = d.prompt_len + d.max_gen_len;
+  CUDA_OK(cudaSetDevice(ctx->device));
+  CUDA_OK(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+
+  TkvDims dm{};
+  dm.U = d.num_seqs * d.units_per_seq;
+  dm.G = d.num_q_heads;
+  dm.D = d.head_dim;
+  dm.maxpool = d.gqa_maxpool ? 1 : 0;
+  dm.bs = d.block_size;
+  const int64_t P = effective_pool(d);
+  if (P > 2048) throw TkvError(TKV_ERR_CONFIG, "pool_blocks > 2048 per unit is not supported");
+  dm.P = (int32_t)P;
+  dm.NS = dm.P * dm.bs;
+  dm.NW = dm.NS + 1;
+  dm.g = d.group_size;
+  dm.vchunks = (dm.D + dm.g - 1) / dm.g;
+  dm.in_dtype = d.input_dtype;
+  dm.in_bytes = d.input_dtype == TKV_DTYPE_BF16 ? 2 : (d.input_dtype == TKV_DTYPE_F32 ? 4 : 8);
+  int kbytes = 1;
+  dm.num_bands = d.num_thoughts;
+  for (int b = 0; b < d.num_thoughts; ++b) {
+    dm.band_fmt[b] = fmt_for_bits(d.psi_bits[b]);
+    const int bytes = dm.band_fmt[b] == TKV_FMT_RAW ? dm.D * dm.in_bytes
+                                                   : (dm.D * d.psi_bits[b] + 7) / 8;
+    dm.band_bytes[b] = bytes;
+    kbytes = std::max(kbytes, bytes);
+  }
+  dm.kstride = (kbytes + 15) / 16 * 16;
+  const int64_t T = r->total_steps;
+  if (T > (int64_t)1 << 30) throw TkvError(TKV_ERR_CONFIG, "run too long");
+  dm.T = (int32_t)T;
+  dm.W = (d.tau + 31) / 32;
+  dm.NSEG = (int32_t)((T + d.tau - 1) / d.tau + 2);
+  dm.scale = (float)(1.0 / std::sqrt((double)dm.D));
+  dm.thr_frac = d.threshold_fraction;
+  r->st.dm = dm;
+  const size_t U = dm.U;
+  TkvState& st = r->st;
+  st.blk_thought = dalloc<int8_t>(r, U * dm.P, 0xFF);
+  st.blk_filled = dalloc<uint8_t>(r, U * dm.P, 0);
+  st.blk_evict = dalloc<uint32_t>(r, U * dm.P, 0);
+  st.blk_nstart = dalloc<uint8_t>(r, U * dm.P, 0);
+  st.blk_start = dalloc<int32_t>(r, U * dm.P * (dm.bs + 1), 0);
+  st.blk_segmask = dalloc<uint32_t>(r, U * dm.P * dm.bs, 0);
+  st.unit_nfree = dalloc<int32_t>(r, U);
+  st.slot_k = dalloc<uint8_t>(r, U * dm.NS * dm.kstride, 0);
+  st.slot_v = dalloc<uint8_t>(r, U * dm.NS * dm.kstride, 0);
+  st.slot_vs = dalloc<uint8_t>(r, U * dm.NS * dm.vchunks, 0);
+  st.slot_win = dalloc<int32_t>(r, U * dm.NS, 0xFF);
+  st.slot_id = dalloc<int32_t>(r, U * dm.NS, 0xFF);
+  st.win_ks = dalloc<uint8_t>(r, U * dm.NW * dm.D, 0);
+  st.win_kf = dalloc<float>(r, U * dm.NW, 0);
+  st.win_vf = dalloc<float>(r, U * dm.NW, 0);
+  st.win_refs = dalloc<int32_t>(r, U * dm.NW, 0);
+  st.win_free = dalloc<int32_t>(r, U * dm.NW);
+  st.win_nfree = dalloc<int32_t>(r, U);
+  st.tok_slot = dalloc<int32_t>(r, U * (size_t)dm.T, 0xFF);
+  st.seg_mask = dalloc<uint32_t>(r, U * dm.NSEG * dm.W, 0xFF);
+  st.buf = dalloc<uint8_t>(r, U * 4 * (size_t)dm.g * dm.D * dm.in_bytes, 0);
+  st.sparsity = dalloc<double>(r, U);
+  st.err = dalloc<int32_t>(r, U);
+  check_launch(tkv_launch_init(st, r->stream), "init kernel");
+  // arenas
+  r->arena_cap = 8 << 20;
+  r->d_arena = dalloc<uint8_t>(r, r->arena_cap);
+  for (int i = 0; i < 2; ++i) {
+    CUDA_OK(cudaMallocHost(&r->h_pinned[i], r->arena_cap));
+    CUDA_OK(cudaEventCreateWithFlags(&r->pinned_ev[i], cudaEventDisableTiming));
+    CUDA_OK(cudaEventRecord(r->pinned_ev[i], r->stream));
+  }
+  const int64_t per_step_ops = 64;
+  const int64_t ops_bound = d.record_events ? (int64_t)dm.NSEG * (d.num_levels + 1) + 16 : per_step_ops;
+  r->log_cap = ops_bound * (int64_t)U * dm.W;
+  r->d_log = dalloc<uint32_t>(r, r->log_cap, 0);
+  r->max_m = std::max<int>(d.tau, 1);
+  r->scratch_per_cta = (int64_t)6 * r->max_m * dm.D;
+  r->scratch_ctas = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, U));
+  r->d_scratch = dalloc<double>(r, (size_t)r->scratch_ctas * r->scratch_per_cta);
+  // groups = sequences
+  for (int s = 0; s < d.num_seqs; ++s) {
+    Group g;
+    g.seq = s;
+    g.unit0 = s * d.units_per_seq;
+    g.nunits = d.units_per_seq;
+    r->groups.push_back(std::move(g));
+  }
+  CUDA_OK(cudaStreamSynchronize(r->stream));
+}
+
+void destroy_run(tkv_run* r) {
+  if (r->stream) cudaStreamSynchronize(r->stream);
+  for (void* p : r->allocations) cudaFree(p);
+  for (int i = 0; i < 2; ++i) {
+    if (r->h_pinned[i]) cudaFreeHost(r->h_pinned[i]);
+    if (r->pinned_ev[i]) cudaEventDestroy(r->pinned_ev[i]);
+  }
+  if (r->stream) cudaStreamDestroy(r->stream);
+}
+
+int64_t live_bytes_stats(tkv_run* r, tkv_bytes_t* out) {
+  const TkvDims& dm = r->st.dm;
+  std::memset(out, 0, sizeof(*out));
+  const size_t U = dm.U;
+  std::vector<int8_t> th;
+  std::vector<uint8_t> fl;
+  std::vector<uint32_t> ev;
+  std::vector<int32_t> swin;
+  d2h(r, th, r->st.blk_thought, U * dm.P);
+  d2h(r, fl, r->st.blk_filled, U * dm.P);
+  d2h(r, ev, r->st.blk_evict, U * dm.P);
+  d2h(r, swin, r->st.slot_win, U * dm.NS);
+  CUDA_OK(cudaStreamSynchronize(r->stream));
+  std::vector<uint8_t> win_seen;
+  for (size_t u = 0; u < U; ++u) {
+    win_seen.assign(dm.NW, 0);
+    for (int b = 0; b < dm.P; ++b) {
+      const int t = th[u * dm.P + b];
+      out->meta_bytes += 6;  // thought, filled, evict mask
+      if (t < 0) continue;
+      const int fmt = dm.band_fmt[t];
+      for (int s = 0; s < fl[u * dm.P + b]; ++s) {
+        out->resident_slots += 1;
+        if ((ev[u * dm.P + b] >> s) & 1u) continue;
+        out->live_slots += 1;
+        out->live_code_bytes += 2 * (int64_t)dm.band_bytes[t];
+        out->meta_bytes += 8;  // slot -> window index + live-list entry
+        if (fmt == TKV_FMT_RAW) continue;
+        const int w = swin[u * dm.NS + (size_t)b * dm.bs + s];
+        if (fmt == TKV_FMT_FP8) {
+          if (w >= 0 && !win_seen[w]) { win_seen[w] = 1; out->live_scale_bytes += 8; }
+        } else {
+          out->live_scale_bytes += dm.vchunks;  // per-token value-chunk scales
+          if (w >= 0 && !win_seen[w]) { win_seen[w] = 1; out->live_scale_bytes += dm.D; }
+        }
+      }
+    }
+  }
+  out->buffer_bytes = (int64_t)U * (r->buf_len + 1) * 2 * dm.D * dm.in_bytes;
+  const int rows = dm.maxpool ? 1 : dm.G;
+  out->qo_bytes = (int64_t)U * ((int64_t)dm.G * dm.D * dm.in_bytes + (int64_t)rows * dm.D * 4);
+  out->algorithmic_bytes = out->live_code_bytes + out->live_scale_bytes + out->buffer_bytes + out->qo_bytes +
+                           out->meta_bytes;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tkv_last_error(void) { return g_last_error.c_str(); }
+int tkv_abi_version(void) { return TKV_ABI_VERSION; }
+
+int tkv_init(int device, tkv_ctx** out) {
+  try {
+    int n = 0;
+    CUDA_OK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw TkvError(TKV_ERR_CONFIG, "no such CUDA device");
+    cudaDeviceProp prop{};
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) throw TkvError(TKV_ERR_CONFIG, "this build targets sm_100a (B200)");
+    CUDA_OK(cudaSetDevice(device));
+    *out = new tkv_ctx{device};
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  }
+}
+
+int tkv_ctx_destroy(tkv_ctx* ctx) {
+  delete ctx;
+  return TKV_OK;
+}
+
+int tkv_run_create(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run** out) {
+  auto r = std::make_unique<tkv_run>();
+  try {
+    create_run(ctx, desc, r.get());
+    *out = r.release();
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    destroy_run(r.get());
+    return fail(e);
+  } catch (const std::exception& e) {
+    destroy_run(r.get());
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_run_destroy(tkv_run* run) {
+  if (!run) return TKV_OK;
+  destroy_run(run);
+  delete run;
+  return TKV_OK;
+}
+
+int tkv_step(tkv_run* run, const void* q, const void* k, const void* v, float* out, void* stream) {
+  try {
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaEvent_t ev = nullptr;
+    if (user && user != run->stream) {  // order the run's stream after the caller's
+      CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CUDA_OK(cudaEventRecord(ev, user));
+      CUDA_OK(cudaStreamWaitEvent(run->stream, ev, 0));
+    }
+    do_step(run, q, k, v, out);
+    if (ev) {
+      CUDA_OK(cudaEventRecord(ev, run->stream));
+      CUDA_OK(cudaStreamWaitEvent(user, ev, 0));
+      CUDA_OK(cudaEventDestroy(ev));
+    }
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_step_host(tkv_run* run, const void* q, const void* k, const void* v, float* out) {
+  try {
+    const TkvDims& dm = run->st.dm;
+    const size_t qb = (size_t)dm.U * dm.G * dm.D * dm.in_bytes, kb = (size_t)dm.U * dm.D * dm.in_bytes;
+    const size_t ob = (size_t)dm.U * (dm.maxpool ? 1 : dm.G) * dm.D * sizeof(float);
+    if (!run->d_q) {
+      run->d_q = dalloc<uint8_t>(run, qb);
+      run->d_k = dalloc<uint8_t>(run, kb);
+      run->d_v = dalloc<uint8_t>(run, kb);
+      run->d_out = dalloc<float>(run, ob / sizeof(float));
+    }
+    CUDA_OK(cudaMemcpyAsync(run->d_q, q, qb, cudaMemcpyHostToDevice, run->stream));
+    CUDA_OK(cudaMemcpyAsync(run->d_k, k, kb, cudaMemcpyHostToDevice, run->stream));
+    CUDA_OK(cudaMemcpyAsync(run->d_v, v, kb, cudaMemcpyHostToDevice, run->stream));
+    do_step(run, run->d_q, run->d_k, run->d_v, run->d_out);
+    CUDA_OK(cudaMemcpyAsync(out, run->d_out, ob, cudaMemcpyDeviceToHost, run->stream));
+    CUDA_OK(cudaStreamSynchronize(run->stream));
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_finish(tkv_run* run) {
+  try {
+    do_finish(run);
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_synchronize(tkv_run* run) {
+  try {
+    check_device_errors(run);
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  }
+}
+
+int64_t tkv_position(const tkv_run* run) { return run->pos; }
+
+int tkv_dump_json(tkv_run* run, int seq, const char* what, char* buf, size_t cap, size_t* needed) {
+  try {
+    if (seq < 0 || seq >= (int)run->groups.size()) throw TkvError(TKV_ERR_CONFIG, "no such sequence");
+    check_device_errors(run);
+    const std::string w(what);
+    Group& g = run->groups[seq];
+    std::string s;
+    if (w == "tables") {
+      s = tables_json(run, snapshot(run, g.unit0, g.nunits)).dump();
+    } else if (w == "segments") {
+      s = segments_json(run, g, snapshot(run, g.unit0, g.nunits)).dump();
+    } else if (w == "events") {
+      if (!run->desc.record_events) throw TkvError(TKV_ERR_CONFIG, "run was created without record_events");
+      events_json_lines(run, g, &s);
+    } else if (w == "metrics") {
+      if (!run->finished) throw TkvError(TKV_ERR_CONFIG, "metrics are available after tkv_finish");
+      s = run->metrics.at(seq).dump();
+    } else if (w == "step_dumps") {
+      s = g.step_dumps.dump();
+    } else {
+      throw TkvError(TKV_ERR_CONFIG, "unknown dump '" + w + "'");
+    }
+    if (needed) *needed = s.size() + 1;
+    if (buf && cap > 0) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_bytes(tkv_run* run, tkv_bytes_t* out) {
+  try {
+    live_bytes_stats(run, out);
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  }
+}
+
+int tkv_unit_sparsity(tkv_run* run, double* out, int64_t n) {
+  try {
+    const auto sp = download_sparsity(run);
+    std::memcpy(out, sp.data(), std::min<int64_t>(n, (int64_t)sp.size()) * sizeof(double));
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  }
+}
+
+int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t step, void* q, void* k, void* v, void* stream) {
+  try {
+    const TkvDims& dm = run->st.dm;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : run->stream;
+    check_launch(tkv_launch_synth(seed, run->desc.units_per_seq, run->desc.tau, 4, 0, dm.U, dm.G, dm.D, step,
+                                  static_cast<uint16_t*>(q), static_cast<uint16_t*>(k), static_cast<uint16_t*>(v), s),
+                 "synth kernel");
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  }
+}
+
+}  // extern "C"

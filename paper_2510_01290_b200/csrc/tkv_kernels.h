@@ -1,0 +1,45 @@
+// Host-side launchers for the sm_100a kernels (implemented in k_*.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tkv_state.h"
+
+// K1: paged mixed-precision decode attention over every unit's live slots,
+// its fp buffer (first nbuf tokens of half buf_half) and the current token.
+// Also stores the current k/v into buffer (put_half, put_slot) when put_slot >= 0.
+cudaError_t tkv_launch_attend(const TkvState& st, const void* q, const void* k, const void* v,
+                              float* out, int buf_half, int nbuf, int put_half, int put_slot,
+                              cudaStream_t stream);
+
+// K3a: fp64 sparsity statistics (layer_sparsity_average) over the same view.
+cudaError_t tkv_launch_score(const TkvState& st, const void* q, const void* k, int buf_half,
+                             int nbuf, cudaStream_t stream);
+
+// K2: quantize the n buffered tokens of half `half` (token ids pos0..pos0+n-1)
+// and place them; ctl is indexed by group = unit / units_per_group.
+cudaError_t tkv_launch_flush(const TkvState& st, int half, int n, int pos0, const TkvFlushCtl* ctl,
+                             int units_per_group, cudaStream_t stream);
+
+// K3d: K-means medoid anneals.  ops[nops] with item prefix sums over units;
+// evicted masks are logged at log + op.log_off + unit_rel * W.
+cudaError_t tkv_launch_anneal(const TkvState& st, const TkvAnnealOp* ops, int nops,
+                              const int32_t* item_prefix, int nitems, uint32_t* log,
+                              double* scratch, int scratch_ctas, int64_t scratch_doubles_per_cta,
+                              int max_m, cudaStream_t stream);
+
+// K3e: apply the evictions of ops[0..nops) (soft-mask slots, release window
+// references, free empty blocks).  One CTA per unit of the listed groups.
+cudaError_t tkv_launch_apply(const TkvState& st, const TkvAnnealOp* ops,
+                             const TkvApplyGroup* groups, int ngroups,
+                             const int32_t* unit_prefix, int nitems, const uint32_t* log,
+                             cudaStream_t stream);
+
+// Synthetic decode inputs (bf16) generated on device with the same integer
+// generator as the host oracle (synth.h).
+cudaError_t tkv_launch_synth(uint64_t seed, int units_per_seq, int tau, int sink_tokens, int64_t unit0,
+                             int units, int G, int D, int64_t step, uint16_t* q, uint16_t* k,
+                             uint16_t* v, cudaStream_t stream);
+
+// One-time state initialisation (window free stacks, free-block counts).
+cudaError_t tkv_launch_init(const TkvState& st, cudaStream_t stream);

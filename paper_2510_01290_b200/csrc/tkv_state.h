@@ -1,0 +1,116 @@
+// Device-resident cache state for the ThinKV decode path (one struct of raw
+// device pointers, passed by value to every kernel).
+//
+// A *unit* is one (sequence, layer, kv-head) triple -- one reference
+// "layer" (proj/src/sim.cpp:496-508 gives every layer its own BlockPager,
+// segment list and buffer).  All per-unit arrays are unit-major so a CTA that
+// owns a unit touches one contiguous region per array.
+//
+// HBM layout (SoA; P = pool blocks per unit, bs = block size, NS = P*bs):
+//   block table   thought[P] i8, filled[P] u8, evict[P] u32 (slot bitmask),
+//                 nstart[P] u8, start[P][bs+1] i32, segmask[P][bs] u32
+//                 -- BlockTableEntry (pager.hpp:55-62) with the segment masks
+//                 stored as bitmasks, one per start index beyond the first.
+//   slots         kcode[NS][kstride] u8, vcode[NS][vstride] u8 (packed 2/4/8-bit
+//                 codes, or raw input-dtype values for 16-bit passthrough),
+//                 vscale[NS][vchunks] u8 (E4M3 per-token value-chunk scales),
+//                 win[NS] i32 (window -> key scales), id[NS] i32 (token id).
+//   windows       kscale[NW][d] u8 (per-channel E4M3 key scales, one window =
+//                 one 16-token emission), kscale_f32[NW], vscale_f32[NW] (FP8
+//                 per-window scales), refs[NW] (live slots referencing it),
+//                 free stack[NW] + nfree.
+//   tokens        tok_slot[T] i32: slot of each live token id (-1 otherwise).
+//   segments      segmask[NSEG][W] u32: member bitmask relative to start_step.
+//   buffer        buf_k/buf_v[2][g][d] input dtype (double-buffered emission window).
+#pragma once
+#include <stdint.h>
+
+#define TKV_MAX_BANDS 8
+#define TKV_MAX_G 16
+
+enum { TKV_FMT_TERNARY = 0, TKV_FMT_NVFP4 = 1, TKV_FMT_FP8 = 2, TKV_FMT_RAW = 3 };
+enum { TKV_IN_BF16 = 0, TKV_IN_F32 = 1, TKV_IN_F64 = 2 };
+
+// Error codes mirror thinkv::Error::exit_code() (proj/include/thinkv/errors.hpp:31-46).
+enum { TKV_E_OK = 0, TKV_E_UNEXPECTED = 1, TKV_E_STRUCTURAL = 2, TKV_E_CALIBRATION = 3,
+       TKV_E_OOM = 4, TKV_E_INTEGRITY = 5 };
+
+struct TkvDims {
+  int32_t U;          // units
+  int32_t G;          // query heads per unit
+  int32_t D;          // head dim
+  int32_t maxpool;    // 1 = one max-pooled softmax row per unit
+  int32_t bs;         // block size (<= 32)
+  int32_t P;          // pool blocks per unit
+  int32_t NS;         // slots per unit = P * bs
+  int32_t NW;         // window capacity per unit
+  int32_t g;          // quantization group size (emission window length)
+  int32_t vchunks;    // ceil(D / g)
+  int32_t kstride;    // bytes per slot in kcode/vcode
+  int32_t T;          // token-id capacity (prompt_len + max_gen_len)
+  int32_t W;          // u32 words per segment member mask = ceil(tau / 32)
+  int32_t NSEG;       // segment capacity per unit
+  int32_t in_dtype;   // TKV_IN_*
+  int32_t in_bytes;   // bytes per input element
+  int32_t num_bands;
+  int32_t band_fmt[TKV_MAX_BANDS];   // TKV_FMT_* per thought band
+  int32_t band_bytes[TKV_MAX_BANDS]; // code bytes per K (or V) vector per band
+  float scale;        // 1/sqrt(D)
+  double thr_frac;    // sparsity threshold fraction
+};
+
+struct TkvState {
+  TkvDims dm;
+  // block table
+  int8_t* blk_thought;
+  uint8_t* blk_filled;
+  uint32_t* blk_evict;
+  uint8_t* blk_nstart;
+  int32_t* blk_start;
+  uint32_t* blk_segmask;
+  int32_t* unit_nfree;    // free blocks per unit
+  // slots
+  uint8_t* slot_k;
+  uint8_t* slot_v;
+  uint8_t* slot_vs;
+  int32_t* slot_win;
+  int32_t* slot_id;
+  // windows
+  uint8_t* win_ks;
+  float* win_kf;
+  float* win_vf;
+  int32_t* win_refs;
+  int32_t* win_free;
+  int32_t* win_nfree;
+  // tokens / segments / buffer
+  int32_t* tok_slot;
+  uint32_t* seg_mask;
+  uint8_t* buf;          // [U][2][2 (k,v)][g][D] * in_bytes
+  // per-unit outputs of the score kernel and sticky device errors
+  double* sparsity;      // [U]
+  int32_t* err;          // [U]
+};
+
+// Per-group (sequence) control values for an emission (flush).
+struct TkvFlushCtl {
+  int32_t band;        // open segment's thought band
+  int32_t seg_start;   // open segment's start_step (start index for the block table)
+};
+
+// One K-means anneal of one segment, identical for every unit of a group.
+struct TkvAnnealOp {
+  int32_t unit0, nunits;  // unit range of the group
+  int32_t seg;            // device segment index
+  int32_t seg_start;      // start_step (bit 0 of the member mask)
+  int32_t span;           // initial_size (valid member bits)
+  int32_t m;              // members before this anneal
+  int32_t K;              // retention target (< m)
+  int32_t log_off;        // offset (in u32 words) of this op's evicted-mask log, per unit: + u_rel*W
+};
+
+// Units of one group whose anneal ops [op_begin, op_end) are applied together
+// (one evict event per unit, sim.cpp:652-671).
+struct TkvApplyGroup {
+  int32_t unit0, nunits;
+  int32_t op_begin, op_end;
+};

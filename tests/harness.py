@@ -1,0 +1,94 @@
+"""Shared parity harness: drive the CUDA path (paper_2510_01290_b200) and the
+oracle (oracle/, the reference restatement over the compiled reference
+library) on identical inputs and compare everything the reference exposes.
+
+Tolerances:
+  * cache state (codes implied by dumps, block tables, eviction masks, start
+    indices, segment masks, free lists, segment members, events, metrics):
+    exact equality of the reference's JSON views;
+  * attention outputs: max |gpu - oracle| <= ATOL + RTOL * max|oracle| per
+    step, with ATOL = 1e-3 and RTOL = 1e-3 (north_star: "max-abs 1e-3
+    relative to the reference"); the CUDA kernel accumulates in fp32 with
+    exact dequantised products, so observed errors are ~1e-6.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+import oracle as O
+
+ATOL = 1e-3
+RTOL = 1e-3
+
+
+def oracle_config(cfg) -> "O.RunConfig":
+    fields = {f.name for f in dataclasses.fields(O.RunConfig)}
+    return O.RunConfig(**{k: v for k, v in dataclasses.asdict(cfg).items() if k in fields})
+
+
+def synth_inputs(cfg, seed, step):
+    q, k, v = O.synth_step(seed, cfg.units_per_seq, cfg.tau, cfg.units, cfg.num_q_heads,
+                           cfg.head_dim, step)
+    return q, k, v
+
+
+def run_parity(cfg, seed=0x71534B56, steps=None, check_every=1, inputs=None):
+    """Returns a dict of comparison results.  inputs: optional callable
+    step -> (q, k, v) numpy arrays in cfg.input_dtype's host representation
+    (uint16 bf16 bits or float64)."""
+    import torch
+    from paper_2510_01290_b200 import DecodeRun
+
+    steps = steps if steps is not None else cfg.prompt_len + cfg.max_gen_len
+    run = DecodeRun(cfg)
+    orc = O.OracleRun(oracle_config(cfg))
+    dev = torch.device("cuda:0")
+    rows = cfg.out_rows
+    out = torch.empty((cfg.units, rows, cfg.head_dim), dtype=torch.float32, device=dev)
+    max_err = 0.0
+    for t in range(steps):
+        if inputs is None:
+            q, k, v = synth_inputs(cfg, seed, t)
+        else:
+            q, k, v = inputs(t)
+        if cfg.input_dtype == "bf16":
+            qd, kd, vd = O.bf16_to_f64(q), O.bf16_to_f64(k), O.bf16_to_f64(v)
+            tq = torch.from_numpy(q.view(np.int16)).view(torch.bfloat16).to(dev)
+            tk = torch.from_numpy(k.view(np.int16)).view(torch.bfloat16).to(dev)
+            tv = torch.from_numpy(v.view(np.int16)).view(torch.bfloat16).to(dev)
+        else:
+            qd, kd, vd = q, k, v
+            tt = torch.float64 if cfg.input_dtype == "f64" else torch.float32
+            tq, tk, tv = (torch.from_numpy(np.ascontiguousarray(x)).to(dev, tt) for x in (q, k, v))
+        ref_out, _ = orc.step(qd, kd, vd)
+        run.step(tq, tk, tv, out)
+        if t % check_every == 0 or t == steps - 1:
+            got = out.double().cpu().numpy()
+            err = float(np.max(np.abs(got - ref_out)))
+            scale = float(np.max(np.abs(ref_out)))
+            assert err <= ATOL + RTOL * scale, f"step {t}: attention error {err} (scale {scale})"
+            max_err = max(max_err, err)
+    run.synchronize()
+    res = {"max_err": max_err, "run": run, "oracle": orc, "steps": steps}
+    return res
+
+
+def compare_state(res, cfg, finish=True):
+    run, orc = res["run"], res["oracle"]
+    if finish:
+        run.finish()
+        orc.finish()
+    for s in range(cfg.num_seqs):
+        gt, ot = run.tables(s), orc.dump(s, "tables")
+        assert gt == ot, f"seq {s}: block tables differ"
+        gs, os_ = run.segments(s), orc.dump(s, "segments")
+        assert gs == os_, f"seq {s}: segments differ"
+        if cfg.record_events:
+            ge, oe = run.events(s), orc.dump(s, "events")
+            assert [l for l in ge.splitlines()] == [l for l in oe.splitlines()], f"seq {s}: events differ"
+        if cfg.dump_positions:
+            assert run.step_dumps(s) == orc.dump(s, "step_dumps"), f"seq {s}: step dumps differ"
+        if finish:
+            assert run.metrics(s) == orc.dump(s, "metrics"), f"seq {s}: metrics differ"

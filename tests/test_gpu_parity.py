@@ -1,0 +1,112 @@
+"""GPU parity: the CUDA decode path against the oracle (reference
+restatement over the compiled reference library) on identical inputs.
+
+Cache state, eviction decisions, slot placements, free lists, events and
+metrics must be bit-identical; attention outputs within harness.ATOL/RTOL.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle as O  # noqa: E402
+from harness import compare_state, run_parity  # noqa: E402
+from paper_2510_01290_b200 import DecodeRun, ThinkvConfig, TkvError  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def script(num_seqs, intervals, seed=3, pT=200):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(num_seqs):
+        s = []
+        for _ in range(intervals):
+            s.append(2 if rng.random() < pT / 1000 else int(rng.integers(0, 2)))
+        out.append(s)
+    return out
+
+
+def test_walkthrough_golden_fixture_on_gpu():
+    """The reference's golden walkthrough (test_sim.cpp:386-489), fed the
+    ToyModel stream in fp64, reproduces walkthrough_dumps.json on the GPU."""
+    ref_cfg = {"model": {"num_layers": 1, "head_dim": 4, "num_heads": 1, "embed_dim": 8, "seed": 7},
+               "tau": 4, "group_size": 4, "block_size": 4, "budget": 64, "schedule": [2],
+               "num_thoughts": 3, "max_gen_len": 16, "seed": 1, "pool_blocks": 16,
+               "scripted_trace": ["R", "E", "T", "R"], "dump_positions": [3, 7, 11, 12, 15]}
+    q, k, v = O.toy_stream(ref_cfg)
+    cfg = ThinkvConfig(num_seqs=1, units_per_seq=1, num_q_heads=1, head_dim=4, tau=4, group_size=4,
+                       block_size=4, pool_blocks=16, budget=64, levels=(2,), psi_bits=(4, 4, 2),
+                       max_gen_len=16, script=[[1, 0, 2, 1]], input_dtype="f64", record_events=True,
+                       dump_positions=(3, 7, 11, 12, 15))
+    res = run_parity(cfg, inputs=lambda t: (q[t], k[t], v[t]))
+    golden = json.load(open(os.path.join(HERE, "golden", "walkthrough_dumps.json")))
+    assert res["run"].step_dumps(0) == golden
+    compare_state(res, cfg)
+
+
+CONFIGS = {
+    # d=128, G=4 per-head (R1-Llama-8B head shape), block 16, R4E4T2, transitions
+    "llama_shape": ThinkvConfig(num_seqs=2, units_per_seq=3, num_q_heads=4, head_dim=128, tau=32,
+                                group_size=16, block_size=16, budget=96, levels=(16, 8, 4),
+                                max_gen_len=420, script=script(2, 16), record_events=True,
+                                dump_positions=(100, 257)),
+    # GPT-OSS head shape d=64, G=8, max-pool GQA, FP8 reasoning band, block 8
+    "gptoss_maxpool_fp8": ThinkvConfig(num_seqs=2, units_per_seq=2, num_q_heads=8, gqa_maxpool=True,
+                                       head_dim=64, tau=32, group_size=16, block_size=8, budget=80,
+                                       levels=(16, 8, 4), psi_bits=(4, 8, 2), max_gen_len=360,
+                                       script=script(2, 12, seed=5), record_events=True),
+    # Qwen-14B G=5, raw 16-bit passthrough band + ternary, prompt prefix, tau % g != 0
+    "qwen_raw16_prompt": ThinkvConfig(num_seqs=1, units_per_seq=3, num_q_heads=5, head_dim=128, tau=24,
+                                      group_size=16, block_size=8, budget=60, levels=(12, 6, 3),
+                                      psi_bits=(8, 16, 2), prompt_len=20, max_gen_len=300,
+                                      script=script(1, 14, seed=9, pT=300), record_events=True),
+    # calibrated labels from the fp64 sparsity kernel (refresh steps only)
+    "calibrated": ThinkvConfig(num_seqs=2, units_per_seq=3, num_q_heads=4, head_dim=64, tau=32,
+                               group_size=16, block_size=16, budget=90, levels=(16, 8, 4),
+                               max_gen_len=400, scripted=False, thresholds=(0.25, 0.55),
+                               calib_units=(0, 2), record_events=True),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_parity_synthetic(name):
+    cfg = CONFIGS[name]
+    res = run_parity(cfg)
+    compare_state(res, cfg)
+
+
+def test_parity_full_tau_kmeans():
+    """tau = 128 segments: the 128 -> 64 K-means with farthest-first restarts
+    and the 8 -> 4 exhaustive-seed path, at the paper's schedule."""
+    cfg = ThinkvConfig(num_seqs=1, units_per_seq=2, num_q_heads=4, head_dim=128, tau=128,
+                       group_size=16, block_size=16, budget=400, levels=(64, 32, 16, 8, 4),
+                       max_gen_len=1300, script=[[1, 0, 1, 0, 2, 1, 0, 1, 0, 1, 2]], record_events=True)
+    res = run_parity(cfg, check_every=7)
+    compare_state(res, cfg)
+
+
+def test_pool_exhaustion_matches_reference_error():
+    cfg = ThinkvConfig(num_seqs=1, units_per_seq=1, num_q_heads=2, head_dim=16, tau=16, group_size=8,
+                       block_size=4, pool_blocks=3, budget=4096, levels=(8, 4), max_gen_len=64,
+                       script=[[1]])
+    with pytest.raises(O.OracleError) as oe:
+        run_parity(cfg)
+    assert oe.value.code == 4
+    run = DecodeRun(cfg)
+    dev = torch.device("cuda:0")
+    q = torch.zeros((1, 2, 16), dtype=torch.bfloat16, device=dev)
+    kv = torch.ones((1, 16), dtype=torch.bfloat16, device=dev)
+    out = torch.empty((1, 2, 16), device=dev)
+    for _ in range(64):
+        run.step(q, kv, kv, out)
+    with pytest.raises(TkvError) as ge:
+        run.synchronize()
+    assert ge.value.code == 4
