@@ -159,9 +159,12 @@ class OracleRun:
             raise ValueError(err.value.decode())
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().orc_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                lib().orc_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
 
     def step(self, q: np.ndarray, k: np.ndarray, v: np.ndarray):
         c = self.cfg

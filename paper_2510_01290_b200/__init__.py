@@ -141,9 +141,18 @@ class DecodeRun:
         self.close()
 
     # -- stepping ---------------------------------------------------------
+    @staticmethod
+    def _stream(stream):
+        # Default: PyTorch's current stream, so the caller's reads/writes of
+        # q/k/v/out are ordered with the run (tkv_step joins the two streams).
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream()
+        return stream.cuda_stream
+
     def step(self, q, k, v, out, stream=None):
         """q [units,G,d], k/v [units,d] (input dtype), out [units,rows,d] fp32: CUDA tensors."""
-        s = stream.cuda_stream if stream is not None else None
+        s = self._stream(stream)
         check(lib.tkv_step(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), s))
 
     def step_host(self, q, k, v, out):
@@ -152,7 +161,7 @@ class DecodeRun:
         check(lib.tkv_step_host(self._h, ptr(q), ptr(k), ptr(v), ptr(out)))
 
     def synth_inputs(self, seed: int, step: int, q, k, v, stream=None):
-        s = stream.cuda_stream if stream is not None else None
+        s = self._stream(stream)
         check(lib.tkv_synth_inputs(self._h, seed, step, q.data_ptr(), k.data_ptr(), v.data_ptr(), s))
 
     def finish(self):

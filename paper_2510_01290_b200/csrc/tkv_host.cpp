@@ -883,7 +883,9 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   r->levels.assign(d.levels, d.levels + d.num_levels);
   r->total_steps = d.prompt_len + d.max_gen_len;
   CUDA_OK(cudaSetDevice(ctx->device));
-  CUDA_OK(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+  // A blocking stream: ordered with the legacy default stream (what PyTorch
+  // uses unless told otherwise); other caller streams are joined with events.
+  CUDA_OK(cudaStreamCreate(&r->stream));
 
   TkvDims dm{};
   dm.U = d.num_seqs * d.units_per_seq;
