@@ -1,0 +1,321 @@
+"""ThinKV decode-path benchmark (see BASELINE.json: decode tokens/s & TPOT at the
+R1-Distill-Llama-8B attention shape, bs 32, 32K generated tokens, <5% KV
+budget; achieved HBM GB/s of the paged-attention kernel).
+
+One "step" = one decode step of the ThinKV path for every unit of the batch:
+paged mixed-precision attention (K1) for all 32 layers x 8 KV heads x 32
+sequences, buffer append, and whatever emission (K2) / refresh scoring (K3a)
+/ K-means eviction (K3d+e) that step triggers -- the reference's
+ThinkvMethod::process (proj/src/sim.cpp:748-843) for 8192 units.
+
+Usage:  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU: launched under torchrun; each rank decodes its own 32 sequences
+(weak scaling, no data-path collective); NCCL all-gathers per-rank stats.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/s & TPOT, R1-Llama-8B shape bs32 32K ctx; achieved HBM GB/s"
+SEED = 0x71534B56
+
+
+def workload(args):
+    from paper_2510_01290_b200 import ThinkvConfig
+    from paper_2510_01290_b200.synth import band_script
+    intervals = args.max_gen // args.tau + 2
+    # Scripted thought labels per sequence: T with p=0.1, else R/E 50/50.
+    script = band_script(SEED, args.seqs, intervals, 3, args.pT_permille)
+    return ThinkvConfig(num_seqs=args.seqs, units_per_seq=args.layers * args.kv_heads, num_q_heads=args.q_per_kv,
+                        head_dim=args.head_dim, tau=args.tau, group_size=16, block_size=args.block_size,
+                        budget=args.budget, levels=(64, 32, 16, 8, 4), psi_bits=(4, 4, 2),
+                        max_gen_len=args.max_gen, script=script)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                f = [x.strip() for x in out.split(",")]
+                self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        import statistics
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace('.', '').isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace('.', '').isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_reference(args, cfg, steps_timed=None):
+    """The reference's own CPU implementation (compiled from /root/reference by
+    oracle/Makefile into oracle/_ref/, driven by the ThinkvMethod restatement)
+    on the host's cores: one single-unit sequence per thread, at this config's
+    unit shape, decoded from step 0; the last `steps_timed` steps of each are
+    timed.  Per unit-step time x units / threads = extrapolated TPOT."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    threads = os.cpu_count() or 1
+    steps_timed = steps_timed or args.cpu_steps
+    warm = args.cpu_warm
+    per_thread_time = [0.0] * threads
+    errs = []
+
+    def worker(i):
+        try:
+            rc = O.RunConfig(num_seqs=1, units_per_seq=1, num_q_heads=cfg.num_q_heads, head_dim=cfg.head_dim,
+                             tau=cfg.tau, group_size=cfg.group_size, block_size=cfg.block_size,
+                             budget=cfg.budget, levels=cfg.levels, psi_bits=cfg.psi_bits,
+                             max_gen_len=warm + steps_timed, script=[cfg.script[i % cfg.num_seqs]])
+            run = O.OracleRun(rc)
+            unit = i * 37  # distinct units of the workload
+            acc = 0.0
+            for t in range(warm + steps_timed):
+                q, k, v = O.synth_step(SEED, cfg.units_per_seq, cfg.tau, 1, cfg.num_q_heads, cfg.head_dim, t,
+                                       unit0=unit)
+                qd, kd, vd = O.bf16_to_f64(q), O.bf16_to_f64(k), O.bf16_to_f64(v)
+                t0 = time.perf_counter()
+                run.step(qd, kd, vd)
+                if t >= warm:
+                    acc += time.perf_counter() - t0
+            per_thread_time[i] = acc
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(threads)]
+    wall0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    wall = time.perf_counter() - wall0
+    if errs:
+        raise RuntimeError(errs[0])
+    unit_step_s = sum(per_thread_time) / (threads * steps_timed)
+    tpot_s = unit_step_s * cfg.units / threads
+    return {
+        "value": cfg.num_seqs / tpot_s, "unit": "tokens/s", "cores": threads, "kind": "reference",
+        "tpot_ms": tpot_s * 1e3, "unit_step_us": unit_step_s * 1e6,
+        "sample": (f"{threads} threads x 1 unit each (config-2 unit shape), steps {warm}..{warm + steps_timed - 1} "
+                   f"timed after an untimed decode from step 0; TPOT extrapolated as per-unit-step time x "
+                   f"{cfg.units} units / {threads} threads; only the reference step calls are timed "
+                   f"({wall:.1f} s wall)"),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=128)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ctx", type=int, default=None, help="decode position at which timing starts")
+    ap.add_argument("--e2e-steps", type=int, default=32)
+    ap.add_argument("--seqs", type=int, default=32)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--kv-heads", type=int, default=8)
+    ap.add_argument("--q-per-kv", type=int, default=4)
+    ap.add_argument("--head-dim", type=int, default=128)
+    ap.add_argument("--tau", type=int, default=128)
+    ap.add_argument("--block-size", type=int, default=16)
+    ap.add_argument("--budget", type=int, default=1024)
+    ap.add_argument("--max-gen", type=int, default=32768)
+    ap.add_argument("--pT-permille", type=int, default=100)
+    ap.add_argument("--cpu-steps", type=int, default=128)
+    ap.add_argument("--cpu-warm", type=int, default=1280)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = workload(args)
+    config = {"workload": "ThinKV decode, R1-Distill-Llama-8B attention shape (32 q / 8 kv heads, d=128, "
+                          "32 layers), bs32 per GPU, 32K generated, budget 1024 (3.1%), R4E4T2, block 16",
+              "global_batch": args.seqs * world, "units_per_gpu": cfg.units, "parallelism": f"seq-shard x{world}",
+              "gqa": "per-head", "l2": "working set (compressed KV, ~2 GB/GPU) larger than L2"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_reference(args, cfg)
+        line = {"metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": cb["tpot_ms"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference", "config": config,
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2510_01290_b200 import DecodeRun
+
+    dev = torch.device("cuda", local)
+    U, G, D = cfg.units, cfg.num_q_heads, cfg.head_dim
+    K, W, E = args.steps, args.warmup, args.e2e_steps
+    ctx = args.ctx if args.ctx is not None else cfg.max_gen_len - (W + K + E)
+    ctx = max(0, min(ctx, cfg.max_gen_len - (W + K + E)))
+    run = DecodeRun(cfg, device=local)
+    q = torch.empty((U, G, D), dtype=torch.bfloat16, device=dev)
+    k = torch.empty((U, D), dtype=torch.bfloat16, device=dev)
+    v = torch.empty((U, D), dtype=torch.bfloat16, device=dev)
+    out = torch.empty((U, G, D), dtype=torch.float32, device=dev)
+    # 1. build the decode context (untimed): the real path, step by step.
+    t_ctx = time.time()
+    for t in range(ctx):
+        run.synth_inputs(SEED + rank, t, q, k, v)
+        run.step(q, k, v, out)
+    torch.cuda.synchronize(dev)
+    t_ctx = time.time() - t_ctx
+    # 2. inputs of the warmup + timed steps, resident in HBM before timing.
+    qs = torch.empty((W + K, U, G, D), dtype=torch.bfloat16, device=dev)
+    ks = torch.empty((W + K, U, D), dtype=torch.bfloat16, device=dev)
+    vs = torch.empty((W + K, U, D), dtype=torch.bfloat16, device=dev)
+    for i in range(W + K):
+        run.synth_inputs(SEED + rank, ctx + i, qs[i], ks[i], vs[i])
+    for i in range(W):
+        run.step(qs[i], ks[i], vs[i], out)
+    bytes_k1 = run.bytes()  # algorithmic bytes of one attention launch at this point
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    run.timing_enable(True)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        start.record()
+        for i in range(W, W + K):
+            run.step(qs[i], ks[i], vs[i], out)
+        end.record()
+        torch.cuda.synchronize(dev)
+    tm = run.timing_read()
+    ms = start.elapsed_time(end)
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    # 3. end to end through the public API with host buffers (pinned).
+    pq = torch.empty((U, G, D), dtype=torch.bfloat16).pin_memory()
+    pk = torch.empty((U, D), dtype=torch.bfloat16).pin_memory()
+    pv = torch.empty((U, D), dtype=torch.bfloat16).pin_memory()
+    pout = torch.empty((U, G, D), dtype=torch.float32).pin_memory()
+    host_inputs = []
+    for i in range(E):
+        run.synth_inputs(SEED + rank, ctx + W + K + i, q, k, v)
+        host_inputs.append((q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()))
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for i in range(E):
+        hq, hk, hv = host_inputs[i]
+        run.step_host(hq, hk, hv, pout)
+    e2e_s = time.perf_counter() - t0
+    e2e_t = torch.tensor([e2e_s], device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+    run.synchronize()
+    # stats gather over NVLink (the path's only collective)
+    stats = torch.tensor([tm["attend_ms"], tm["anneal_ms"], float(bytes_k1["live_slots"])], device=dev)
+    if world > 1:
+        gathered = [torch.zeros_like(stats) for _ in range(world)]
+        torch.distributed.all_gather(gathered, stats)
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    tok_s = cfg.num_seqs * world * K / (ms_max / 1e3)
+    peak, peak_kind = measured_peak()
+    k1_ms = tm["attend_ms"] / max(1, tm["attend_launches"])
+    achieved = bytes_k1["algorithmic_bytes"] / (k1_ms / 1e3) / 1e9
+    traffic = ncu_traffic()
+    line = {
+        "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16 in / fp32 attention / fp64 eviction", "data": "synthetic (deterministic bf16 q/k/v, scripted labels)",
+        "config": {**config, "context_steps": ctx, "timed_positions": [ctx + W, ctx + W + K - 1]},
+        "tpot_ms": ms_max / K,
+        "gpu_launches": tm["total_launches"],
+        "breakdown_ms_per_step": {n: tm[n] / K for n in ("attend_ms", "score_ms", "flush_ms", "anneal_ms", "apply_ms")},
+        "roofline": {"kernel": "K1 paged decode attention", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": bytes_k1["algorithmic_bytes"],
+                     "launch_ms": k1_ms, "live_tokens_per_unit": bytes_k1["live_slots"] / U},
+        "e2e": {"value": cfg.num_seqs * world * E / e2e_s, "unit": "tokens/s",
+                "h2d_bytes_per_step": int(pq.numel() * 2 + pk.numel() * 2 + pv.numel() * 2),
+                "d2h_bytes_per_step": int(pout.numel() * 4), "steps": E},
+        "clocks": clk.summary(),
+        "context_build_s": t_ctx,
+    }
+    if not args.no_cpu and world == 1:
+        cb = cpu_reference(args, cfg)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -134,6 +134,16 @@ int tkv_bytes(tkv_run* run, tkv_bytes_t* out);
 /* Last fp64 per-unit sparsity (layer_sparsity_average) computed on a refresh step. */
 int tkv_unit_sparsity(tkv_run* run, double* out, int64_t n);
 
+/* Per-kernel device time of the run's launches (CUDA events on the run's
+ * stream).  Enabling resets the counters; reading synchronises. */
+typedef struct tkv_timing_t {
+  double attend_ms, score_ms, flush_ms, anneal_ms, apply_ms;
+  int64_t attend_launches, score_launches, flush_launches, anneal_launches, apply_launches;
+  int64_t total_launches;  /* every kernel launched by the run since enable */
+} tkv_timing_t;
+int tkv_timing_enable(tkv_run* run, int enable);
+int tkv_timing_read(tkv_run* run, tkv_timing_t* out);
+
 /* Deterministic synthetic bf16 inputs for step `step` (synth.h) on device. */
 int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t step, void* q, void* k, void* v, void* stream);
 

@@ -202,6 +202,14 @@ class DecodeRun:
         check(lib.tkv_bytes(self._h, C.byref(b)))
         return {n: getattr(b, n) for n, _ in _abi.Bytes._fields_}
 
+    def timing_enable(self, enable: bool = True):
+        check(lib.tkv_timing_enable(self._h, int(enable)))
+
+    def timing_read(self) -> dict:
+        t = _abi.Timing()
+        check(lib.tkv_timing_read(self._h, C.byref(t)))
+        return {n: getattr(t, n) for n, _ in _abi.Timing._fields_}
+
     def unit_sparsity(self):
         import numpy as np
         out = np.zeros(self.cfg.units, dtype=np.float64)

@@ -16,6 +16,7 @@ EXPORTS = (
     "tkv_last_error", "tkv_abi_version", "tkv_init", "tkv_ctx_destroy", "tkv_run_create",
     "tkv_run_destroy", "tkv_step", "tkv_step_host", "tkv_finish", "tkv_synchronize",
     "tkv_position", "tkv_dump_json", "tkv_bytes", "tkv_unit_sparsity", "tkv_synth_inputs",
+    "tkv_timing_enable", "tkv_timing_read",
 )
 
 STATUS = {0: "ok", 1: "unexpected", 2: "config", 3: "calibration", 4: "out_of_memory",
@@ -47,6 +48,12 @@ class Bytes(C.Structure):
         "qo_bytes", "meta_bytes", "algorithmic_bytes")]
 
 
+class Timing(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("attend_ms", "score_ms", "flush_ms", "anneal_ms", "apply_ms")] + \
+               [(n, C.c_int64) for n in ("attend_launches", "score_launches", "flush_launches",
+                                         "anneal_launches", "apply_launches", "total_launches")]
+
+
 class TkvError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{STATUS.get(code, code)}] {msg}")
@@ -76,6 +83,8 @@ def _load():
                                 C.POINTER(C.c_size_t)]
     L.tkv_bytes.argtypes = [vp, C.POINTER(Bytes)]
     L.tkv_unit_sparsity.argtypes = [vp, vp, C.c_int64]
+    L.tkv_timing_enable.argtypes = [vp, C.c_int]
+    L.tkv_timing_read.argtypes = [vp, C.POINTER(Timing)]
     L.tkv_synth_inputs.argtypes = [vp, C.c_uint64, C.c_int64, vp, vp, vp, vp]
     return L
 

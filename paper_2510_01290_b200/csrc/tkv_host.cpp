@@ -175,6 +175,17 @@ struct tkv_run {
   std::vector<double> last_sparsity;
   std::vector<std::vector<double>> refresh_sparsity;  // per refresh (record mode)
   std::vector<json> metrics;
+  // per-kernel timing (tkv_timing_enable / tkv_timing_read)
+  struct TimedLaunch {
+    int cat;
+    cudaEvent_t a, b;
+  };
+  bool timing = false;
+  std::vector<TimedLaunch> timed;
+  std::vector<cudaEvent_t> ev_pool;
+  double acc_ms[5] = {0, 0, 0, 0, 0};
+  int64_t acc_n[5] = {0, 0, 0, 0, 0};
+  int64_t launches = 0;
   // host-pointer step staging
   void* d_q = nullptr;
   void* d_k = nullptr;
@@ -286,6 +297,49 @@ void check_launch(cudaError_t e, const char* what) {
     throw TkvError(TKV_ERR_UNEXPECTED, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+enum { CAT_ATTEND = 0, CAT_SCORE = 1, CAT_FLUSH = 2, CAT_ANNEAL = 3, CAT_APPLY = 4 };
+
+cudaEvent_t pool_event(tkv_run* r) {
+  if (!r->ev_pool.empty()) {
+    cudaEvent_t e = r->ev_pool.back();
+    r->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CUDA_OK(cudaEventCreate(&e));
+  return e;
+}
+
+void drain_timing(tkv_run* r) {
+  CUDA_OK(cudaStreamSynchronize(r->stream));
+  for (auto& t : r->timed) {
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, t.a, t.b));
+    r->acc_ms[t.cat] += ms;
+    r->acc_n[t.cat] += 1;
+    r->ev_pool.push_back(t.a);
+    r->ev_pool.push_back(t.b);
+  }
+  r->timed.clear();
+}
+
+// Every kernel launch of the run goes through here (launch count + optional
+// CUDA-event timing on the run's stream).
+template <typename F>
+void launch(tkv_run* r, int cat, const char* what, F&& fn) {
+  r->launches += 1;
+  if (!r->timing) {
+    check_launch(fn(), what);
+    return;
+  }
+  if (r->timed.size() >= 4096) drain_timing(r);
+  cudaEvent_t a = pool_event(r), b = pool_event(r);
+  CUDA_OK(cudaEventRecord(a, r->stream));
+  check_launch(fn(), what);
+  CUDA_OK(cudaEventRecord(b, r->stream));
+  r->timed.push_back({cat, a, b});
+}
+
 // -------------------------------------------------------------------------
 // schedule arithmetic (sizes only): evictor.cpp:348-433
 // -------------------------------------------------------------------------
@@ -375,9 +429,10 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
     for (size_t i = 0; i < wv.size(); ++i) { prefix[i] = items; items += wv[i].nunits; }
     TkvAnnealOp* d_ops = upload(r, wv.data(), wv.size());
     int32_t* d_pre = upload(r, prefix.data(), prefix.size());
-    check_launch(tkv_launch_anneal(r->st, d_ops, (int)wv.size(), d_pre, items, r->d_log, r->d_scratch,
-                                   r->scratch_ctas, r->scratch_per_cta, r->max_m, r->stream),
-                 "anneal kernel");
+    launch(r, CAT_ANNEAL, "anneal kernel", [&] {
+      return tkv_launch_anneal(r->st, d_ops, (int)wv.size(), d_pre, items, r->d_log, r->d_scratch,
+                               r->scratch_ctas, r->scratch_per_cta, r->max_m, r->stream);
+    });
   }
   std::vector<TkvAnnealOp> aops;
   std::vector<TkvApplyGroup> ag;
@@ -397,8 +452,9 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
     TkvAnnealOp* d_aops = upload(r, aops.data(), aops.size());
     TkvApplyGroup* d_ag = upload(r, ag.data(), ag.size());
     int32_t* d_apre = upload(r, aprefix.data(), aprefix.size());
-    check_launch(tkv_launch_apply(r->st, d_aops, d_ag, (int)ag.size(), d_apre, aitems, r->d_log, r->stream),
-                 "apply kernel");
+    launch(r, CAT_APPLY, "apply kernel", [&] {
+      return tkv_launch_apply(r->st, d_aops, d_ag, (int)ag.size(), d_apre, aitems, r->d_log, r->stream);
+    });
   }
   // events
   for (size_t pi = 0; pi < plans.size(); ++pi) {
@@ -439,9 +495,10 @@ void flush_all(tkv_run* r, int64_t step) {
     ctl[gi].seg_start = (int32_t)s.start;
   }
   TkvFlushCtl* d_ctl = upload(r, ctl.data(), ctl.size());
-  check_launch(tkv_launch_flush(r->st, r->cur_half, r->buf_len, (int)r->buf_pos0, d_ctl, r->desc.units_per_seq,
-                                r->stream),
-               "flush kernel");
+  launch(r, CAT_FLUSH, "flush kernel", [&] {
+    return tkv_launch_flush(r->st, r->cur_half, r->buf_len, (int)r->buf_pos0, d_ctl, r->desc.units_per_seq,
+                            r->stream);
+  });
   if (r->desc.record_events) {
     for (size_t gi = 0; gi < r->groups.size(); ++gi) {
       Group& g = r->groups[gi];
@@ -819,9 +876,11 @@ void do_step(tkv_run* r, const void* q, const void* k, const void* v, float* out
   const int put_slot = flush_first ? 0 : r->buf_len;
   // 1. attention (+ exact sparsity on refresh steps, where it is consumed)
   if (refresh && decode)
-    check_launch(tkv_launch_score(r->st, q, k, r->cur_half, r->buf_len, r->stream), "score kernel");
-  check_launch(tkv_launch_attend(r->st, q, k, v, out, r->cur_half, r->buf_len, put_half, put_slot, r->stream),
-               "attend kernel");
+    launch(r, CAT_SCORE, "score kernel",
+           [&] { return tkv_launch_score(r->st, q, k, r->cur_half, r->buf_len, r->stream); });
+  launch(r, CAT_ATTEND, "attend kernel", [&] {
+    return tkv_launch_attend(r->st, q, k, v, out, r->cur_half, r->buf_len, put_half, put_slot, r->stream);
+  });
   // 2. refresh boundary
   if (refresh) boundary(r, pos, decode);
   // 3. buffer the token under the open segment
@@ -976,6 +1035,8 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
 void destroy_run(tkv_run* r) {
   if (r->stream) cudaStreamSynchronize(r->stream);
   for (void* p : r->allocations) cudaFree(p);
+  for (auto& t : r->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  for (auto e : r->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
     if (r->h_pinned[i]) cudaFreeHost(r->h_pinned[i]);
     if (r->pinned_ev[i]) cudaEventDestroy(r->pinned_ev[i]);
@@ -1198,6 +1259,38 @@ int tkv_unit_sparsity(tkv_run* run, double* out, int64_t n) {
   try {
     const auto sp = download_sparsity(run);
     std::memcpy(out, sp.data(), std::min<int64_t>(n, (int64_t)sp.size()) * sizeof(double));
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  }
+}
+
+int tkv_timing_enable(tkv_run* run, int enable) {
+  try {
+    if (run->timing) drain_timing(run);
+    run->timing = enable != 0;
+    for (int i = 0; i < 5; ++i) { run->acc_ms[i] = 0.0; run->acc_n[i] = 0; }
+    run->launches = 0;
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  }
+}
+
+int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
+  try {
+    drain_timing(run);
+    out->attend_ms = run->acc_ms[CAT_ATTEND];
+    out->score_ms = run->acc_ms[CAT_SCORE];
+    out->flush_ms = run->acc_ms[CAT_FLUSH];
+    out->anneal_ms = run->acc_ms[CAT_ANNEAL];
+    out->apply_ms = run->acc_ms[CAT_APPLY];
+    out->attend_launches = run->acc_n[CAT_ATTEND];
+    out->score_launches = run->acc_n[CAT_SCORE];
+    out->flush_launches = run->acc_n[CAT_FLUSH];
+    out->anneal_launches = run->acc_n[CAT_ANNEAL];
+    out->apply_launches = run->acc_n[CAT_APPLY];
+    out->total_launches = run->launches;
     return TKV_OK;
   } catch (const TkvError& e) {
     return fail(e);
