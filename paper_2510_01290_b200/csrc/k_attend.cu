@@ -523,6 +523,10 @@ cudaError_t launch_attend_g(const TkvState& st, const void* q, const void* k, co
 
 cudaError_t tkv_launch_attend(const TkvState& st, const void* q, const void* k, const void* v, float* out,
                               int buf_half, int nbuf, int put_half, int put_slot, cudaStream_t s) {
+  // Tensor-core kernel for the production shapes (d = 64/128, bf16, G <= 8,
+  // quantised bands); the SIMT kernel below covers every other shape/dtype.
+  if (tkv_attend_mma_supported(st.dm))
+    return tkv_launch_attend_mma(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
   const int D = st.dm.D;
   if (D <= 32) return launch_attend_g<1>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
   if (D <= 64) return launch_attend_g<2>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);

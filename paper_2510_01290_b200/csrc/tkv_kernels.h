@@ -12,6 +12,11 @@ cudaError_t tkv_launch_attend(const TkvState& st, const void* q, const void* k, 
                               float* out, int buf_half, int nbuf, int put_half, int put_slot,
                               cudaStream_t stream);
 
+// K1 tensor-core variant (k_attend_mma.cu) and its shape predicate.
+bool tkv_attend_mma_supported(const TkvDims& dm);
+cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void* k, const void* v, float* out,
+                                  int buf_half, int nbuf, int put_half, int put_slot, cudaStream_t stream);
+
 // K3a: fp64 sparsity statistics (layer_sparsity_average) over the same view.
 cudaError_t tkv_launch_score(const TkvState& st, const void* q, const void* k, int buf_half,
                              int nbuf, cudaStream_t stream);
