@@ -64,7 +64,11 @@ struct Km {
   double* sums;   // [K][D]
   double* means;  // [K][D]
   double* best;   // [K][D]
+  unsigned long long* ks;  // optional counters
 };
+__device__ __forceinline__ void kstat(const Km& km, int i, unsigned long long v) {
+  if (km.ks && threadIdx.x == 0) atomicAdd(km.ks + i, v);
+}
 
 // Stable member lists per cluster (ascending point index) from assign/sizes.
 __device__ void build_members(KmSmem& s, int m, int K) {
@@ -99,7 +103,10 @@ __device__ void kmeans_from_seeds(const Km& km, KmSmem& s) {
   }
   if (threadIdx.x == 0) s.cur = 0;
   __syncthreads();
+  long long c0 = clock64();
+  kstat(km, 0, 1);
   for (int iter = 0; iter < 50; ++iter) {
+    kstat(km, 1, 1);
     const double* cent = km.cb[s.cur];
     double* next = km.cb[s.cur ^ 1];
     // Assign; ties go to the lowest cluster index.
@@ -156,6 +163,8 @@ __device__ void kmeans_from_seeds(const Km& km, KmSmem& s) {
   }
 
   // Hartigan single moves + pairwise swaps (evictor.cpp:179-243).
+  long long c1 = clock64();
+  kstat(km, 6, (unsigned long long)(c1 - c0));
   count_sizes(s, m, K);
   build_members(s, m, K);
   for (int idx = threadIdx.x; idx < K * D; idx += kThreads) {
@@ -167,6 +176,8 @@ __device__ void kmeans_from_seeds(const Km& km, KmSmem& s) {
   }
   __syncthreads();
   for (int pass = 0; pass < 100; ++pass) {
+    kstat(km, 2, 1);
+    long long ch0 = clock64();
     bool moved = false;  // CTA-uniform
     for (int i = 0; i < m; ++i) {
       const int from = s.assign[i];
@@ -194,6 +205,7 @@ __device__ void kmeans_from_seeds(const Km& km, KmSmem& s) {
       __syncthreads();
       const int to = s.best_to;
       if (to != from) {
+        kstat(km, 3, 1);
         moved = true;
         for (int ch = threadIdx.x; ch < D; ch += kThreads) {
           const double x = km.X[i * D + ch];
@@ -205,7 +217,10 @@ __device__ void kmeans_from_seeds(const Km& km, KmSmem& s) {
       }
       __syncthreads();
     }
+    kstat(km, 7, (unsigned long long)(clock64() - ch0));
     if (moved) continue;
+    kstat(km, 4, 1);
+    long long cs0 = clock64();
     // Pairwise exchanges: the lexicographically first improving (i, j).
     if (threadIdx.x == 0) s.pair = 0x7fffffff;
     __syncthreads();
@@ -240,7 +255,9 @@ __device__ void kmeans_from_seeds(const Km& km, KmSmem& s) {
     }
     __syncthreads();
     const int p = s.pair;
+    kstat(km, 8, (unsigned long long)(clock64() - cs0));
     if (p == 0x7fffffff) break;
+    kstat(km, 5, 1);
     int i = 0, rem = p;
     while (rem >= m - 1 - i) { rem -= m - 1 - i; ++i; }
     const int j = i + 1 + rem;
@@ -259,6 +276,7 @@ __device__ void kmeans_from_seeds(const Km& km, KmSmem& s) {
     }
     __syncthreads();
   }
+  kstat(km, 9, (unsigned long long)(clock64() - c0));
   // Final centroids = member means; cost summed in point order.
   double* cent = km.cb[s.cur];
   for (int idx = threadIdx.x; idx < K * D; idx += kThreads) cent[idx] = km.means[idx];
@@ -381,6 +399,8 @@ __global__ void __launch_bounds__(kThreads) anneal_kernel(TkvState st, const Tkv
     km.sums = km.cb[1] + (int64_t)max_m * D;
     km.means = km.sums + (int64_t)max_m * D;
     km.best = km.means + (int64_t)max_m * D;
+    km.ks = st.kstats;
+    const long long i0 = clock64();
     if (!bad) {
       // Decoded fp64 keys (BlockPager::key_of, pager.cpp:280-287; exact products).
       for (int idx = threadIdx.x; idx < m * D; idx += kThreads) {
@@ -410,7 +430,9 @@ __global__ void __launch_bounds__(kThreads) anneal_kernel(TkvState st, const Tkv
     // Seed sets (kmeans_cluster, evictor.cpp:255-317).
     double subsets = 1.0;
     for (int i = 0; i < K; ++i) subsets = __dmul_rn(subsets, __ddiv_rn((double)(m - i), (double)(i + 1)));
+    kstat(km, 10, 1);
     if (subsets <= 512.0) {
+      kstat(km, 11, 1);
       if (threadIdx.x == 0)
         for (int i = 0; i < K; ++i) s.seeds[i] = i;
       __syncthreads();
@@ -457,10 +479,14 @@ __global__ void __launch_bounds__(kThreads) anneal_kernel(TkvState st, const Tkv
       }
       __syncthreads();
       for (int a = 0; a < 4; ++a) {
+        const long long f0 = clock64();
         farthest_first(km, s, anchors[a]);
+        kstat(km, 12, (unsigned long long)(clock64() - f0));
         run_seeds(km, s);
       }
     }
+    kstat(km, 13, (unsigned long long)(clock64() - i0));
+    kstat(km, 14, (unsigned long long)m);
     // Medoids: member nearest each centroid, ties to the lowest id.
     for (int c = threadIdx.x; c < K; c += kThreads) {
       int best_i = m;

@@ -1,0 +1,696 @@
+// K3d v2: bit-exact K-means medoid selection (kmeans_select, proj/src/
+// evictor.cpp:55-338) restructured for throughput.
+//
+// Three kernels per anneal wave:
+//   prep     one CTA per (unit, anneal op) "instance": decodes the segment's
+//            member keys once (exact: fp32 value x per-point fp64 scale), the
+//            exact pairwise distance matrix pd[i][j] = dist2(x_i, x_j)
+//            (evictor.cpp:57-64 order: sequential channel sum, no FMA), the
+//            mean anchors and the four farthest-first seed sets
+//            (evictor.cpp:71-92, 284-314) -- one warp per anchor, reading pd.
+//   restart  one CTA per (instance, restart): Lloyd + Hartigan moves + swaps
+//            (kmeans_from_seeds, evictor.cpp:94-251) with keys, centroids and
+//            an exact point-to-centroid distance cache D2[i][c] in shared
+//            memory.  D2 values are the reference's dist2(keys[i], mean_of(c))
+//            bit for bit (same operands, same operation order); a move
+//            invalidates exactly two columns, which are recomputed, so each
+//            Hartigan decision is an O(K) scan of cached values instead of K
+//            fresh distance evaluations.  The O(m^2 D) pairwise-swap scan is
+//            filtered with the algebraic identity
+//              delta = D2[j][a] - D2[i][a] + D2[i][b] - D2[j][b] - (1/na + 1/nb) pd[i][j]
+//            plus a margin that dominates the rounding error of both that
+//            expression and the reference's channel-wise formula by orders of
+//            magnitude; only pairs inside the margin are evaluated with the
+//            reference's exact expression, in lexicographic order.  The
+//            restart writes its cost (summed in point order) and its medoids.
+//   final    one thread per instance: the lowest-cost restart (ties to the
+//            earlier one, evictor.cpp:319-325) supplies the retained set.
+// The file is compiled with --fmad=false and every order-sensitive value uses
+// explicit _rn intrinsics.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdio>
+
+#include "tkv_codec.cuh"
+#include "tkv_kernels.h"
+#include "tkv_state.h"
+
+namespace {
+
+constexpr int kMaxM = 256;
+
+__device__ __forceinline__ int find_op(const int32_t* prefix, int nops, int item) {
+  int lo = 0, hi = nops - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (prefix[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Scratch geometry of one instance (identical formula on host and device).
+struct KmGeo {
+  int mmax, kmax, D, W, R;  // R = restart capacity per instance
+  __host__ __device__ int64_t x_off() const { return 0; }                                   // f32 [mmax][D]
+  __host__ __device__ int64_t xs_off() const { return x_off() + (int64_t)mmax * D * 4; }   // f64 [mmax]
+  __host__ __device__ int64_t pd_off() const { return xs_off() + (int64_t)mmax * 8; }      // f64 [mmax][mmax]
+  __host__ __device__ int64_t ids_off() const { return pd_off() + (int64_t)mmax * mmax * 8; }  // i32 [mmax]
+  __host__ __device__ int64_t seeds_off() const { return ids_off() + (int64_t)mmax * 4; }  // i32 [4][kmax]
+  __host__ __device__ int64_t cost_off() const { return (seeds_off() + (int64_t)4 * kmax * 4 + 7) / 8 * 8; }  // f64 [R]
+  __host__ __device__ int64_t mask_off() const { return cost_off() + (int64_t)R * 8; }     // u32 [R][W]
+  __host__ __device__ int64_t misc_off() const { return mask_off() + (int64_t)R * W * 4; }  // i32 [4]: m, bad
+  __host__ __device__ int64_t bytes() const { return (misc_off() + 16 + 255) / 256 * 256; }
+};
+
+__device__ __forceinline__ double xval(const float* X, const double* xs, int i, int ch, int D, bool scaled) {
+  const double v = (double)X[(int64_t)i * D + ch];
+  return scaled ? __dmul_rn(v, xs[i]) : v;
+}
+
+// ---------------------------------------------------------------------------
+// prep
+// ---------------------------------------------------------------------------
+__device__ void decode_point(const TkvState& st, int u, int slot, float* xrow, double* xs) {
+  const TkvDims& dm = st.dm;
+  const int64_t gs = (int64_t)u * dm.NS + slot;
+  const int fmt = dm.band_fmt[st.blk_thought[(int64_t)u * dm.P + slot / dm.bs]];
+  const uint8_t* kr = st.slot_k + gs * dm.kstride;
+  const int win = st.slot_win[gs];
+  for (int ch = 0; ch < dm.D; ++ch) {
+    float v;
+    if (fmt == TKV_FMT_RAW) {
+      v = dm.in_dtype == TKV_IN_BF16 ? __uint_as_float(((uint32_t) reinterpret_cast<const uint16_t*>(kr)[ch]) << 16)
+                                      : reinterpret_cast<const float*>(kr)[ch];
+    } else if (fmt == TKV_FMT_FP8) {
+      v = (float)tkv_e4m3_decode((uint8_t)kr[ch]);
+    } else {
+      // code x E4M3 scale: <= 7 significant bits, exact in fp32 (and fp64).
+      v = (float)tkv_decode_code(fmt, tkv_get_code(kr, fmt, ch),
+                                 tkv_e4m3_decode(st.win_ks[((int64_t)u * dm.NW + win) * dm.D + ch]));
+    }
+    xrow[ch] = v;
+  }
+  *xs = fmt == TKV_FMT_FP8 ? (double)st.win_kf[(int64_t)u * dm.NW + win] : 1.0;
+}
+
+__global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
+                                                      const int32_t* __restrict__ prefix, int nitems, int item0,
+                                                      uint8_t* __restrict__ scratch, KmGeo geo, int scaled_any) {
+  const TkvDims& dm = st.dm;
+  const int item = item0 + blockIdx.x;
+  if (item >= nitems) return;
+  const int oi = find_op(prefix, nops, item);
+  const TkvAnnealOp op = ops[oi];
+  const int urel = item - prefix[oi];
+  const int u = op.unit0 + urel;
+  const int D = dm.D;
+  uint8_t* base = scratch + (int64_t)blockIdx.x * geo.bytes();
+  float* X = reinterpret_cast<float*>(base + geo.x_off());
+  double* xs = reinterpret_cast<double*>(base + geo.xs_off());
+  double* pd = reinterpret_cast<double*>(base + geo.pd_off());
+  int32_t* ids = reinterpret_cast<int32_t*>(base + geo.ids_off());
+  int32_t* seeds = reinterpret_cast<int32_t*>(base + geo.seeds_off());
+  int32_t* misc = reinterpret_cast<int32_t*>(base + geo.misc_off());
+  __shared__ int sids[kMaxM];
+  __shared__ int sm_m, sm_bad;
+  __shared__ double dmean[kMaxM];
+  __shared__ int anchors[4];
+  const uint32_t* segm = st.seg_mask + ((int64_t)u * dm.NSEG + op.seg) * dm.W;
+  if (threadIdx.x == 0) {
+    int m = 0;
+    for (int b = 0; b < op.span && m < kMaxM; ++b)
+      if ((segm[b >> 5] >> (b & 31)) & 1u) sids[m++] = b;
+    sm_m = m;
+    int bad = (m != op.m) || st.err[u] != 0;
+    for (int i = 0; i < m && !bad; ++i) bad |= st.tok_slot[(int64_t)u * dm.T + op.seg_start + sids[i]] < 0;
+    sm_bad = bad;
+    misc[0] = m;
+    misc[1] = bad;
+  }
+  __syncthreads();
+  if (sm_bad) return;
+  const int m = sm_m, K = op.K;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    ids[i] = sids[i];
+    decode_point(st, u, st.tok_slot[(int64_t)u * dm.T + op.seg_start + sids[i]], X + (int64_t)i * D, xs + i);
+  }
+  __syncthreads();
+  const bool scaled = scaled_any != 0;
+  // exact pairwise distances (symmetric: (a-b)^2 == (b-a)^2 in IEEE)
+  const int npairs = m * (m - 1) / 2;
+  for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+    int i = 0, rem = p;
+    while (rem >= m - 1 - i) { rem -= m - 1 - i; ++i; }
+    const int j = i + 1 + rem;
+    double d = 0.0;
+    for (int ch = 0; ch < D; ++ch) {
+      const double t = __dsub_rn(xval(X, xs, i, ch, D, scaled), xval(X, xs, j, ch, D, scaled));
+      d = __dadd_rn(d, __dmul_rn(t, t));
+    }
+    pd[(int64_t)i * geo.mmax + j] = d;
+    pd[(int64_t)j * geo.mmax + i] = d;
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) pd[(int64_t)i * geo.mmax + i] = 0.0;
+  if (op.nrestart <= 0) return;  // exhaustive seeds: nothing else to prepare
+  __syncthreads();
+  // anchors: 0, farthest from / nearest to the mean, m/2 (evictor.cpp:296-313)
+  __shared__ double mean[256];
+  for (int ch = threadIdx.x; ch < D; ch += blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < m; ++i) acc = __dadd_rn(acc, xval(X, xs, i, ch, D, scaled));
+    mean[ch] = __ddiv_rn(acc, (double)m);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    double d = 0.0;
+    for (int ch = 0; ch < D; ++ch) {
+      const double t = __dsub_rn(xval(X, xs, i, ch, D, scaled), mean[ch]);
+      d = __dadd_rn(d, __dmul_rn(t, t));
+    }
+    dmean[i] = d;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int far_idx = 0, near_idx = 0;
+    double far_d = -1.0, near_d = CUDART_INF;
+    for (int i = 0; i < m; ++i) {
+      const double d = dmean[i];
+      if (d > far_d) { far_d = d; far_idx = i; }
+      if (d < near_d) { near_d = d; near_idx = i; }
+    }
+    anchors[0] = 0;
+    anchors[1] = far_idx;
+    anchors[2] = near_idx;
+    anchors[3] = m / 2;
+  }
+  __syncthreads();
+  // farthest-first per anchor: one warp each over the precomputed pd.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < 4) {
+    __shared__ double nearest[4][kMaxM];
+    __shared__ unsigned char taken[4][kMaxM];
+    double* nr = nearest[warp];
+    unsigned char* tk = taken[warp];
+    int32_t* sd = seeds + warp * geo.kmax;
+    for (int i = lane; i < m; i += 32) { nr[i] = CUDART_INF; tk[i] = 0; }
+    int last = anchors[warp];
+    if (lane == 0) { sd[0] = last; }
+    __syncwarp();
+    if (lane == 0) tk[last] = 1;
+    __syncwarp();
+    for (int n = 1; n < K; ++n) {
+      double best_d = -1.0;
+      int best_i = 0x7fffffff;
+      for (int i = lane; i < m; i += 32) {
+        const double d = pd[(int64_t)i * geo.mmax + last];
+        const double v = d < nr[i] ? d : nr[i];
+        nr[i] = v;
+        if (!tk[i] && v > best_d) { best_d = v; best_i = i; }
+      }
+      // first index of the maximum among untaken points
+      for (int o = 16; o > 0; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
+        const int oi2 = __shfl_xor_sync(0xffffffffu, best_i, o);
+        if (od > best_d || (od == best_d && oi2 < best_i)) { best_d = od; best_i = oi2; }
+      }
+      if (best_i == 0x7fffffff) best_i = 0;  // (far initialised to 0, evictor.cpp:80)
+      last = best_i;
+      if (lane == 0) { sd[n] = last; tk[last] = 1; }
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// restart
+// ---------------------------------------------------------------------------
+struct RsSmem {
+  int assign[kMaxM];
+  int sizes[kMaxM];
+  int order[kMaxM];
+  int offs[kMaxM + 1];
+  int cur[kMaxM];
+  int seeds[kMaxM];
+  double coef_add[kMaxM];  // nb / (nb + 1)
+  double coef_rem[kMaxM];  // -na / (na - 1)
+  double mv[kMaxM];
+  int flag, move_i, move_to, pair;
+  double cost;
+};
+
+// D2[i][c] for all points and the given centroid rows (exact dist2).
+template <int NT>
+__device__ void fill_d2(const float* X, const double* xs, bool scaled, const double* C, int cstride, double* D2,
+                        int m, int K, int D) {
+  // warp task = 4 points x 64 centroids (lane l -> centroids l, l + 32)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pblocks = (m + 3) / 4, cgroups = (K + 63) / 64;
+  for (int task = warp; task < pblocks * cgroups; task += NT / 32) {
+    const int pb = task / cgroups, cg = task % cgroups;
+    const int c0 = cg * 64 + lane, c1 = c0 + 32;
+    const bool v0 = c0 < K, v1 = c1 < K;
+    const double* r0 = C + (int64_t)(v0 ? c0 : 0) * cstride;
+    const double* r1 = C + (int64_t)(v1 ? c1 : 0) * cstride;
+    int ip[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ip[q] = min(pb * 4 + q, m - 1);
+    double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int ch = 0; ch < D; ++ch) {
+      const double a0 = r0[ch], a1 = r1[ch];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double x = xval(X, xs, ip[q], ch, D, scaled);
+        const double t0 = __dsub_rn(x, a0), t1 = __dsub_rn(x, a1);
+        d[q][0] = __dadd_rn(d[q][0], __dmul_rn(t0, t0));
+        d[q][1] = __dadd_rn(d[q][1], __dmul_rn(t1, t1));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = pb * 4 + q;
+      if (i >= m) break;
+      if (v0) D2[(int64_t)i * K + c0] = d[q][0];
+      if (v1) D2[(int64_t)i * K + c1] = d[q][1];
+    }
+  }
+}
+
+// Recompute D2 columns a and b (after a move or swap changed those means).
+template <int NT>
+__device__ void refresh_cols(const float* X, const double* xs, bool scaled, const double* C, int cstride, double* D2,
+                             int m, int K, int D, int a, int b) {
+  for (int t = threadIdx.x; t < 2 * m; t += NT) {
+    const int i = t >> 1, c = (t & 1) ? b : a;
+    const double* cr = C + (int64_t)c * cstride;
+    double d = 0.0;
+    for (int ch = 0; ch < D; ++ch) {
+      const double tt = __dsub_rn(xval(X, xs, i, ch, D, scaled), cr[ch]);
+      d = __dadd_rn(d, __dmul_rn(tt, tt));
+    }
+    D2[(int64_t)i * K + c] = d;
+  }
+}
+
+// Member lists per cluster in ascending point order (offs/order).
+__device__ void members(RsSmem& s, int m, int K) {
+  if (threadIdx.x == 0) {
+    s.offs[0] = 0;
+    for (int c = 0; c < K; ++c) {
+      s.offs[c + 1] = s.offs[c] + s.sizes[c];
+      s.cur[c] = s.offs[c];
+    }
+    for (int i = 0; i < m; ++i) s.order[s.cur[s.assign[i]]++] = i;
+  }
+  __syncthreads();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
+                                                        const int32_t* __restrict__ rprefix, int nruns, int run0,
+                                                        const int32_t* __restrict__ item_prefix, int item0,
+                                                        uint8_t* __restrict__ scratch, KmGeo geo,
+                                                        double* __restrict__ gsums, int scaled_any) {
+  const TkvDims& dm = st.dm;
+  const int run = run0 + blockIdx.x;
+  if (run >= nruns) return;
+  // run -> (op, unit, restart): rprefix[op] = first run of op; runs of an op
+  // are unit-major: run = rprefix[op] + urel * nrestart_eff + r.
+  const int oi = find_op(rprefix, nops, run);
+  const TkvAnnealOp op = ops[oi];
+  const int nr = op.nrestart > 0 ? op.nrestart : op.ncombos;
+  const int local = run - rprefix[oi];
+  const int urel = local / nr, r = local % nr;
+  const int item = item_prefix[oi] + urel - item0;  // scratch slot of the instance
+  uint8_t* base = scratch + (int64_t)item * geo.bytes();
+  const int32_t* misc = reinterpret_cast<const int32_t*>(base + geo.misc_off());
+  if (misc[1]) return;
+  const int m = misc[0], K = op.K, D = dm.D;
+  const bool scaled = scaled_any != 0;
+  extern __shared__ __align__(16) uint8_t dyn[];
+  __shared__ RsSmem s;
+  // smem: X f32 [m][D] | means f64 [K][D] | D2 f64 [m][K]
+  float* X = reinterpret_cast<float*>(dyn);
+  double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)geo.mmax * D * 4 + 15) / 16 * 16));
+  double* D2 = Mn + (int64_t)geo.kmax * D;
+  __shared__ double xs[kMaxM];
+  double* S = gsums + (int64_t)blockIdx.x * geo.kmax * D;  // sums / next (global, per CTA)
+  const float* gX = reinterpret_cast<const float*>(base + geo.x_off());
+  const double* gxs = reinterpret_cast<const double*>(base + geo.xs_off());
+  const double* pd = reinterpret_cast<const double*>(base + geo.pd_off());
+  for (int i = threadIdx.x; i < m * D; i += NT) X[i] = gX[i];
+  for (int i = threadIdx.x; i < m; i += NT) xs[i] = gxs[i];
+  if (threadIdx.x == 0) {
+    if (op.nrestart > 0) {
+      const int32_t* sd = reinterpret_cast<const int32_t*>(base + geo.seeds_off()) + r * geo.kmax;
+      for (int c = 0; c < K; ++c) s.seeds[c] = sd[c];
+    } else {
+      // r-th K-subset of {0..m-1} in lexicographic order (evictor.cpp:274-283)
+      int rank = r, x = 0;
+      for (int c = 0; c < K; ++c) {
+        while (true) {
+          // number of subsets starting with x at position c
+          double cnt = 1.0;
+          const int n = m - x - 1, k = K - c - 1;
+          for (int t = 0; t < k; ++t) cnt = cnt * (double)(n - t) / (double)(t + 1);
+          const int ci = (int)(cnt + 0.5);
+          if (rank < ci) break;
+          rank -= ci;
+          ++x;
+        }
+        s.seeds[c] = x;
+        ++x;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- Lloyd (evictor.cpp:102-159) ----------------------------------------
+  for (int idx = threadIdx.x; idx < K * D; idx += NT) {
+    const int c = idx / D, ch = idx % D;
+    Mn[idx] = xval(X, xs, s.seeds[c], ch, D, scaled);
+  }
+  __syncthreads();
+  for (int iter = 0; iter < 50; ++iter) {
+    fill_d2<NT>(X, xs, scaled, Mn, D, D2, m, K, D);
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += NT) {
+      const double* row = D2 + (int64_t)i * K;
+      int best = 0;
+      double bd = row[0];
+      for (int c = 1; c < K; ++c)
+        if (row[c] < bd) { bd = row[c]; best = c; }
+      s.assign[i] = best;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < K; ++c) s.sizes[c] = 0;
+      for (int i = 0; i < m; ++i) ++s.sizes[s.assign[i]];
+      for (int c = 0; c < K; ++c) {  // empty-cluster repair (evictor.cpp:123-141)
+        if (s.sizes[c] > 0) continue;
+        int donor = 0;
+        for (int d2 = 1; d2 < K; ++d2)
+          if (s.sizes[d2] > s.sizes[donor]) donor = d2;
+        int steal = m;
+        double steal_d = -1.0;
+        for (int i = 0; i < m; ++i) {
+          if (s.assign[i] != donor) continue;
+          const double d = D2[(int64_t)i * K + donor];
+          if (d > steal_d) { steal = i; steal_d = d; }
+        }
+        s.assign[steal] = c;
+        --s.sizes[donor];
+        ++s.sizes[c];
+      }
+    }
+    __syncthreads();
+    members(s, m, K);
+    for (int idx = threadIdx.x; idx < K * D; idx += NT) {
+      const int c = idx / D, ch = idx % D;
+      double acc = 0.0;
+      for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, D, scaled));
+      S[idx] = __ddiv_rn(acc, (double)s.sizes[c]);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < K; c += NT) {
+      double d = 0.0;
+      for (int ch = 0; ch < D; ++ch) {
+        const double t = __dsub_rn(S[(int64_t)c * D + ch], Mn[(int64_t)c * D + ch]);
+        d = __dadd_rn(d, __dmul_rn(t, t));
+      }
+      s.mv[c] = __dsqrt_rn(d);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double movement = 0.0;
+      for (int c = 0; c < K; ++c) movement = movement < s.mv[c] ? s.mv[c] : movement;
+      s.flag = movement < 1e-6;
+    }
+    for (int idx = threadIdx.x; idx < K * D; idx += NT) Mn[idx] = S[idx];
+    __syncthreads();
+    if (s.flag) break;
+  }
+  // ---- Hartigan (evictor.cpp:167-243) --------------------------------------
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < K; ++c) s.sizes[c] = 0;
+    for (int i = 0; i < m; ++i) ++s.sizes[s.assign[i]];
+  }
+  __syncthreads();
+  members(s, m, K);
+  for (int idx = threadIdx.x; idx < K * D; idx += NT) {
+    const int c = idx / D, ch = idx % D;
+    double acc = 0.0;
+    for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, D, scaled));
+    S[idx] = acc;
+    Mn[idx] = __ddiv_rn(acc, (double)s.sizes[c]);
+  }
+  for (int c = threadIdx.x; c < K; c += NT) {
+    const double n = (double)s.sizes[c];
+    s.coef_add[c] = __ddiv_rn(n, __dadd_rn(n, 1.0));
+    s.coef_rem[c] = __ddiv_rn(-n, __dsub_rn(n, 1.0));
+  }
+  __syncthreads();
+  fill_d2<NT>(X, xs, scaled, Mn, D, D2, m, K, D);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int pass = 0; pass < 100; ++pass) {
+    bool moved = false;  // CTA-uniform
+    int start = 0;
+    while (true) {
+      // warp 0 scans points in order with the cached distances until the
+      // first improving single move (no state changes before it).
+      if (warp == 0) {
+        int mi = -1, mto = -1;
+        for (int i = start; i < m; ++i) {
+          const int from = s.assign[i];
+          if (s.sizes[from] <= 1) continue;
+          const double* row = D2 + (int64_t)i * K;
+          const double removal = __dmul_rn(s.coef_rem[from], row[from]);
+          double bd = -1e-12;
+          int bt = 0x7fffffff;
+          for (int to = lane; to < K; to += 32) {
+            if (to == from) continue;
+            const double delta = __dadd_rn(removal, __dmul_rn(s.coef_add[to], row[to]));
+            if (delta < bd) { bd = delta; bt = to; }
+          }
+          for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+            const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+            if (od < bd || (od == bd && ot < bt)) { bd = od; bt = ot; }
+          }
+          if (bt != 0x7fffffff) { mi = i; mto = bt; break; }
+        }
+        if (lane == 0) { s.move_i = mi; s.move_to = mto; }
+      }
+      __syncthreads();
+      const int i = s.move_i, to = s.move_to;
+      if (i < 0) break;
+      const int from = s.assign[i];
+      moved = true;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        --s.sizes[from];
+        ++s.sizes[to];
+        s.assign[i] = to;
+        const double nf = (double)s.sizes[from], nt = (double)s.sizes[to];
+        s.coef_add[from] = __ddiv_rn(nf, __dadd_rn(nf, 1.0));
+        s.coef_rem[from] = __ddiv_rn(-nf, __dsub_rn(nf, 1.0));
+        s.coef_add[to] = __ddiv_rn(nt, __dadd_rn(nt, 1.0));
+        s.coef_rem[to] = __ddiv_rn(-nt, __dsub_rn(nt, 1.0));
+      }
+      for (int ch = threadIdx.x; ch < D; ch += NT) {
+        const double x = xval(X, xs, i, ch, D, scaled);
+        S[(int64_t)from * D + ch] = __dsub_rn(S[(int64_t)from * D + ch], x);
+        S[(int64_t)to * D + ch] = __dadd_rn(S[(int64_t)to * D + ch], x);
+      }
+      __syncthreads();
+      for (int ch = threadIdx.x; ch < D; ch += NT) {
+        Mn[(int64_t)from * D + ch] = __ddiv_rn(S[(int64_t)from * D + ch], (double)s.sizes[from]);
+        Mn[(int64_t)to * D + ch] = __ddiv_rn(S[(int64_t)to * D + ch], (double)s.sizes[to]);
+      }
+      __syncthreads();
+      refresh_cols<NT>(X, xs, scaled, Mn, D, D2, m, K, D, from, to);
+      __syncthreads();
+      start = i + 1;
+    }
+    if (moved) continue;
+    // ---- pairwise swaps: first improving (i, j) in lexicographic order ------
+    if (threadIdx.x == 0) s.pair = 0x7fffffff;
+    __syncthreads();
+    const int npairs = m * (m - 1) / 2;
+    for (int p = threadIdx.x; p < npairs; p += NT) {
+      if (p > *((volatile int*)&s.pair)) break;
+      int i = 0, rem = p;
+      while (rem >= m - 1 - i) { rem -= m - 1 - i; ++i; }
+      const int j = i + 1 + rem;
+      const int a = s.assign[i], b = s.assign[j];
+      if (a == b) continue;
+      const double na = (double)s.sizes[a], nb = (double)s.sizes[b];
+      const double w = 1.0 / na + 1.0 / nb;
+      const double dja = D2[(int64_t)j * K + a], dia = D2[(int64_t)i * K + a];
+      const double dib = D2[(int64_t)i * K + b], djb = D2[(int64_t)j * K + b];
+      const double pij = pd[(int64_t)i * geo.mmax + j];
+      const double approx = dja - dia + dib - djb - w * pij;
+      const double margin = 1e-6 * (dja + dia + dib + djb + w * pij) + 1e-9;
+      if (approx >= -1e-12 + margin) continue;
+      // exact reference expression (evictor.cpp:215-228)
+      const double* mua = Mn + (int64_t)a * D;
+      const double* mub = Mn + (int64_t)b * D;
+      double delta = 0.0;
+      for (int ch = 0; ch < D; ++ch) {
+        const double xi = xval(X, xs, i, ch, D, scaled), xj = xval(X, xs, j, ch, D, scaled);
+        const double ma = __dadd_rn(mua[ch], __ddiv_rn(__dsub_rn(xj, xi), na));
+        const double mb = __dadd_rn(mub[ch], __ddiv_rn(__dsub_rn(xi, xj), nb));
+        const double xx = __dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi));
+        const double yy = __dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj));
+        delta = __dadd_rn(delta, __dsub_rn(xx, __dmul_rn(na, __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua[ch], mua[ch])))));
+        delta = __dadd_rn(delta, __dsub_rn(yy, __dmul_rn(nb, __dsub_rn(__dmul_rn(mb, mb), __dmul_rn(mub[ch], mub[ch])))));
+      }
+      if (delta < -1e-12) {
+        atomicMin(&s.pair, p);
+        break;
+      }
+    }
+    __syncthreads();
+    const int p = s.pair;
+    if (p == 0x7fffffff) break;
+    int i = 0, rem = p;
+    while (rem >= m - 1 - i) { rem -= m - 1 - i; ++i; }
+    const int j = i + 1 + rem;
+    const int a = s.assign[i], b = s.assign[j];
+    for (int ch = threadIdx.x; ch < D; ch += NT) {
+      const double xi = xval(X, xs, i, ch, D, scaled), xj = xval(X, xs, j, ch, D, scaled);
+      S[(int64_t)a * D + ch] = __dadd_rn(__dsub_rn(S[(int64_t)a * D + ch], xi), xj);
+      S[(int64_t)b * D + ch] = __dsub_rn(__dadd_rn(S[(int64_t)b * D + ch], xi), xj);
+      Mn[(int64_t)a * D + ch] = __ddiv_rn(S[(int64_t)a * D + ch], (double)s.sizes[a]);
+      Mn[(int64_t)b * D + ch] = __ddiv_rn(S[(int64_t)b * D + ch], (double)s.sizes[b]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s.assign[i] = b;
+      s.assign[j] = a;
+    }
+    refresh_cols<NT>(X, xs, scaled, Mn, D, D2, m, K, D, a, b);
+    __syncthreads();
+  }
+  // ---- cost (point order) and medoids --------------------------------------
+  if (threadIdx.x == 0) {
+    double c = 0.0;
+    for (int i = 0; i < m; ++i) c = __dadd_rn(c, D2[(int64_t)i * K + s.assign[i]]);
+    s.cost = c;
+  }
+  for (int c = threadIdx.x; c < K; c += NT) {
+    int bi = m;
+    double bd = CUDART_INF;
+    for (int i = 0; i < m; ++i) {
+      if (s.assign[i] != c) continue;
+      const double d = D2[(int64_t)i * K + c];
+      if (d < bd) { bd = d; bi = i; }
+    }
+    s.order[c] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double* cost = reinterpret_cast<double*>(base + geo.cost_off());
+    uint32_t* mask = reinterpret_cast<uint32_t*>(base + geo.mask_off()) + (int64_t)r * geo.W;
+    const int32_t* ids = reinterpret_cast<const int32_t*>(base + geo.ids_off());
+    for (int w = 0; w < geo.W; ++w) mask[w] = 0;
+    for (int c = 0; c < K; ++c) {
+      const int b = ids[s.order[c]];
+      mask[b >> 5] |= 1u << (b & 31);
+    }
+    cost[r] = s.cost;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// final: lowest cost restart -> retained mask, eviction log, segment mask
+// ---------------------------------------------------------------------------
+__global__ void km_final_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
+                                const int32_t* __restrict__ prefix, int nitems, int item0,
+                                const uint8_t* __restrict__ scratch, KmGeo geo, uint32_t* __restrict__ log) {
+  const TkvDims& dm = st.dm;
+  const int li = blockIdx.x * blockDim.x + threadIdx.x;
+  const int item = item0 + li;
+  if (item >= nitems || li >= (int)gridDim.x * (int)blockDim.x) return;
+  const int oi = find_op(prefix, nops, item);
+  const TkvAnnealOp op = ops[oi];
+  const int urel = item - prefix[oi];
+  const int u = op.unit0 + urel;
+  const int W = dm.W;
+  uint32_t* segm = st.seg_mask + ((int64_t)u * dm.NSEG + op.seg) * W;
+  uint32_t* logm = log + op.log_off + (int64_t)urel * W;
+  const uint8_t* base = scratch + (int64_t)li * geo.bytes();
+  const int32_t* misc = reinterpret_cast<const int32_t*>(base + geo.misc_off());
+  if (misc[1]) {
+    if (st.err[u] == 0) st.err[u] = TKV_E_INTEGRITY;
+    for (int w = 0; w < W; ++w) logm[w] = 0;
+    return;
+  }
+  const int nr = op.nrestart > 0 ? op.nrestart : op.ncombos;
+  const double* cost = reinterpret_cast<const double*>(base + geo.cost_off());
+  int best = 0;
+  for (int r = 1; r < nr; ++r)
+    if (cost[r] < cost[best]) best = r;
+  const uint32_t* keep = reinterpret_cast<const uint32_t*>(base + geo.mask_off()) + (int64_t)best * W;
+  for (int w = 0; w < W; ++w) {
+    const uint32_t valid = w * 32 >= op.span ? 0u : (op.span - w * 32 >= 32 ? 0xffffffffu : ((1u << (op.span - w * 32)) - 1u));
+    const uint32_t old = segm[w] & valid;
+    logm[w] = old & ~keep[w];
+    segm[w] = keep[w];
+  }
+}
+
+}  // namespace
+
+// Host-side planning helpers --------------------------------------------------
+int64_t tkv_km_instance_bytes(int mmax, int kmax, int D, int W, int R) {
+  KmGeo g{mmax, kmax, D, W, R};
+  return g.bytes();
+}
+
+size_t tkv_km_restart_smem(int mmax, int kmax, int D) {
+  return (size_t)(((int64_t)mmax * D * 4 + 15) / 16 * 16) + (size_t)kmax * D * 8 + (size_t)mmax * kmax * 8;
+}
+
+cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int nops, const int32_t* item_prefix,
+                              int nitems, const int32_t* run_prefix, int nruns, int item0, int item_count,
+                              int run0, int run_count, int mmax, int kmax, int R, uint8_t* scratch, double* gsums,
+                              int gsums_ctas, uint32_t* log, int scaled_any, cudaStream_t stream) {
+  KmGeo geo{mmax, kmax, st.dm.D, st.dm.W, R};
+  km_prep_kernel<<<item_count, 256, 0, stream>>>(st, ops, nops, item_prefix, nitems, item0, scratch, geo, scaled_any);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[kmeans] prep launch failed: items=%d: %s\n", item_count, cudaGetErrorString(e));
+    return e;
+  }
+  const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D);
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // tau x d beyond the smem design point
+  // runs are processed in chunks of gsums_ctas CTAs (one global sums buffer each)
+  for (int r = 0; r < run_count; r += gsums_ctas) {
+    const int n = run_count - r < gsums_ctas ? run_count - r : gsums_ctas;
+    if (mmax <= 32) {
+      if (smem > 16 * 1024) {  // static (~14 KB) + dynamic must opt in beyond 48 KB
+        e = cudaFuncSetAttribute(km_restart_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      km_restart_kernel<64><<<n, 64, smem, stream>>>(st, ops, nops, run_prefix, run0 + run_count, run0 + r,
+                                                      item_prefix, item0, scratch, geo, gsums, scaled_any);
+    } else {
+      if (smem > 16 * 1024) {  // static (~14 KB) + dynamic must opt in beyond 48 KB
+        e = cudaFuncSetAttribute(km_restart_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      km_restart_kernel<256><<<n, 256, smem, stream>>>(st, ops, nops, run_prefix, run0 + run_count, run0 + r,
+                                                        item_prefix, item0, scratch, geo, gsums, scaled_any);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      fprintf(stderr, "[kmeans] restart launch failed: n=%d smem=%zu mmax=%d kmax=%d R=%d: %s\n", n, smem, mmax, kmax, R,
+              cudaGetErrorString(e));
+      return e;
+    }
+  }
+  km_final_kernel<<<(item_count + 127) / 128, 128, 0, stream>>>(st, ops, nops, item_prefix, item0 + item_count, item0,
+                                                                 scratch, geo, log);
+  return cudaGetLastError();
+}

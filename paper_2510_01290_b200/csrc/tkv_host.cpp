@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -168,6 +169,10 @@ struct tkv_run {
   uint32_t* d_log = nullptr;
   int64_t log_cap = 0, log_used = 0;
   double* d_scratch = nullptr;
+  uint8_t* km_scratch = nullptr;   // K-means v2 per-instance scratch (grown on demand)
+  int64_t km_scratch_bytes = 0;
+  double* km_sums = nullptr;       // per restart-CTA sums rows
+  int km_sums_ctas = 0;
   int scratch_ctas = 0;
   int64_t scratch_per_cta = 0;
   int max_m = 0;
@@ -414,6 +419,13 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
       op.span = (int32_t)s.initial;
       op.m = (int32_t)o.m;
       op.K = (int32_t)o.K;
+      // seed sets (kmeans_cluster, evictor.cpp:266-314): every K-subset when
+      // C(m, K) <= 512 (computed exactly as the reference does), else 4
+      // farthest-first restarts.
+      double subsets = 1.0;
+      for (int64_t i = 0; i < o.K; ++i) subsets *= (double)(o.m - i) / (double)(i + 1);
+      op.nrestart = subsets <= 512.0 ? 0 : 4;
+      op.ncombos = subsets <= 512.0 ? (int32_t)std::llround(subsets) : 0;
       const int64_t need = (int64_t)g.nunits * W;
       if (r->log_used + need > r->log_cap) throw TkvError(TKV_ERR_UNEXPECTED, "eviction log capacity exceeded");
       op.log_off = (int32_t)r->log_used;
@@ -423,16 +435,62 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
       per_group[pi].push_back({o.seg_idx, op});
     }
   }
+  const TkvDims& dm = r->st.dm;
+  bool f64_raw = false, fp8 = false;
+  for (int b = 0; b < dm.num_bands; ++b) {
+    f64_raw = f64_raw || (dm.band_fmt[b] == TKV_FMT_RAW && dm.in_dtype == TKV_IN_F64);
+    fp8 = fp8 || dm.band_fmt[b] == TKV_FMT_FP8;
+  }
   for (auto& wv : waves) {
-    std::vector<int32_t> prefix(wv.size());
-    int32_t items = 0;
-    for (size_t i = 0; i < wv.size(); ++i) { prefix[i] = items; items += wv[i].nunits; }
+    std::vector<int32_t> prefix(wv.size()), rprefix(wv.size());
+    int32_t items = 0, runs = 0;
+    int mmax = 1, kmax = 1, R = 1;
+    for (size_t i = 0; i < wv.size(); ++i) {
+      prefix[i] = items;
+      rprefix[i] = runs;
+      const int nr = wv[i].nrestart > 0 ? wv[i].nrestart : wv[i].ncombos;
+      items += wv[i].nunits;
+      runs += wv[i].nunits * nr;
+      mmax = std::max(mmax, (int)wv[i].m);
+      kmax = std::max(kmax, (int)wv[i].K);
+      R = std::max(R, nr);
+    }
     TkvAnnealOp* d_ops = upload(r, wv.data(), wv.size());
     int32_t* d_pre = upload(r, prefix.data(), prefix.size());
-    launch(r, CAT_ANNEAL, "anneal kernel", [&] {
-      return tkv_launch_anneal(r->st, d_ops, (int)wv.size(), d_pre, items, r->d_log, r->d_scratch,
-                               r->scratch_ctas, r->scratch_per_cta, r->max_m, r->stream);
-    });
+    if (f64_raw) {  // raw fp64 keys are not representable in the v2 key store
+      launch(r, CAT_ANNEAL, "anneal kernel", [&] {
+        return tkv_launch_anneal(r->st, d_ops, (int)wv.size(), d_pre, items, r->d_log, r->d_scratch,
+                                 r->scratch_ctas, r->scratch_per_cta, r->max_m, r->stream);
+      });
+      continue;
+    }
+    int32_t* d_rpre = upload(r, rprefix.data(), rprefix.size());
+    const int64_t inst = tkv_km_instance_bytes(mmax, kmax, dm.D, dm.W, R);
+    const int64_t want = inst * std::min<int64_t>(items, 16384);
+    if (want > r->km_scratch_bytes) {
+      CUDA_OK(cudaStreamSynchronize(r->stream));
+      if (r->km_scratch) CUDA_OK(cudaFree(r->km_scratch));
+      CUDA_OK(cudaMalloc(&r->km_scratch, want));
+      r->km_scratch_bytes = want;
+    }
+    const int per_chunk = (int)std::max<int64_t>(1, r->km_scratch_bytes / inst);
+    for (int i0 = 0; i0 < items; i0 += per_chunk) {
+      const int cnt = std::min(per_chunk, items - i0);
+      // runs of items [i0, i0 + cnt): ops are item-contiguous and runs are
+      // (op, unit, restart)-ordered, so they form one contiguous range.
+      auto run_of_item = [&](int item) {
+        int o = (int)(std::upper_bound(prefix.begin(), prefix.end(), item) - prefix.begin()) - 1;
+        const int nr = wv[o].nrestart > 0 ? wv[o].nrestart : wv[o].ncombos;
+        return rprefix[o] + (item - prefix[o]) * nr;
+      };
+      const int run0 = run_of_item(i0);
+      const int run1 = i0 + cnt < items ? run_of_item(i0 + cnt) : runs;
+      launch(r, CAT_ANNEAL, "kmeans kernels", [&] {
+        return tkv_launch_kmeans(r->st, d_ops, (int)wv.size(), d_pre, items, d_rpre, runs, i0, cnt, run0,
+                                 run1 - run0, mmax, kmax, R, r->km_scratch, r->km_sums, r->km_sums_ctas, r->d_log,
+                                 fp8 ? 1 : 0, r->stream);
+      });
+    }
   }
   std::vector<TkvAnnealOp> aops;
   std::vector<TkvApplyGroup> ag;
@@ -1003,6 +1061,8 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   st.seg_mask = dalloc<uint32_t>(r, U * dm.NSEG * dm.W, 0xFF);
   st.buf = dalloc<uint8_t>(r, U * 4 * (size_t)dm.g * dm.D * dm.in_bytes, 0);
   st.sparsity = dalloc<double>(r, U);
+  st.kstats = nullptr;
+  if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 16, 0);
   st.err = dalloc<int32_t>(r, U);
   check_launch(tkv_launch_init(st, r->stream), "init kernel");
   // arenas
@@ -1018,9 +1078,15 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   r->log_cap = ops_bound * (int64_t)U * dm.W;
   r->d_log = dalloc<uint32_t>(r, r->log_cap, 0);
   r->max_m = std::max<int>(d.tau, 1);
-  r->scratch_per_cta = (int64_t)6 * r->max_m * dm.D;
-  r->scratch_ctas = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, U));
+  bool f64_raw = false;
+  for (int b = 0; b < d.num_thoughts; ++b)
+    f64_raw = f64_raw || (dm.band_fmt[b] == TKV_FMT_RAW && dm.in_dtype == TKV_IN_F64);
+  // v1 anneal scratch only for raw fp64 keys; everything else runs K-means v2.
+  r->scratch_per_cta = f64_raw ? (int64_t)6 * r->max_m * dm.D : 1;
+  r->scratch_ctas = f64_raw ? (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, U)) : 1;
   r->d_scratch = dalloc<double>(r, (size_t)r->scratch_ctas * r->scratch_per_cta);
+  r->km_sums_ctas = 1024;
+  r->km_sums = dalloc<double>(r, (size_t)r->km_sums_ctas * std::max(1, r->max_m - 1) * dm.D);
   // groups = sequences
   for (int s = 0; s < d.num_seqs; ++s) {
     Group g;
@@ -1035,6 +1101,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
 void destroy_run(tkv_run* r) {
   if (r->stream) cudaStreamSynchronize(r->stream);
   for (void* p : r->allocations) cudaFree(p);
+  if (r->km_scratch) cudaFree(r->km_scratch);
   for (auto& t : r->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
@@ -1280,6 +1347,14 @@ int tkv_timing_enable(tkv_run* run, int enable) {
 int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
   try {
     drain_timing(run);
+    if (run->st.kstats) {
+      unsigned long long k[16];
+      CUDA_OK(cudaMemcpy(k, run->st.kstats, sizeof(k), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[kstats] inst=%llu exh=%llu restarts=%llu lloyd_it=%llu hart_pass=%llu moves=%llu swapscans=%llu swaps=%llu "
+              "cyc: lloyd=%llu hartmove=%llu swapscan=%llu restart=%llu ff=%llu inst=%llu sum_m=%llu\n",
+              k[10], k[11], k[0], k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8], k[9], k[12], k[13], k[14]);
+      CUDA_OK(cudaMemset(run->st.kstats, 0, sizeof(k)));
+    }
     out->attend_ms = run->acc_ms[CAT_ATTEND];
     out->score_ms = run->acc_ms[CAT_SCORE];
     out->flush_ms = run->acc_ms[CAT_FLUSH];

@@ -88,6 +88,7 @@ struct TkvState {
   uint8_t* buf;          // [U][2][2 (k,v)][g][D] * in_bytes
   // per-unit outputs of the score kernel and sticky device errors
   double* sparsity;      // [U]
+  unsigned long long* kstats;  // optional K-means counters (TKV_KSTATS=1), else null
   int32_t* err;          // [U]
 };
 
@@ -106,6 +107,8 @@ struct TkvAnnealOp {
   int32_t m;              // members before this anneal
   int32_t K;              // retention target (< m)
   int32_t log_off;        // offset (in u32 words) of this op's evicted-mask log, per unit: + u_rel*W
+  int32_t nrestart;       // 4 farthest-first restarts, or 0 when seeds enumerate all K-subsets
+  int32_t ncombos;        // C(m, K) when nrestart == 0 (<= 512, evictor.cpp:270-283)
 };
 
 // Units of one group whose anneal ops [op_begin, op_end) are applied together
