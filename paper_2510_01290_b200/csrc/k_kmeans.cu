@@ -39,6 +39,7 @@
 namespace {
 
 constexpr int kMaxM = 256;
+constexpr int kSwapWin = 1024;  // pairs per swap-filter window (= candidate list capacity)
 
 __device__ __forceinline__ int find_op(const int32_t* prefix, int nops, int item) {
   int lo = 0, hi = nops - 1;
@@ -63,8 +64,16 @@ struct KmGeo {
   __host__ __device__ int64_t bytes() const { return (misc_off() + 16 + 255) / 256 * 256; }
 };
 
-__device__ __forceinline__ double xval(const float* X, const double* xs, int i, int ch, int D, bool scaled) {
-  const double v = (double)X[(int64_t)i * D + ch];
+__device__ int g_kst_small;  // unused
+__device__ __forceinline__ void kst(const TkvState& st, int i, unsigned long long v) {
+  if (st.kstats && threadIdx.x == 0) atomicAdd(st.kstats + i, v);
+}
+__device__ __forceinline__ void kstm(const TkvState& st, int m, int i, unsigned long long v) {
+  if (st.kstats && threadIdx.x == 0) atomicAdd(st.kstats + i + (m <= 16 ? 16 : 0), v);
+}
+
+__device__ __forceinline__ double xval(const float* X, const double* xs, int i, int ch, int xstride, bool scaled) {
+  const double v = (double)X[(int64_t)i * xstride + ch];
   return scaled ? __dmul_rn(v, xs[i]) : v;
 }
 
@@ -100,12 +109,14 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
   const TkvDims& dm = st.dm;
   const int item = item0 + blockIdx.x;
   if (item >= nitems) return;
+  const long long t_prep = clock64();
   const int oi = find_op(prefix, nops, item);
   const TkvAnnealOp op = ops[oi];
   const int urel = item - prefix[oi];
   const int u = op.unit0 + urel;
   const int D = dm.D;
   uint8_t* base = scratch + (int64_t)blockIdx.x * geo.bytes();
+  kst(st, 0, 1);
   float* X = reinterpret_cast<float*>(base + geo.x_off());
   double* xs = reinterpret_cast<double*>(base + geo.xs_off());
   double* pd = reinterpret_cast<double*>(base + geo.pd_off());
@@ -131,41 +142,69 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
   __syncthreads();
   if (sm_bad) return;
   const int m = sm_m, K = op.K;
+  extern __shared__ __align__(16) uint8_t pdyn[];
+  float* sX = reinterpret_cast<float*>(pdyn);  // [m][D + 1] (padded: conflict-free column access)
+  const int XS = D + 1;
+  __shared__ double sxs[kMaxM];
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     ids[i] = sids[i];
-    decode_point(st, u, st.tok_slot[(int64_t)u * dm.T + op.seg_start + sids[i]], X + (int64_t)i * D, xs + i);
+    decode_point(st, u, st.tok_slot[(int64_t)u * dm.T + op.seg_start + sids[i]], sX + (int64_t)i * XS, sxs + i);
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < m * D; i += blockDim.x) X[i] = sX[(i / D) * XS + i % D];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) xs[i] = sxs[i];
   const bool scaled = scaled_any != 0;
-  // exact pairwise distances (symmetric: (a-b)^2 == (b-a)^2 in IEEE)
-  const int npairs = m * (m - 1) / 2;
-  for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-    int i = 0, rem = p;
-    while (rem >= m - 1 - i) { rem -= m - 1 - i; ++i; }
-    const int j = i + 1 + rem;
-    double d = 0.0;
-    for (int ch = 0; ch < D; ++ch) {
-      const double t = __dsub_rn(xval(X, xs, i, ch, D, scaled), xval(X, xs, j, ch, D, scaled));
-      d = __dadd_rn(d, __dmul_rn(t, t));
+  // Exact pairwise distances, upper triangle mirrored ((a-b)^2 == (b-a)^2 in
+  // IEEE).  Warp task = 4 rows i x 64 columns j (lane -> j, j + 32), 8
+  // independent channel-sequential chains per thread, operands from smem.
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pblocks = (m + 3) / 4, cgroups = (m + 63) / 64;
+    for (int task = warp; task < pblocks * cgroups; task += blockDim.x / 32) {
+      const int pb = task / cgroups, cg = task % cgroups;
+      if (cg * 64 + 63 <= pb * 4) continue;  // entirely on/below the diagonal
+      const int j0 = cg * 64 + lane, j1 = j0 + 32;
+      const int jj0 = min(j0, m - 1), jj1 = min(j1, m - 1);
+      int ip[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ip[q] = min(pb * 4 + q, m - 1);
+      double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      for (int ch = 0; ch < D; ++ch) {
+        const double a0 = xval(sX, sxs, jj0, ch, XS, scaled), a1 = xval(sX, sxs, jj1, ch, XS, scaled);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double x = xval(sX, sxs, ip[q], ch, XS, scaled);
+          const double t0 = __dsub_rn(x, a0), t1 = __dsub_rn(x, a1);
+          d[q][0] = __dadd_rn(d[q][0], __dmul_rn(t0, t0));
+          d[q][1] = __dadd_rn(d[q][1], __dmul_rn(t1, t1));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = pb * 4 + q;
+        if (i >= m) break;
+        if (j0 < m && j0 > i) { pd[(int64_t)i * geo.mmax + j0] = d[q][0]; pd[(int64_t)j0 * geo.mmax + i] = d[q][0]; }
+        if (j1 < m && j1 > i) { pd[(int64_t)i * geo.mmax + j1] = d[q][1]; pd[(int64_t)j1 * geo.mmax + i] = d[q][1]; }
+      }
     }
-    pd[(int64_t)i * geo.mmax + j] = d;
-    pd[(int64_t)j * geo.mmax + i] = d;
   }
   for (int i = threadIdx.x; i < m; i += blockDim.x) pd[(int64_t)i * geo.mmax + i] = 0.0;
+  __syncthreads();
+  kst(st, 1, (unsigned long long)(clock64() - t_prep));
   if (op.nrestart <= 0) return;  // exhaustive seeds: nothing else to prepare
   __syncthreads();
   // anchors: 0, farthest from / nearest to the mean, m/2 (evictor.cpp:296-313)
   __shared__ double mean[256];
   for (int ch = threadIdx.x; ch < D; ch += blockDim.x) {
     double acc = 0.0;
-    for (int i = 0; i < m; ++i) acc = __dadd_rn(acc, xval(X, xs, i, ch, D, scaled));
+    for (int i = 0; i < m; ++i) acc = __dadd_rn(acc, xval(sX, sxs, i, ch, XS, scaled));
     mean[ch] = __ddiv_rn(acc, (double)m);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     double d = 0.0;
     for (int ch = 0; ch < D; ++ch) {
-      const double t = __dsub_rn(xval(X, xs, i, ch, D, scaled), mean[ch]);
+      const double t = __dsub_rn(xval(sX, sxs, i, ch, XS, scaled), mean[ch]);
       d = __dadd_rn(d, __dmul_rn(t, t));
     }
     dmean[i] = d;
@@ -220,28 +259,35 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
       __syncwarp();
     }
   }
+  __syncthreads();
+  kst(st, 2, (unsigned long long)(clock64() - t_prep));
 }
 
 // ---------------------------------------------------------------------------
 // restart
 // ---------------------------------------------------------------------------
+template <int MAXM>
 struct RsSmem {
-  int assign[kMaxM];
-  int sizes[kMaxM];
-  int order[kMaxM];
-  int offs[kMaxM + 1];
-  int cur[kMaxM];
-  int seeds[kMaxM];
-  double coef_add[kMaxM];  // nb / (nb + 1)
-  double coef_rem[kMaxM];  // -na / (na - 1)
-  double mv[kMaxM];
-  int flag, move_i, move_to, pair;
+  static constexpr int WIN = MAXM * (MAXM - 1) / 2 < kSwapWin ? MAXM * (MAXM - 1) / 2 : kSwapWin;
+  int assign[MAXM];
+  int sizes[MAXM];
+  int order[MAXM];
+  int offs[MAXM + 1];
+  int cur[MAXM];
+  int seeds[MAXM];
+  double tabA[MAXM + 1];  // n / (n + 1.0), indexed by cluster size (evictor.cpp:205)
+  double tabR[MAXM + 1];  // -n / (n - 1.0) (evictor.cpp:201)
+  double mv[MAXM];
+  double xs[MAXM];
+  int flag, move_i, move_to, pair, ncand;
+  int res[32];
+  int cand[WIN];
   double cost;
 };
 
 // D2[i][c] for all points and the given centroid rows (exact dist2).
 template <int NT>
-__device__ void fill_d2(const float* X, const double* xs, bool scaled, const double* C, int cstride, double* D2,
+__device__ void fill_d2(const float* X, int XS, const double* xs, bool scaled, const double* C, int cstride, double* D2,
                         int m, int K, int D) {
   // warp task = 4 points x 64 centroids (lane l -> centroids l, l + 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -260,7 +306,7 @@ __device__ void fill_d2(const float* X, const double* xs, bool scaled, const dou
       const double a0 = r0[ch], a1 = r1[ch];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const double x = xval(X, xs, ip[q], ch, D, scaled);
+        const double x = xval(X, xs, ip[q], ch, XS, scaled);
         const double t0 = __dsub_rn(x, a0), t1 = __dsub_rn(x, a1);
         d[q][0] = __dadd_rn(d[q][0], __dmul_rn(t0, t0));
         d[q][1] = __dadd_rn(d[q][1], __dmul_rn(t1, t1));
@@ -278,14 +324,14 @@ __device__ void fill_d2(const float* X, const double* xs, bool scaled, const dou
 
 // Recompute D2 columns a and b (after a move or swap changed those means).
 template <int NT>
-__device__ void refresh_cols(const float* X, const double* xs, bool scaled, const double* C, int cstride, double* D2,
-                             int m, int K, int D, int a, int b) {
+__device__ void refresh_cols(const float* X, int XS, const double* xs, bool scaled, const double* C, int cstride,
+                             double* D2, int m, int K, int D, int a, int b) {
   for (int t = threadIdx.x; t < 2 * m; t += NT) {
     const int i = t >> 1, c = (t & 1) ? b : a;
     const double* cr = C + (int64_t)c * cstride;
     double d = 0.0;
     for (int ch = 0; ch < D; ++ch) {
-      const double tt = __dsub_rn(xval(X, xs, i, ch, D, scaled), cr[ch]);
+      const double tt = __dsub_rn(xval(X, xs, i, ch, XS, scaled), cr[ch]);
       d = __dadd_rn(d, __dmul_rn(tt, tt));
     }
     D2[(int64_t)i * K + c] = d;
@@ -293,7 +339,8 @@ __device__ void refresh_cols(const float* X, const double* xs, bool scaled, cons
 }
 
 // Member lists per cluster in ascending point order (offs/order).
-__device__ void members(RsSmem& s, int m, int K) {
+template <typename SM>
+__device__ void members(SM& s, int m, int K) {
   if (threadIdx.x == 0) {
     s.offs[0] = 0;
     for (int c = 0; c < K; ++c) {
@@ -305,7 +352,7 @@ __device__ void members(RsSmem& s, int m, int K) {
   __syncthreads();
 }
 
-template <int NT>
+template <int NT, int MAXM>
 __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
                                                         const int32_t* __restrict__ rprefix, int nruns, int run0,
                                                         const int32_t* __restrict__ item_prefix, int item0,
@@ -328,18 +375,25 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   const int m = misc[0], K = op.K, D = dm.D;
   const bool scaled = scaled_any != 0;
   extern __shared__ __align__(16) uint8_t dyn[];
-  __shared__ RsSmem s;
-  // smem: X f32 [m][D] | means f64 [K][D] | D2 f64 [m][K]
+  __shared__ RsSmem<MAXM> s;
+  double* xs = s.xs;
+  // smem: X f32 [m][D+1] | means f64 [K][D+1] | D2 f64 [m][K]  (rows padded
+  // by one element so column-wise accesses across lanes are conflict-free)
+  const int XS = D + 1, MS = D + 1;
   float* X = reinterpret_cast<float*>(dyn);
-  double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)geo.mmax * D * 4 + 15) / 16 * 16));
-  double* D2 = Mn + (int64_t)geo.kmax * D;
-  __shared__ double xs[kMaxM];
+  double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)geo.mmax * XS * 4 + 15) / 16 * 16));
+  double* D2 = Mn + (int64_t)geo.kmax * MS;
   double* S = gsums + (int64_t)blockIdx.x * geo.kmax * D;  // sums / next (global, per CTA)
   const float* gX = reinterpret_cast<const float*>(base + geo.x_off());
   const double* gxs = reinterpret_cast<const double*>(base + geo.xs_off());
   const double* pd = reinterpret_cast<const double*>(base + geo.pd_off());
-  for (int i = threadIdx.x; i < m * D; i += NT) X[i] = gX[i];
+  for (int i = threadIdx.x; i < m * D; i += NT) X[(i / D) * XS + i % D] = gX[i];
   for (int i = threadIdx.x; i < m; i += NT) xs[i] = gxs[i];
+  for (int n = threadIdx.x; n <= MAXM; n += NT) {
+    const double dn = (double)n;
+    s.tabA[n] = __ddiv_rn(dn, __dadd_rn(dn, 1.0));
+    s.tabR[n] = __ddiv_rn(-dn, __dsub_rn(dn, 1.0));
+  }
   if (threadIdx.x == 0) {
     if (op.nrestart > 0) {
       const int32_t* sd = reinterpret_cast<const int32_t*>(base + geo.seeds_off()) + r * geo.kmax;
@@ -364,14 +418,17 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     }
   }
   __syncthreads();
+  const long long t0 = clock64();
+  kstm(st, m, 3, 1);
   // ---- Lloyd (evictor.cpp:102-159) ----------------------------------------
   for (int idx = threadIdx.x; idx < K * D; idx += NT) {
     const int c = idx / D, ch = idx % D;
-    Mn[idx] = xval(X, xs, s.seeds[c], ch, D, scaled);
+    Mn[(int64_t)c * MS + ch] = xval(X, xs, s.seeds[c], ch, XS, scaled);
   }
   __syncthreads();
   for (int iter = 0; iter < 50; ++iter) {
-    fill_d2<NT>(X, xs, scaled, Mn, D, D2, m, K, D);
+    kstm(st, m, 4, 1);
+    fill_d2<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D);
     __syncthreads();
     for (int i = threadIdx.x; i < m; i += NT) {
       const double* row = D2 + (int64_t)i * K;
@@ -407,14 +464,14 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     for (int idx = threadIdx.x; idx < K * D; idx += NT) {
       const int c = idx / D, ch = idx % D;
       double acc = 0.0;
-      for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, D, scaled));
+      for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
       S[idx] = __ddiv_rn(acc, (double)s.sizes[c]);
     }
     __syncthreads();
     for (int c = threadIdx.x; c < K; c += NT) {
       double d = 0.0;
       for (int ch = 0; ch < D; ++ch) {
-        const double t = __dsub_rn(S[(int64_t)c * D + ch], Mn[(int64_t)c * D + ch]);
+        const double t = __dsub_rn(S[(int64_t)c * D + ch], Mn[(int64_t)c * MS + ch]);
         d = __dadd_rn(d, __dmul_rn(t, t));
       }
       s.mv[c] = __dsqrt_rn(d);
@@ -424,11 +481,14 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       double movement = 0.0;
       for (int c = 0; c < K; ++c) movement = movement < s.mv[c] ? s.mv[c] : movement;
       s.flag = movement < 1e-6;
+      s.cost = movement;  // == 0 exactly: the next centroids equal the ones D2 was filled with
     }
-    for (int idx = threadIdx.x; idx < K * D; idx += NT) Mn[idx] = S[idx];
+    for (int idx = threadIdx.x; idx < K * D; idx += NT) Mn[(idx / D) * MS + idx % D] = S[idx];
     __syncthreads();
     if (s.flag) break;
   }
+  const long long t1 = clock64();
+  kstm(st, m, 5, (unsigned long long)(t1 - t0));
   // ---- Hartigan (evictor.cpp:167-243) --------------------------------------
   if (threadIdx.x == 0) {
     for (int c = 0; c < K; ++c) s.sizes[c] = 0;
@@ -439,139 +499,221 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   for (int idx = threadIdx.x; idx < K * D; idx += NT) {
     const int c = idx / D, ch = idx % D;
     double acc = 0.0;
-    for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, D, scaled));
+    for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
     S[idx] = acc;
-    Mn[idx] = __ddiv_rn(acc, (double)s.sizes[c]);
-  }
-  for (int c = threadIdx.x; c < K; c += NT) {
-    const double n = (double)s.sizes[c];
-    s.coef_add[c] = __ddiv_rn(n, __dadd_rn(n, 1.0));
-    s.coef_rem[c] = __ddiv_rn(-n, __dsub_rn(n, 1.0));
+    Mn[(int64_t)c * MS + ch] = __ddiv_rn(acc, (double)s.sizes[c]);
   }
   __syncthreads();
-  fill_d2<NT>(X, xs, scaled, Mn, D, D2, m, K, D);
+  if (s.cost != 0.0) fill_d2<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D);
   __syncthreads();
+  kstm(st, m, 6, (unsigned long long)(clock64() - t1));
+  long long tmove = 0, tswap = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int pass = 0; pass < 100; ++pass) {
+    kstm(st, m, 7, 1);
+    const long long tp = clock64();
     bool moved = false;  // CTA-uniform
     int start = 0;
     while (true) {
-      // warp 0 scans points in order with the cached distances until the
-      // first improving single move (no state changes before it).
-      if (warp == 0) {
-        int mi = -1, mto = -1;
-        for (int i = start; i < m; ++i) {
+      // Each warp evaluates one of the next NT/32 points against the cached
+      // distances; no state changes before the first improving point, so all
+      // decisions up to it are exactly the sequential ones (evictor.cpp:196-212).
+      {
+        const int i = start + warp;
+        int mto = -1;
+        if (i < m) {
           const int from = s.assign[i];
-          if (s.sizes[from] <= 1) continue;
-          const double* row = D2 + (int64_t)i * K;
-          const double removal = __dmul_rn(s.coef_rem[from], row[from]);
-          double bd = -1e-12;
-          int bt = 0x7fffffff;
-          for (int to = lane; to < K; to += 32) {
-            if (to == from) continue;
-            const double delta = __dadd_rn(removal, __dmul_rn(s.coef_add[to], row[to]));
-            if (delta < bd) { bd = delta; bt = to; }
+          if (s.sizes[from] > 1) {
+            const double* row = D2 + (int64_t)i * K;
+            const double removal = __dmul_rn(s.tabR[s.sizes[from]], row[from]);
+            double bd = -1e-12;
+            int bt = 0x7fffffff;
+            for (int to = lane; to < K; to += 32) {
+              if (to == from) continue;
+              const double delta = __dadd_rn(removal, __dmul_rn(s.tabA[s.sizes[to]], row[to]));
+              if (delta < bd) { bd = delta; bt = to; }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+              const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+              const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+              if (od < bd || (od == bd && ot < bt)) { bd = od; bt = ot; }
+            }
+            if (bt != 0x7fffffff) mto = bt;
           }
-          for (int o = 16; o > 0; o >>= 1) {
-            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-            const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-            if (od < bd || (od == bd && ot < bt)) { bd = od; bt = ot; }
-          }
-          if (bt != 0x7fffffff) { mi = i; mto = bt; break; }
         }
-        if (lane == 0) { s.move_i = mi; s.move_to = mto; }
+        if (lane == 0) s.res[warp] = mto;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int mi = -1, mt = -1;
+        for (int w = 0; w < NT / 32 && start + w < m; ++w)
+          if (s.res[w] >= 0) { mi = start + w; mt = s.res[w]; break; }
+        s.move_i = mi;
+        s.move_to = mt;
+        s.flag = mi >= 0 ? mi + 1 : start + NT / 32;
       }
       __syncthreads();
       const int i = s.move_i, to = s.move_to;
-      if (i < 0) break;
+      start = s.flag;
+      if (i < 0) {
+        if (start >= m) break;
+        continue;
+      }
       const int from = s.assign[i];
+      const int nf = s.sizes[from] - 1, nt = s.sizes[to] + 1;
+      kstm(st, m, 8, 1);
       moved = true;
       __syncthreads();
       if (threadIdx.x == 0) {
-        --s.sizes[from];
-        ++s.sizes[to];
+        s.sizes[from] = nf;
+        s.sizes[to] = nt;
         s.assign[i] = to;
-        const double nf = (double)s.sizes[from], nt = (double)s.sizes[to];
-        s.coef_add[from] = __ddiv_rn(nf, __dadd_rn(nf, 1.0));
-        s.coef_rem[from] = __ddiv_rn(-nf, __dsub_rn(nf, 1.0));
-        s.coef_add[to] = __ddiv_rn(nt, __dadd_rn(nt, 1.0));
-        s.coef_rem[to] = __ddiv_rn(-nt, __dsub_rn(nt, 1.0));
       }
+      // apply_move (evictor.cpp:189-196) and mean_of for the two clusters
       for (int ch = threadIdx.x; ch < D; ch += NT) {
-        const double x = xval(X, xs, i, ch, D, scaled);
-        S[(int64_t)from * D + ch] = __dsub_rn(S[(int64_t)from * D + ch], x);
-        S[(int64_t)to * D + ch] = __dadd_rn(S[(int64_t)to * D + ch], x);
+        const double x = xval(X, xs, i, ch, XS, scaled);
+        const double sf = __dsub_rn(S[(int64_t)from * D + ch], x);
+        const double sto = __dadd_rn(S[(int64_t)to * D + ch], x);
+        S[(int64_t)from * D + ch] = sf;
+        S[(int64_t)to * D + ch] = sto;
+        Mn[(int64_t)from * MS + ch] = __ddiv_rn(sf, (double)nf);
+        Mn[(int64_t)to * MS + ch] = __ddiv_rn(sto, (double)nt);
       }
       __syncthreads();
-      for (int ch = threadIdx.x; ch < D; ch += NT) {
-        Mn[(int64_t)from * D + ch] = __ddiv_rn(S[(int64_t)from * D + ch], (double)s.sizes[from]);
-        Mn[(int64_t)to * D + ch] = __ddiv_rn(S[(int64_t)to * D + ch], (double)s.sizes[to]);
-      }
+      refresh_cols<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D, from, to);
       __syncthreads();
-      refresh_cols<NT>(X, xs, scaled, Mn, D, D2, m, K, D, from, to);
-      __syncthreads();
-      start = i + 1;
     }
+    tmove += clock64() - tp;
     if (moved) continue;
+    const long long ts = clock64();
+    kstm(st, m, 9, 1);
     // ---- pairwise swaps: first improving (i, j) in lexicographic order ------
     if (threadIdx.x == 0) s.pair = 0x7fffffff;
-    __syncthreads();
+    // Pairs in lexicographic-rank windows of kSwapWin: filter (O(1) per pair
+    // from D2 and pd) into a candidate list, evaluate the candidates exactly
+    // in parallel, stop at the first window holding an improving pair.
     const int npairs = m * (m - 1) / 2;
-    for (int p = threadIdx.x; p < npairs; p += NT) {
-      if (p > *((volatile int*)&s.pair)) break;
-      int i = 0, rem = p;
-      while (rem >= m - 1 - i) { rem -= m - 1 - i; ++i; }
-      const int j = i + 1 + rem;
-      const int a = s.assign[i], b = s.assign[j];
-      if (a == b) continue;
-      const double na = (double)s.sizes[a], nb = (double)s.sizes[b];
-      const double w = 1.0 / na + 1.0 / nb;
-      const double dja = D2[(int64_t)j * K + a], dia = D2[(int64_t)i * K + a];
-      const double dib = D2[(int64_t)i * K + b], djb = D2[(int64_t)j * K + b];
-      const double pij = pd[(int64_t)i * geo.mmax + j];
-      const double approx = dja - dia + dib - djb - w * pij;
-      const double margin = 1e-6 * (dja + dia + dib + djb + w * pij) + 1e-9;
-      if (approx >= -1e-12 + margin) continue;
-      // exact reference expression (evictor.cpp:215-228)
-      const double* mua = Mn + (int64_t)a * D;
-      const double* mub = Mn + (int64_t)b * D;
-      double delta = 0.0;
-      for (int ch = 0; ch < D; ++ch) {
-        const double xi = xval(X, xs, i, ch, D, scaled), xj = xval(X, xs, j, ch, D, scaled);
-        const double ma = __dadd_rn(mua[ch], __ddiv_rn(__dsub_rn(xj, xi), na));
-        const double mb = __dadd_rn(mub[ch], __ddiv_rn(__dsub_rn(xi, xj), nb));
-        const double xx = __dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi));
-        const double yy = __dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj));
-        delta = __dadd_rn(delta, __dsub_rn(xx, __dmul_rn(na, __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua[ch], mua[ch])))));
-        delta = __dadd_rn(delta, __dsub_rn(yy, __dmul_rn(nb, __dsub_rn(__dmul_rn(mb, mb), __dmul_rn(mub[ch], mub[ch])))));
+    long long tfilt = 0;
+    for (int p0 = 0; p0 < npairs; p0 += RsSmem<MAXM>::WIN) {
+      if (threadIdx.x == 0) s.ncand = 0;
+      __syncthreads();
+      const long long tf0 = clock64();
+      for (int p = p0 + threadIdx.x; p < min(npairs, p0 + RsSmem<MAXM>::WIN); p += NT) {
+        int lo = 0, hi = m - 2;  // row i: prow(i) <= p < prow(i + 1)
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (mid * (2 * m - mid - 1) / 2 <= p) lo = mid; else hi = mid - 1;
+        }
+        const int i = lo, j = i + 1 + (p - i * (2 * m - i - 1) / 2);
+        const int a = s.assign[i], b = s.assign[j];
+        if (a == b) continue;
+        const double na = (double)s.sizes[a], nb = (double)s.sizes[b];
+        const double w = 1.0 / na + 1.0 / nb;
+        const double dja = D2[(int64_t)j * K + a], dia = D2[(int64_t)i * K + a];
+        const double dib = D2[(int64_t)i * K + b], djb = D2[(int64_t)j * K + b];
+        const double pij = pd[(int64_t)i * geo.mmax + j];
+        const double approx = dja - dia + dib - djb - w * pij;
+        const double margin = 1e-6 * (dja + dia + dib + djb + w * pij) + 1e-9;
+        if (approx >= -1e-12 + margin) continue;
+        s.cand[atomicAdd(&s.ncand, 1)] = p;
       }
-      if (delta < -1e-12) {
-        atomicMin(&s.pair, p);
-        break;
+      __syncthreads();
+      tfilt += clock64() - tf0;
+      if (s.ncand == 0) continue;
+      kstm(st, m, 10, (unsigned long long)s.ncand);
+      // One warp per candidate: lanes evaluate the per-channel terms (the
+      // divisions of different channels are independent), then the terms are
+      // accumulated in the reference's channel order through shuffles.
+      for (int c = warp; c < s.ncand; c += NT / 32) {
+        const int p = s.cand[c];
+        int lo = 0, hi = m - 2;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (mid * (2 * m - mid - 1) / 2 <= p) lo = mid; else hi = mid - 1;
+        }
+        const int i = lo, j = i + 1 + (p - i * (2 * m - i - 1) / 2);
+        const int a = s.assign[i], b = s.assign[j];
+        const double na = (double)s.sizes[a], nb = (double)s.sizes[b];
+        // exact reference expression (evictor.cpp:215-228)
+        const double* mua = Mn + (int64_t)a * MS;
+        const double* mub = Mn + (int64_t)b * MS;
+        // (x / 1.0 == x and 1.0 * x == x exactly, so singleton clusters skip
+        // the division and the multiply without changing any bit.)
+        const bool ua = na == 1.0, ub = nb == 1.0;
+        double TA[8], TB[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int ch = lane + 32 * k;
+          TA[k] = TB[k] = 0.0;
+          if (ch < D) {
+            const double xi = xval(X, xs, i, ch, XS, scaled), xj = xval(X, xs, j, ch, XS, scaled);
+            const double dji = __dsub_rn(xj, xi), dij = __dsub_rn(xi, xj);
+            const double ma = __dadd_rn(mua[ch], ua ? dji : __ddiv_rn(dji, na));
+            const double mb = __dadd_rn(mub[ch], ub ? dij : __ddiv_rn(dij, nb));
+            const double xx = __dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi));
+            const double yy = __dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj));
+            const double ta = __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua[ch], mua[ch]));
+            const double tb = __dsub_rn(__dmul_rn(mb, mb), __dmul_rn(mub[ch], mub[ch]));
+            TA[k] = __dsub_rn(xx, ua ? ta : __dmul_rn(na, ta));
+            TB[k] = __dsub_rn(yy, ub ? tb : __dmul_rn(nb, tb));
+          }
+        }
+        // The ordered sum can only fall below -1e-12 if some term is negative
+        // and the terms' absolute sum reaches it: a sum of non-negative terms
+        // rounds to a non-negative value, and |fl(sum)| <= (1 + 2^-44) sum|t|.
+        // Singleton-pair swaps (exact means) have all terms exactly zero.
+        bool neg = false;
+        double abssum = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          neg = neg || TA[k] < 0.0 || TB[k] < 0.0;
+          abssum += fabs(TA[k]) + fabs(TB[k]);
+        }
+        for (int o = 16; o > 0; o >>= 1) abssum += __shfl_xor_sync(0xffffffffu, abssum, o);
+        if (!__any_sync(0xffffffffu, neg) || abssum < 5e-13) continue;
+        if (st.kstats && lane == 0 && m > 16) atomicAdd(st.kstats + 31, 1ull);
+        double delta = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (32 * k >= D) break;
+          for (int l = 0; l < 32 && 32 * k + l < D; ++l) {
+            delta = __dadd_rn(delta, __shfl_sync(0xffffffffu, TA[k], l));
+            delta = __dadd_rn(delta, __shfl_sync(0xffffffffu, TB[k], l));
+          }
+        }
+        if (lane == 0 && delta < -1e-12) atomicMin(&s.pair, p);
       }
+      __syncthreads();
+      if (s.pair != 0x7fffffff) break;
     }
     __syncthreads();
     const int p = s.pair;
+    tswap += clock64() - ts;
+    kstm(st, m, 15, (unsigned long long)tfilt);
     if (p == 0x7fffffff) break;
     int i = 0, rem = p;
     while (rem >= m - 1 - i) { rem -= m - 1 - i; ++i; }
     const int j = i + 1 + rem;
     const int a = s.assign[i], b = s.assign[j];
     for (int ch = threadIdx.x; ch < D; ch += NT) {
-      const double xi = xval(X, xs, i, ch, D, scaled), xj = xval(X, xs, j, ch, D, scaled);
+      const double xi = xval(X, xs, i, ch, XS, scaled), xj = xval(X, xs, j, ch, XS, scaled);
       S[(int64_t)a * D + ch] = __dadd_rn(__dsub_rn(S[(int64_t)a * D + ch], xi), xj);
       S[(int64_t)b * D + ch] = __dsub_rn(__dadd_rn(S[(int64_t)b * D + ch], xi), xj);
-      Mn[(int64_t)a * D + ch] = __ddiv_rn(S[(int64_t)a * D + ch], (double)s.sizes[a]);
-      Mn[(int64_t)b * D + ch] = __ddiv_rn(S[(int64_t)b * D + ch], (double)s.sizes[b]);
+      Mn[(int64_t)a * MS + ch] = __ddiv_rn(S[(int64_t)a * D + ch], (double)s.sizes[a]);
+      Mn[(int64_t)b * MS + ch] = __ddiv_rn(S[(int64_t)b * D + ch], (double)s.sizes[b]);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       s.assign[i] = b;
       s.assign[j] = a;
     }
-    refresh_cols<NT>(X, xs, scaled, Mn, D, D2, m, K, D, a, b);
+    refresh_cols<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D, a, b);
     __syncthreads();
   }
+  kstm(st, m, 11, (unsigned long long)tmove);
+  kstm(st, m, 12, (unsigned long long)tswap);
+  kstm(st, m, 13, (unsigned long long)(clock64() - t0));
+  kstm(st, m, 14, (unsigned long long)m);
   // ---- cost (point order) and medoids --------------------------------------
   if (threadIdx.x == 0) {
     double c = 0.0;
@@ -649,7 +791,7 @@ int64_t tkv_km_instance_bytes(int mmax, int kmax, int D, int W, int R) {
 }
 
 size_t tkv_km_restart_smem(int mmax, int kmax, int D) {
-  return (size_t)(((int64_t)mmax * D * 4 + 15) / 16 * 16) + (size_t)kmax * D * 8 + (size_t)mmax * kmax * 8;
+  return (size_t)(((int64_t)mmax * (D + 1) * 4 + 15) / 16 * 16) + (size_t)kmax * (D + 1) * 8 + (size_t)mmax * kmax * 8;
 }
 
 cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int nops, const int32_t* item_prefix,
@@ -657,8 +799,15 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
                               int run0, int run_count, int mmax, int kmax, int R, uint8_t* scratch, double* gsums,
                               int gsums_ctas, uint32_t* log, int scaled_any, cudaStream_t stream) {
   KmGeo geo{mmax, kmax, st.dm.D, st.dm.W, R};
-  km_prep_kernel<<<item_count, 256, 0, stream>>>(st, ops, nops, item_prefix, nitems, item0, scratch, geo, scaled_any);
-  cudaError_t e = cudaGetLastError();
+  const size_t psmem = (size_t)mmax * (st.dm.D + 1) * 4;
+  if (psmem > 160 * 1024) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaSuccess;
+  if (psmem > 16 * 1024) {
+    e = cudaFuncSetAttribute(km_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    if (e != cudaSuccess) return e;
+  }
+  km_prep_kernel<<<item_count, 256, psmem, stream>>>(st, ops, nops, item_prefix, nitems, item0, scratch, geo, scaled_any);
+  e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "[kmeans] prep launch failed: items=%d: %s\n", item_count, cudaGetErrorString(e));
     return e;
@@ -668,21 +817,23 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
   // runs are processed in chunks of gsums_ctas CTAs (one global sums buffer each)
   for (int r = 0; r < run_count; r += gsums_ctas) {
     const int n = run_count - r < gsums_ctas ? run_count - r : gsums_ctas;
-    if (mmax <= 32) {
-      if (smem > 16 * 1024) {  // static (~14 KB) + dynamic must opt in beyond 48 KB
-        e = cudaFuncSetAttribute(km_restart_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
+    // Instance-size variants: static shared arrays and CTA width scale with
+    // m, so tiny exhaustive-seed instances (e.g. 8 -> 4, 70 restarts) run as
+    // many single-warp CTAs per SM.
+    auto go = [&](auto kern, int nt) -> cudaError_t {
+      if (smem > 16 * 1024) {  // static + dynamic must opt in beyond 48 KB
+        const cudaError_t ee = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ee != cudaSuccess) return ee;
       }
-      km_restart_kernel<64><<<n, 64, smem, stream>>>(st, ops, nops, run_prefix, run0 + run_count, run0 + r,
-                                                      item_prefix, item0, scratch, geo, gsums, scaled_any);
-    } else {
-      if (smem > 16 * 1024) {  // static (~14 KB) + dynamic must opt in beyond 48 KB
-        e = cudaFuncSetAttribute(km_restart_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-      }
-      km_restart_kernel<256><<<n, 256, smem, stream>>>(st, ops, nops, run_prefix, run0 + run_count, run0 + r,
-                                                        item_prefix, item0, scratch, geo, gsums, scaled_any);
-    }
+      kern<<<n, nt, smem, stream>>>(st, ops, nops, run_prefix, run0 + run_count, run0 + r, item_prefix, item0,
+                                    scratch, geo, gsums, scaled_any);
+      return cudaSuccess;
+    };
+    if (mmax <= 16) e = go(km_restart_kernel<32, 16>, 32);
+    else if (mmax <= 32) e = go(km_restart_kernel<64, 32>, 64);
+    else if (mmax <= 64) e = go(km_restart_kernel<128, 64>, 128);
+    else e = go(km_restart_kernel<256, kMaxM>, 256);
+    if (e != cudaSuccess) return e;
     e = cudaGetLastError();
     if (e != cudaSuccess) {
       fprintf(stderr, "[kmeans] restart launch failed: n=%d smem=%zu mmax=%d kmax=%d R=%d: %s\n", n, smem, mmax, kmax, R,

@@ -1062,7 +1062,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   st.buf = dalloc<uint8_t>(r, U * 4 * (size_t)dm.g * dm.D * dm.in_bytes, 0);
   st.sparsity = dalloc<double>(r, U);
   st.kstats = nullptr;
-  if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 16, 0);
+  if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 32, 0);
   st.err = dalloc<int32_t>(r, U);
   check_launch(tkv_launch_init(st, r->stream), "init kernel");
   // arenas
@@ -1348,11 +1348,16 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
   try {
     drain_timing(run);
     if (run->st.kstats) {
-      unsigned long long k[16];
+      unsigned long long k[32];
       CUDA_OK(cudaMemcpy(k, run->st.kstats, sizeof(k), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[kstats] inst=%llu exh=%llu restarts=%llu lloyd_it=%llu hart_pass=%llu moves=%llu swapscans=%llu swaps=%llu "
-              "cyc: lloyd=%llu hartmove=%llu swapscan=%llu restart=%llu ff=%llu inst=%llu sum_m=%llu\n",
-              k[10], k[11], k[0], k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8], k[9], k[12], k[13], k[14]);
+      fprintf(stderr, "[kstats] prep=%llu cyc_pd=%llu cyc_prep=%llu restarts=%llu lloyd_it=%llu cyc_lloyd=%llu cyc_hinit=%llu "
+              "passes=%llu moves=%llu swapscans=%llu exact_swaps=%llu cyc_moves=%llu cyc_swaps=%llu cyc_restart=%llu sum_m=%llu "
+              "cyc_swapfilter=%llu ordered_sums=%llu\n",
+              k[0], k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8], k[9], k[10], k[11], k[12], k[13], k[14], k[15],
+              k[31]);
+      fprintf(stderr, "[kstats-small] restarts=%llu lloyd_it=%llu cyc_lloyd=%llu cyc_hinit=%llu passes=%llu moves=%llu "
+              "swapscans=%llu exact_swaps=%llu cyc_moves=%llu cyc_swaps=%llu cyc_restart=%llu sum_m=%llu\n",
+              k[19], k[20], k[21], k[22], k[23], k[24], k[25], k[26], k[27], k[28], k[29], k[30]);
       CUDA_OK(cudaMemset(run->st.kstats, 0, sizeof(k)));
     }
     out->attend_ms = run->acc_ms[CAT_ATTEND];
