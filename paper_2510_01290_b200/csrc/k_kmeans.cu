@@ -289,6 +289,27 @@ struct RsSmem {
 template <int NT>
 __device__ void fill_d2(const float* X, int XS, const double* xs, bool scaled, const double* C, int cstride, double* D2,
                         int m, int K, int D) {
+  if (K <= 16) {
+    // small K: one (point, centroid) pair per thread, two chains for ILP
+    for (int t = threadIdx.x; t < m * K; t += 2 * NT) {
+      const int t2 = t + NT;
+      const bool v1 = t2 < m * K;
+      const int i0 = t / K, c0 = t % K;
+      const int i1 = v1 ? t2 / K : i0, c1 = v1 ? t2 % K : c0;
+      const double* r0 = C + (int64_t)c0 * cstride;
+      const double* r1 = C + (int64_t)c1 * cstride;
+      double d0 = 0.0, d1 = 0.0;
+      for (int ch = 0; ch < D; ++ch) {
+        const double t0 = __dsub_rn(xval(X, xs, i0, ch, XS, scaled), r0[ch]);
+        const double t1 = __dsub_rn(xval(X, xs, i1, ch, XS, scaled), r1[ch]);
+        d0 = __dadd_rn(d0, __dmul_rn(t0, t0));
+        d1 = __dadd_rn(d1, __dmul_rn(t1, t1));
+      }
+      D2[(int64_t)i0 * K + c0] = d0;
+      if (v1) D2[(int64_t)i1 * K + c1] = d1;
+    }
+    return;
+  }
   // warp task = 4 points x 64 centroids (lane l -> centroids l, l + 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pblocks = (m + 3) / 4, cgroups = (K + 63) / 64;
@@ -383,7 +404,8 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   float* X = reinterpret_cast<float*>(dyn);
   double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)geo.mmax * XS * 4 + 15) / 16 * 16));
   double* D2 = Mn + (int64_t)geo.kmax * MS;
-  double* S = gsums + (int64_t)blockIdx.x * geo.kmax * D;  // sums / next (global, per CTA)
+  // sums / next: shared memory for small instances, else a global row block per CTA
+  double* S = MAXM <= 32 ? D2 + (int64_t)geo.mmax * geo.kmax : gsums + (int64_t)blockIdx.x * geo.kmax * D;
   const float* gX = reinterpret_cast<const float*>(base + geo.x_off());
   const double* gxs = reinterpret_cast<const double*>(base + geo.xs_off());
   const double* pd = reinterpret_cast<const double*>(base + geo.pd_off());
@@ -821,11 +843,12 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
     // m, so tiny exhaustive-seed instances (e.g. 8 -> 4, 70 restarts) run as
     // many single-warp CTAs per SM.
     auto go = [&](auto kern, int nt) -> cudaError_t {
-      if (smem > 16 * 1024) {  // static + dynamic must opt in beyond 48 KB
-        const cudaError_t ee = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const size_t sm = mmax <= 32 ? smem + (size_t)kmax * st.dm.D * 8 : smem;  // + shared sums rows
+      if (sm > 16 * 1024) {  // static + dynamic must opt in beyond 48 KB
+        const cudaError_t ee = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (ee != cudaSuccess) return ee;
       }
-      kern<<<n, nt, smem, stream>>>(st, ops, nops, run_prefix, run0 + run_count, run0 + r, item_prefix, item0,
+      kern<<<n, nt, sm, stream>>>(st, ops, nops, run_prefix, run0 + run_count, run0 + r, item_prefix, item0,
                                     scratch, geo, gsums, scaled_any);
       return cudaSuccess;
     };
