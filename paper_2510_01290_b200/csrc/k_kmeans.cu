@@ -72,6 +72,14 @@ __device__ __forceinline__ void kstm(const TkvState& st, int m, int i, unsigned 
   if (st.kstats && threadIdx.x == 0) atomicAdd(st.kstats + i + (m <= 16 ? 16 : 0), v);
 }
 
+// x / n for a cluster size n >= 1.  For n = 2^k the multiply by the exact
+// reciprocal 2^-k is the same correctly rounded real x / 2^k as the
+// division, so both produce identical bits; other sizes divide.
+__device__ __forceinline__ double div_n(double x, int n) {
+  if ((n & (n - 1)) == 0) return __dmul_rn(x, __longlong_as_double((long long)(1024 - __ffs(n)) << 52));
+  return __ddiv_rn(x, (double)n);
+}
+
 __device__ __forceinline__ double xval(const float* X, const double* xs, int i, int ch, int xstride, bool scaled) {
   const double v = (double)X[(int64_t)i * xstride + ch];
   return scaled ? __dmul_rn(v, xs[i]) : v;
@@ -487,7 +495,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       const int c = idx / D, ch = idx % D;
       double acc = 0.0;
       for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
-      S[idx] = __ddiv_rn(acc, (double)s.sizes[c]);
+      S[idx] = div_n(acc, s.sizes[c]);
     }
     __syncthreads();
     for (int c = threadIdx.x; c < K; c += NT) {
@@ -523,7 +531,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     double acc = 0.0;
     for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
     S[idx] = acc;
-    Mn[(int64_t)c * MS + ch] = __ddiv_rn(acc, (double)s.sizes[c]);
+    Mn[(int64_t)c * MS + ch] = div_n(acc, s.sizes[c]);
   }
   __syncthreads();
   if (s.cost != 0.0) fill_d2<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D);
@@ -598,8 +606,8 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
         const double sto = __dadd_rn(S[(int64_t)to * D + ch], x);
         S[(int64_t)from * D + ch] = sf;
         S[(int64_t)to * D + ch] = sto;
-        Mn[(int64_t)from * MS + ch] = __ddiv_rn(sf, (double)nf);
-        Mn[(int64_t)to * MS + ch] = __ddiv_rn(sto, (double)nt);
+        Mn[(int64_t)from * MS + ch] = div_n(sf, nf);
+        Mn[(int64_t)to * MS + ch] = div_n(sto, nt);
       }
       __syncthreads();
       refresh_cols<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D, from, to);
@@ -670,8 +678,8 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
           if (ch < D) {
             const double xi = xval(X, xs, i, ch, XS, scaled), xj = xval(X, xs, j, ch, XS, scaled);
             const double dji = __dsub_rn(xj, xi), dij = __dsub_rn(xi, xj);
-            const double ma = __dadd_rn(mua[ch], ua ? dji : __ddiv_rn(dji, na));
-            const double mb = __dadd_rn(mub[ch], ub ? dij : __ddiv_rn(dij, nb));
+            const double ma = __dadd_rn(mua[ch], div_n(dji, s.sizes[a]));
+            const double mb = __dadd_rn(mub[ch], div_n(dij, s.sizes[b]));
             const double xx = __dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi));
             const double yy = __dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj));
             const double ta = __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua[ch], mua[ch]));
@@ -721,8 +729,8 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       const double xi = xval(X, xs, i, ch, XS, scaled), xj = xval(X, xs, j, ch, XS, scaled);
       S[(int64_t)a * D + ch] = __dadd_rn(__dsub_rn(S[(int64_t)a * D + ch], xi), xj);
       S[(int64_t)b * D + ch] = __dsub_rn(__dadd_rn(S[(int64_t)b * D + ch], xi), xj);
-      Mn[(int64_t)a * MS + ch] = __ddiv_rn(S[(int64_t)a * D + ch], (double)s.sizes[a]);
-      Mn[(int64_t)b * MS + ch] = __ddiv_rn(S[(int64_t)b * D + ch], (double)s.sizes[b]);
+      Mn[(int64_t)a * MS + ch] = div_n(S[(int64_t)a * D + ch], s.sizes[a]);
+      Mn[(int64_t)b * MS + ch] = div_n(S[(int64_t)b * D + ch], s.sizes[b]);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -837,8 +845,10 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
   const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // tau x d beyond the smem design point
   // runs are processed in chunks of gsums_ctas CTAs (one global sums buffer each)
-  for (int r = 0; r < run_count; r += gsums_ctas) {
-    const int n = run_count - r < gsums_ctas ? run_count - r : gsums_ctas;
+  // Small classes keep their sums in shared memory: one launch for all runs.
+  const int chunk = mmax <= 32 ? (run_count > 0 ? run_count : 1) : gsums_ctas;
+  for (int r = 0; r < run_count; r += chunk) {
+    const int n = run_count - r < chunk ? run_count - r : chunk;
     // Instance-size variants: static shared arrays and CTA width scale with
     // m, so tiny exhaustive-seed instances (e.g. 8 -> 4, 70 restarts) run as
     // many single-warp CTAs per SM.

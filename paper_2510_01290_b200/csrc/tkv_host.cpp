@@ -441,7 +441,17 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
     f64_raw = f64_raw || (dm.band_fmt[b] == TKV_FMT_RAW && dm.in_dtype == TKV_IN_F64);
     fp8 = fp8 || dm.band_fmt[b] == TKV_FMT_FP8;
   }
+  // Ops of one wave are independent; split each wave by instance-size class
+  // so small instances get the small (high-occupancy) restart variant
+  // instead of inheriting the shared-memory footprint of the largest op.
+  std::vector<std::vector<TkvAnnealOp>> subwaves;
   for (auto& wv : waves) {
+    std::vector<TkvAnnealOp> cls[4];
+    for (const TkvAnnealOp& op : wv) cls[op.m <= 16 ? 0 : op.m <= 32 ? 1 : op.m <= 64 ? 2 : 3].push_back(op);
+    for (auto& c : cls)
+      if (!c.empty()) subwaves.push_back(std::move(c));
+  }
+  for (auto& wv : subwaves) {
     std::vector<int32_t> prefix(wv.size()), rprefix(wv.size());
     int32_t items = 0, runs = 0;
     int mmax = 1, kmax = 1, R = 1;
