@@ -1,0 +1,57 @@
+"""Summarise ncu captures for profiles/ (run here, on the CPU box).
+
+  python profiles/summarize.py launches <launches.csv>      per-kernel shares of a launch list
+  python profiles/summarize.py full <prof.ncu-rep> [...]    key counters of a --set full capture
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+FULL = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__maximum_warps_per_active_cycle_pct", "launch__registers_per_thread", "launch__grid_size",
+    "launch__block_size", "launch__shared_mem_per_block_dynamic", "launch__occupancy_limit_registers",
+    "launch__occupancy_limit_shared_mem", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+    "l1tex__t_sector_hit_rate.pct", "lts__t_bytes.sum", "smsp__inst_executed.sum",
+]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hi]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
+        agg[name][0] += 1
+        agg[name][1] += float(r[vi].replace(",", ""))
+    tot = sum(a[1] for a in agg.values())
+    print(f"| kernel | launches | total us | avg us | share |\n|---|---|---|---|---|")
+    for n, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"| `{n}` | {c} | {t / 1e3:.1f} | {t / c / 1e3:.1f} | {t / tot * 100:.1f}% |")
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    idx = {h: i for i, h in enumerate(hdr)}
+    kn = idx.get("Kernel Name")
+    for r in rows[2:]:
+        print(f"### {r[kn].split('(')[0] if kn is not None else '?'}")
+        for m in FULL:
+            if m in idx:
+                print(f"- {m}: {r[idx[m]]} {units[idx[m]]}")
+        print()
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](*sys.argv[2:])
