@@ -29,12 +29,15 @@ METRIC = "decode tokens/s & TPOT, R1-Llama-8B shape bs32 32K ctx; achieved HBM G
 SEED = 0x71534B56
 
 
-def workload(args):
+def workload(args, rank=0, world=1):
+    """This rank's share of the global batch: args.seqs sequences per rank
+    (weak scaling), global sequences [rank*seqs, (rank+1)*seqs)."""
     from paper_2510_01290_b200 import ThinkvConfig
+    from paper_2510_01290_b200.shard import shard_script
     from paper_2510_01290_b200.synth import band_script
     intervals = args.max_gen // args.tau + 2
-    # Scripted thought labels per sequence: T with p=0.1, else R/E 50/50.
-    script = band_script(SEED, args.seqs, intervals, 3, args.pT_permille)
+    # Scripted thought labels per global sequence: T with p=0.1, else R/E 50/50.
+    script = shard_script(band_script(SEED, args.seqs * world, intervals, 3, args.pT_permille), rank, world)
     return ThinkvConfig(num_seqs=args.seqs, units_per_seq=args.layers * args.kv_heads, num_q_heads=args.q_per_kv,
                         head_dim=args.head_dim, tau=args.tau, group_size=16, block_size=args.block_size,
                         budget=args.budget, levels=(64, 32, 16, 8, 4), psi_bits=(4, 4, 2),
@@ -102,37 +105,36 @@ def ncu_traffic():
         return None
 
 
-def cpu_reference(args, cfg, steps_timed=None):
+def cpu_reference(args, cfg, start, steps, unit0=0):
     """The reference's own CPU implementation (compiled from /root/reference by
     oracle/Makefile into oracle/_ref/, driven by the ThinkvMethod restatement)
-    on the host's cores: one single-unit sequence per thread, at this config's
-    unit shape, decoded from step 0; the last `steps_timed` steps of each are
-    timed.  Per unit-step time x units / threads = extrapolated TPOT."""
-    import numpy as np
+    on all host cores: one thread per core, each decoding one unit of this
+    workload (its own sequence's scripted labels and synthetic inputs) from
+    step 0; steps [start, start + steps) -- the positions the GPU arm times --
+    are timed.  Per unit-step time x units / threads = extrapolated TPOT."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     threads = os.cpu_count() or 1
-    steps_timed = steps_timed or args.cpu_steps
-    warm = args.cpu_warm
     per_thread_time = [0.0] * threads
     errs = []
 
     def worker(i):
         try:
+            unit = (i * cfg.units) // threads  # spread over the batch's sequences
+            seq = unit // cfg.units_per_seq
             rc = O.RunConfig(num_seqs=1, units_per_seq=1, num_q_heads=cfg.num_q_heads, head_dim=cfg.head_dim,
                              tau=cfg.tau, group_size=cfg.group_size, block_size=cfg.block_size,
                              budget=cfg.budget, levels=cfg.levels, psi_bits=cfg.psi_bits,
-                             max_gen_len=warm + steps_timed, script=[cfg.script[i % cfg.num_seqs]])
+                             max_gen_len=start + steps, script=[cfg.script[seq]])
             run = O.OracleRun(rc)
-            unit = i * 37  # distinct units of the workload
             acc = 0.0
-            for t in range(warm + steps_timed):
+            for t in range(start + steps):
                 q, k, v = O.synth_step(SEED, cfg.units_per_seq, cfg.tau, 1, cfg.num_q_heads, cfg.head_dim, t,
-                                       unit0=unit)
+                                       unit0=unit0 + unit)
                 qd, kd, vd = O.bf16_to_f64(q), O.bf16_to_f64(k), O.bf16_to_f64(v)
                 t0 = time.perf_counter()
                 run.step(qd, kd, vd)
-                if t >= warm:
+                if t >= start:
                     acc += time.perf_counter() - t0
             per_thread_time[i] = acc
         except Exception as e:  # pragma: no cover
@@ -147,16 +149,24 @@ def cpu_reference(args, cfg, steps_timed=None):
     wall = time.perf_counter() - wall0
     if errs:
         raise RuntimeError(errs[0])
-    unit_step_s = sum(per_thread_time) / (threads * steps_timed)
+    unit_step_s = sum(per_thread_time) / (threads * steps)
     tpot_s = unit_step_s * cfg.units / threads
     return {
         "value": cfg.num_seqs / tpot_s, "unit": "tokens/s", "cores": threads, "kind": "reference",
         "tpot_ms": tpot_s * 1e3, "unit_step_us": unit_step_s * 1e6,
-        "sample": (f"{threads} threads x 1 unit each (config-2 unit shape), steps {warm}..{warm + steps_timed - 1} "
-                   f"timed after an untimed decode from step 0; TPOT extrapolated as per-unit-step time x "
-                   f"{cfg.units} units / {threads} threads; only the reference step calls are timed "
+        "sample": (f"{threads} threads x 1 unit each (units spread over the batch), decoded from step 0; "
+                   f"positions {start}..{start + steps - 1} timed (only the reference step calls); TPOT "
+                   f"extrapolated as per-unit-step time x {cfg.units} units / {threads} threads "
                    f"({wall:.1f} s wall)"),
     }
+
+
+def positions(args, cfg):
+    """Decode position where the warmup starts: the timed K steps and the e2e
+    steps end at the end of the 32K generation."""
+    need = args.warmup + args.steps + args.e2e_steps
+    ctx = args.ctx if args.ctx is not None else cfg.max_gen_len - need
+    return max(0, min(ctx, cfg.max_gen_len - need))
 
 
 def main():
@@ -166,7 +176,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ctx", type=int, default=None, help="decode position at which timing starts")
-    ap.add_argument("--e2e-steps", type=int, default=32)
+    ap.add_argument("--e2e-steps", type=int, default=128)
     ap.add_argument("--seqs", type=int, default=32)
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--kv-heads", type=int, default=8)
@@ -177,15 +187,17 @@ def main():
     ap.add_argument("--budget", type=int, default=1024)
     ap.add_argument("--max-gen", type=int, default=32768)
     ap.add_argument("--pT-permille", type=int, default=100)
-    ap.add_argument("--cpu-steps", type=int, default=128)
-    ap.add_argument("--cpu-warm", type=int, default=1280)
+    ap.add_argument("--cpu-start", type=int, default=None, help="first timed CPU position (default: the GPU's)")
+    ap.add_argument("--cpu-steps", type=int, default=None, help="timed CPU steps (default: --steps)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = workload(args)
+    cfg = workload(args, rank, world)
+    from paper_2510_01290_b200.shard import unit_offset
+    unit0 = unit_offset(args.seqs * world, cfg.units_per_seq, rank, world)
     config = {"workload": "ThinKV decode, R1-Distill-Llama-8B attention shape (32 q / 8 kv heads, d=128, "
                           "32 layers), bs32 per GPU, 32K generated, budget 1024 (3.1%), R4E4T2, block 16",
               "global_batch": args.seqs * world, "units_per_gpu": cfg.units, "parallelism": f"seq-shard x{world}",
@@ -194,7 +206,9 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_reference(args, cfg)
+        ctx = positions(args, cfg)
+        cb = cpu_reference(args, cfg, args.cpu_start if args.cpu_start is not None else ctx + args.warmup,
+                           args.cpu_steps or args.steps, unit0)
         line = {"metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": cb["tpot_ms"], "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference", "config": config,
@@ -213,8 +227,7 @@ def main():
     dev = torch.device("cuda", local)
     U, G, D = cfg.units, cfg.num_q_heads, cfg.head_dim
     K, W, E = args.steps, args.warmup, args.e2e_steps
-    ctx = args.ctx if args.ctx is not None else cfg.max_gen_len - (W + K + E)
-    ctx = max(0, min(ctx, cfg.max_gen_len - (W + K + E)))
+    ctx = positions(args, cfg)
     run = DecodeRun(cfg, device=local)
     q = torch.empty((U, G, D), dtype=torch.bfloat16, device=dev)
     k = torch.empty((U, D), dtype=torch.bfloat16, device=dev)
@@ -223,7 +236,7 @@ def main():
     # 1. build the decode context (untimed): the real path, step by step.
     t_ctx = time.time()
     for t in range(ctx):
-        run.synth_inputs(SEED + rank, t, q, k, v)
+        run.synth_inputs(SEED, t, q, k, v, unit0=unit0)
         run.step(q, k, v, out)
     torch.cuda.synchronize(dev)
     t_ctx = time.time() - t_ctx
@@ -232,7 +245,7 @@ def main():
     ks = torch.empty((W + K, U, D), dtype=torch.bfloat16, device=dev)
     vs = torch.empty((W + K, U, D), dtype=torch.bfloat16, device=dev)
     for i in range(W + K):
-        run.synth_inputs(SEED + rank, ctx + i, qs[i], ks[i], vs[i])
+        run.synth_inputs(SEED, ctx + i, qs[i], ks[i], vs[i], unit0=unit0)
     for i in range(W):
         run.step(qs[i], ks[i], vs[i], out)
     bytes_k1 = run.bytes()  # algorithmic bytes of one attention launch at this point
@@ -261,7 +274,7 @@ def main():
     pout = torch.empty((U, G, D), dtype=torch.float32).pin_memory()
     host_inputs = []
     for i in range(E):
-        run.synth_inputs(SEED + rank, ctx + W + K + i, q, k, v)
+        run.synth_inputs(SEED, ctx + W + K + i, q, k, v, unit0=unit0)
         host_inputs.append((q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()))
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -310,7 +323,8 @@ def main():
         "context_build_s": t_ctx,
     }
     if not args.no_cpu and world == 1:
-        cb = cpu_reference(args, cfg)
+        cb = cpu_reference(args, cfg, args.cpu_start if args.cpu_start is not None else ctx + W,
+                           args.cpu_steps or K, unit0)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
     if world > 1:

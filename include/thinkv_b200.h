@@ -144,8 +144,12 @@ typedef struct tkv_timing_t {
 int tkv_timing_enable(tkv_run* run, int enable);
 int tkv_timing_read(tkv_run* run, tkv_timing_t* out);
 
-/* Deterministic synthetic bf16 inputs for step `step` (synth.h) on device. */
-int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t step, void* q, void* k, void* v, void* stream);
+/* Deterministic synthetic bf16 inputs for step `step` (synth.h) on device.
+ * Unit u of the run receives the inputs of global unit unit0 + u, so a
+ * sequence-sharded run (rank r: unit0 = r * units) sees exactly the inputs
+ * the same sequences get in a 1-GPU run of the whole batch. */
+int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t unit0, int64_t step, void* q, void* k, void* v,
+                     void* stream);
 
 #ifdef __cplusplus
 }

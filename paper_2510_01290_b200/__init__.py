@@ -160,9 +160,10 @@ class DecodeRun:
         ptr = (lambda a: a.ctypes.data) if hasattr(q, "ctypes") else (lambda a: a.data_ptr())
         check(lib.tkv_step_host(self._h, ptr(q), ptr(k), ptr(v), ptr(out)))
 
-    def synth_inputs(self, seed: int, step: int, q, k, v, stream=None):
+    def synth_inputs(self, seed: int, step: int, q, k, v, stream=None, unit0: int = 0):
+        """Synthetic bf16 inputs of global units unit0.. for `step` (csrc/synth.h)."""
         s = self._stream(stream)
-        check(lib.tkv_synth_inputs(self._h, seed, step, q.data_ptr(), k.data_ptr(), v.data_ptr(), s))
+        check(lib.tkv_synth_inputs(self._h, seed, unit0, step, q.data_ptr(), k.data_ptr(), v.data_ptr(), s))
 
     def finish(self):
         check(lib.tkv_finish(self._h))

@@ -85,7 +85,7 @@ def _load():
     L.tkv_unit_sparsity.argtypes = [vp, vp, C.c_int64]
     L.tkv_timing_enable.argtypes = [vp, C.c_int]
     L.tkv_timing_read.argtypes = [vp, C.POINTER(Timing)]
-    L.tkv_synth_inputs.argtypes = [vp, C.c_uint64, C.c_int64, vp, vp, vp, vp]
+    L.tkv_synth_inputs.argtypes = [vp, C.c_uint64, C.c_int64, C.c_int64, vp, vp, vp, vp]
     return L
 
 

@@ -1387,11 +1387,12 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
   }
 }
 
-int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t step, void* q, void* k, void* v, void* stream) {
+int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t unit0, int64_t step, void* q, void* k, void* v,
+                     void* stream) {
   try {
     const TkvDims& dm = run->st.dm;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : run->stream;
-    check_launch(tkv_launch_synth(seed, run->desc.units_per_seq, run->desc.tau, 4, 0, dm.U, dm.G, dm.D, step,
+    check_launch(tkv_launch_synth(seed, run->desc.units_per_seq, run->desc.tau, 4, unit0, dm.U, dm.G, dm.D, step,
                                   static_cast<uint16_t*>(q), static_cast<uint16_t*>(k), static_cast<uint16_t*>(v), s),
                  "synth kernel");
     return TKV_OK;

@@ -110,3 +110,21 @@ def test_pool_exhaustion_matches_reference_error():
     with pytest.raises(TkvError) as ge:
         run.synchronize()
     assert ge.value.code == 4
+
+
+def test_device_synth_matches_host_generator():
+    """tkv_synth_inputs (device) == the oracle's generator for the same global
+    units, so sharded runs (unit0 = rank offset) see the 1-GPU inputs."""
+    cfg = ThinkvConfig(num_seqs=2, units_per_seq=3, num_q_heads=4, head_dim=64, tau=32, group_size=16,
+                       block_size=16, budget=96, levels=(16, 8, 4), max_gen_len=64, script=[[1], [0]])
+    run = DecodeRun(cfg)
+    dev = torch.device("cuda:0")
+    q = torch.empty((6, 4, 64), dtype=torch.bfloat16, device=dev)
+    k = torch.empty((6, 64), dtype=torch.bfloat16, device=dev)
+    v = torch.empty((6, 64), dtype=torch.bfloat16, device=dev)
+    for unit0, step in ((0, 0), (0, 37), (12, 5), (6 * 1000, 129)):
+        run.synth_inputs(0x71534B56, step, q, k, v, unit0=unit0)
+        hq, hk, hv = O.synth_step(0x71534B56, 3, 32, 6, 4, 64, step, unit0=unit0)
+        torch.cuda.synchronize()
+        for got, want in ((q, hq), (k, hk), (v, hv)):
+            assert np.array_equal(got.cpu().view(torch.int16).numpy().view(np.uint16), want)
