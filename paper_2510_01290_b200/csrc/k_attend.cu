@@ -1,5 +1,6 @@
-// K1: paged mixed-precision decode attention, and K3a: the fp64 sparsity
-// statistics that feed the thought classifier.
+// K1 (SIMT variant): paged mixed-precision decode attention for the shapes
+// the tensor-core kernel (k_attend_mma.cu) does not cover -- fp32/fp64
+// inputs, head dims other than 64/128, G > 8.
 //
 // Reference semantics (what one unit computes per step):
 //   live view = pager slots in physical (block, slot) order (BlockPager::
@@ -16,11 +17,7 @@
 // are skipped at slot granularity through a per-CTA compacted live list that
 // is grouped by storage format, so every 32-token tile is format-uniform.
 //
-// K3a (tkv_score_kernel) recomputes, on refresh steps only, the exact fp64
-// sparsity of each softmax row in the reference's order (sequential dot
-// products, sequential softmax denominator) -- sparsity is consumed only at
-// refresh boundaries (sim.cpp:704-733), so the exact recomputation costs
-// 1/tau of a step.
+// The fp64 sparsity statistics (K3a) live in k_score.cu.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -379,171 +376,6 @@ __global__ void __launch_bounds__(kThreads) attend_kernel(TkvState st, const voi
   }
 }
 
-// ---------------------------------------------------------------------------
-// K3a: exact fp64 sparsity per unit (attention.cpp:32-67, 148-167).
-// ---------------------------------------------------------------------------
-__device__ double key_d(const TkvState& st, int u, int slot, int ch) {
-  const TkvDims& dm = st.dm;
-  const int64_t gs = (int64_t)u * dm.NS + slot;
-  const int band = st.blk_thought[(int64_t)u * dm.P + slot / dm.bs];
-  const int fmt = dm.band_fmt[band];
-  const uint8_t* kr = st.slot_k + gs * dm.kstride;
-  if (fmt == TKV_FMT_RAW) return in_d(kr, dm.in_dtype, ch);
-  const int win = st.slot_win[gs];
-  const uint32_t code = tkv_get_code(kr, fmt, ch);
-  if (fmt == TKV_FMT_FP8) return tkv_decode_code(fmt, code, (double)st.win_kf[(int64_t)u * dm.NW + win]);
-  return tkv_decode_code(fmt, code, tkv_e4m3_decode(st.win_ks[((int64_t)u * dm.NW + win) * dm.D + ch]));
-}
-
-constexpr int kScoreRows = 4;  // softmax rows per pass over the keys
-
-__global__ void __launch_bounds__(kThreads) score_kernel(TkvState st, const void* __restrict__ qin,
-                                                         const void* __restrict__ kin, int buf_half, int nbuf) {
-  const TkvDims& dm = st.dm;
-  const int u = blockIdx.x;
-  const int D = dm.D, G = dm.G, P = dm.P, bs = dm.bs;
-  const int nmax = dm.NS + dm.g + 1;
-  extern __shared__ __align__(16) uint8_t dyn[];
-  double* lg = reinterpret_cast<double*>(dyn);                        // [kScoreRows][nmax]
-  double* qd = lg + (int64_t)kScoreRows * nmax;                       // [G][D]
-  int* list = reinterpret_cast<int*>(qd + (int64_t)G * D);            // [NS] physical order
-  int* scan = list + dm.NS;                                           // [kThreads]
-  __shared__ double red[kWarps];
-  __shared__ double rowsum[kScoreRows], rowmax[kScoreRows];
-  __shared__ int below[kScoreRows];
-  // live slots in physical (block, slot) order (read_active, pager.cpp:261-271)
-  const int8_t* th = st.blk_thought + (int64_t)u * P;
-  const uint8_t* fl = st.blk_filled + (int64_t)u * P;
-  const uint32_t* ev = st.blk_evict + (int64_t)u * P;
-  const int per = (P + kThreads - 1) / kThreads;
-  const int b0 = threadIdx.x * per, b1 = min(P, b0 + per);
-  int c = 0;
-  for (int b = b0; b < b1; ++b)
-    if (th[b] >= 0) c += __popc(~ev[b] & (fl[b] >= 32 ? 0xffffffffu : ((1u << fl[b]) - 1u)));
-  scan[threadIdx.x] = c;
-  for (int i = threadIdx.x; i < G * D; i += kThreads) qd[i] = in_d(qin, dm.in_dtype, (int64_t)u * G * D + i);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int i = 0; i < kThreads; ++i) { const int x = scan[i]; scan[i] = run; run += x; }
-    below[0] = run;  // nlive (temporarily)
-  }
-  __syncthreads();
-  const int nlive = below[0];
-  {
-    int w = scan[threadIdx.x];
-    for (int b = b0; b < b1; ++b) {
-      if (th[b] < 0) continue;
-      uint32_t live = ~ev[b] & (fl[b] >= 32 ? 0xffffffffu : ((1u << fl[b]) - 1u));
-      while (live) {
-        const int sl = __ffs(live) - 1;
-        live &= live - 1;
-        list[w++] = b * bs + sl;
-      }
-    }
-  }
-  __syncthreads();
-  const int n = nlive + nbuf + 1;
-  const int rows = dm.maxpool ? 1 : G;
-  const double scale = 1.0 / sqrt((double)D);
-  const int64_t brow = (int64_t)dm.g * D;
-  const uint8_t* bk = st.buf + ((int64_t)u * 4 + buf_half * 2 + 0) * brow * dm.in_bytes;
-  const uint8_t* kc = (const uint8_t*)kin + (int64_t)u * D * dm.in_bytes;
-  double total = 0.0;
-  for (int r0 = 0; r0 < rows; r0 += kScoreRows) {
-    const int nr = min(kScoreRows, rows - r0);
-    // logits of rows r0..r0+nr: one pass over each key (decoded exactly),
-    // sequential channel order per dot product (attention.cpp:32-45).
-    for (int i = threadIdx.x; i < n; i += kThreads) {
-      int fmt = TKV_FMT_RAW;
-      const uint8_t* kr;
-      const uint8_t* ksc = nullptr;
-      double kf = 1.0;
-      if (i < nlive) {
-        const int slot = list[i];
-        const int64_t gs = (int64_t)u * dm.NS + slot;
-        fmt = dm.band_fmt[th[slot / bs]];
-        kr = st.slot_k + gs * dm.kstride;
-        const int win = st.slot_win[gs];
-        if (fmt == TKV_FMT_FP8) kf = (double)st.win_kf[(int64_t)u * dm.NW + win];
-        else if (fmt != TKV_FMT_RAW) ksc = st.win_ks + ((int64_t)u * dm.NW + win) * D;
-      } else {
-        kr = i < nlive + nbuf ? bk + (int64_t)(i - nlive) * D * dm.in_bytes : kc;
-      }
-      double dot[16];
-#pragma unroll
-      for (int g = 0; g < 16; ++g) dot[g] = 0.0;
-      const int g0 = dm.maxpool ? 0 : r0, g1 = dm.maxpool ? G : r0 + nr;
-      for (int ch = 0; ch < D; ++ch) {
-        double kv;
-        if (fmt == TKV_FMT_RAW) kv = in_d(kr, dm.in_dtype, ch);
-        else if (fmt == TKV_FMT_FP8) kv = tkv_decode_code(fmt, kr[ch], kf);
-        else kv = tkv_decode_code(fmt, tkv_get_code(kr, fmt, ch), tkv_e4m3_decode(ksc[ch]));
-#pragma unroll
-        for (int g = 0; g < 16; ++g)
-          if (g >= g0 && g < g1) dot[g] = __dadd_rn(dot[g], __dmul_rn(qd[g * D + ch], kv));
-      }
-      if (dm.maxpool) {
-        double best = __dmul_rn(dot[0], scale);
-        for (int g = 1; g < G; ++g) best = fmax(best, __dmul_rn(dot[g], scale));  // gqa_aggregate
-        lg[i] = best;
-      } else {
-#pragma unroll
-        for (int g = 0; g < 16; ++g)
-          if (g >= g0 && g < g1) lg[(int64_t)(g - g0) * nmax + i] = __dmul_rn(dot[g], scale);
-      }
-    }
-    __syncthreads();
-    // softmax_row (attention.cpp:54-67) + sparsity (:148-158) per row.
-    for (int rr = 0; rr < nr; ++rr) {
-      double* L = lg + (int64_t)rr * nmax;
-      double mx = -CUDART_INF;
-      for (int i = threadIdx.x; i < n; i += kThreads) mx = fmax(mx, L[i]);
-      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double m = red[0];
-        for (int w = 1; w < kWarps; ++w) m = fmax(m, red[w]);
-        rowmax[rr] = m;
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < n; i += kThreads) L[i] = exp(__dsub_rn(L[i], rowmax[rr]));
-      __syncthreads();
-    }
-    // sequential denominators (one warp per row, lane 0 sums in order)
-    if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < nr) {
-      const double* L = lg + (int64_t)(threadIdx.x >> 5) * nmax;
-      double sum = 0.0;
-      for (int i = 0; i < n; ++i) sum = __dadd_rn(sum, L[i]);
-      rowsum[threadIdx.x >> 5] = sum;
-      below[threadIdx.x >> 5] = 0;
-    }
-    __syncthreads();
-    for (int rr = 0; rr < nr; ++rr) {
-      double* L = lg + (int64_t)rr * nmax;
-      double smax = 0.0;
-      for (int i = threadIdx.x; i < n; i += kThreads) {
-        L[i] = __ddiv_rn(L[i], rowsum[rr]);
-        smax = fmax(smax, L[i]);
-      }
-      for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = smax;
-      __syncthreads();
-      double m = red[0];
-      for (int w = 1; w < kWarps; ++w) m = fmax(m, red[w]);
-      const double thr = __dmul_rn(dm.thr_frac, m);
-      int cb = 0;
-      for (int i = threadIdx.x; i < n; i += kThreads) cb += L[i] < thr ? 1 : 0;
-      atomicAdd(&below[rr], cb);
-      __syncthreads();
-    }
-    for (int rr = 0; rr < nr; ++rr) total = __dadd_rn(total, __ddiv_rn((double)below[rr], (double)n));
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) st.sparsity[u] = __ddiv_rn(total, (double)rows);
-}
-
 template <int CPL, int GM>
 cudaError_t launch_attend_t(const TkvState& st, const void* q, const void* k, const void* v, float* out,
                             int buf_half, int nbuf, int put_half, int put_slot, cudaStream_t s) {
@@ -583,17 +415,4 @@ cudaError_t tkv_launch_attend(const TkvState& st, const void* q, const void* k, 
   if (D <= 64) return launch_attend_g<2>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
   if (D <= 128) return launch_attend_g<4>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
   return launch_attend_g<8>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
-}
-
-cudaError_t tkv_launch_score(const TkvState& st, const void* q, const void* k, int buf_half, int nbuf,
-                             cudaStream_t s) {
-  const size_t smem = (size_t)kScoreRows * (st.dm.NS + st.dm.g + 1) * 8 + (size_t)st.dm.G * st.dm.D * 8 +
-                      (size_t)st.dm.NS * 4 + (size_t)kThreads * 4;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
-  score_kernel<<<st.dm.U, kThreads, smem, s>>>(st, q, k, buf_half, nbuf);
-  return cudaGetLastError();
 }

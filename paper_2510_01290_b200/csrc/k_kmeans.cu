@@ -283,6 +283,9 @@ struct RsSmem {
   int offs[MAXM + 1];
   int cur[MAXM];
   int seeds[MAXM];
+  int colsrc[MAXM];   // per centroid column of D2: kColKeep, kColCompute, or a point whose pd column it equals
+  int ccols[MAXM];    // compacted kColCompute columns
+  int nccols;
   double tabA[MAXM + 1];  // n / (n + 1.0), indexed by cluster size (evictor.cpp:205)
   double tabR[MAXM + 1];  // -n / (n - 1.0) (evictor.cpp:201)
   double mv[MAXM];
@@ -293,17 +296,43 @@ struct RsSmem {
   double cost;
 };
 
-// D2[i][c] for all points and the given centroid rows (exact dist2).
-template <int NT>
-__device__ void fill_d2(const float* X, int XS, const double* xs, bool scaled, const double* C, int cstride, double* D2,
-                        int m, int K, int D) {
-  if (K <= 16) {
-    // small K: one (point, centroid) pair per thread, two chains for ILP
-    for (int t = threadIdx.x; t < m * K; t += 2 * NT) {
+constexpr int kColKeep = -2;     // centroid bits unchanged since D2 was filled: column still exact
+constexpr int kColCompute = -1;  // recompute the column from the centroid
+
+// D2 columns selected by s.colsrc.  A centroid that IS a point (a seed, or
+// the mean of a singleton cluster computed fresh from its member: 0 + x = x,
+// x / 1 = x) has dist2(x_i, mu) == pd[i][p] bit for bit -- same operands in
+// the same order (t = x_i - x_p, channel-sequential sum) -- so its column is
+// copied from the prep kernel's pairwise matrix; unchanged centroids keep
+// their column; only the rest are evaluated.
+template <int NT, typename SM>
+__device__ void fill_sel(SM& s, const float* X, int XS, const double* xs, bool scaled, const double* C, int cstride,
+                         double* D2, const double* __restrict__ pd, int pstride, int m, int K, int D) {
+  if (threadIdx.x < 32) {
+    int base = 0;
+    for (int c0 = 0; c0 < K; c0 += 32) {
+      const int c = c0 + (int)threadIdx.x;
+      const bool comp = c < K && s.colsrc[c] == kColCompute;
+      const unsigned bal = __ballot_sync(0xffffffffu, comp);
+      if (comp) s.ccols[base + __popc(bal & ((1u << threadIdx.x) - 1u))] = c;
+      base += __popc(bal);
+    }
+    if (threadIdx.x == 0) s.nccols = base;
+  }
+  for (int t = threadIdx.x; t < m * K; t += NT) {
+    const int i = t / K, c = t % K;
+    const int src = s.colsrc[c];
+    if (src >= 0) D2[(int64_t)i * K + c] = pd[(int64_t)i * pstride + src];
+  }
+  __syncthreads();
+  const int nc = s.nccols;
+  if (nc == 0) return;
+  if (nc <= 16) {
+    for (int t = threadIdx.x; t < m * nc; t += 2 * NT) {
       const int t2 = t + NT;
-      const bool v1 = t2 < m * K;
-      const int i0 = t / K, c0 = t % K;
-      const int i1 = v1 ? t2 / K : i0, c1 = v1 ? t2 % K : c0;
+      const bool v1 = t2 < m * nc;
+      const int i0 = t / nc, c0 = s.ccols[t % nc];
+      const int i1 = v1 ? t2 / nc : i0, c1 = v1 ? s.ccols[t2 % nc] : c0;
       const double* r0 = C + (int64_t)c0 * cstride;
       const double* r1 = C + (int64_t)c1 * cstride;
       double d0 = 0.0, d1 = 0.0;
@@ -318,15 +347,16 @@ __device__ void fill_d2(const float* X, int XS, const double* xs, bool scaled, c
     }
     return;
   }
-  // warp task = 4 points x 64 centroids (lane l -> centroids l, l + 32)
+  // warp task = 4 points x 64 compute columns (lane l -> list entries l, l + 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pblocks = (m + 3) / 4, cgroups = (K + 63) / 64;
+  const int pblocks = (m + 3) / 4, cgroups = (nc + 63) / 64;
   for (int task = warp; task < pblocks * cgroups; task += NT / 32) {
     const int pb = task / cgroups, cg = task % cgroups;
-    const int c0 = cg * 64 + lane, c1 = c0 + 32;
-    const bool v0 = c0 < K, v1 = c1 < K;
-    const double* r0 = C + (int64_t)(v0 ? c0 : 0) * cstride;
-    const double* r1 = C + (int64_t)(v1 ? c1 : 0) * cstride;
+    const int j0 = cg * 64 + lane, j1 = j0 + 32;
+    const bool v0 = j0 < nc, v1 = j1 < nc;
+    const int c0 = s.ccols[v0 ? j0 : 0], c1 = s.ccols[v1 ? j1 : 0];
+    const double* r0 = C + (int64_t)c0 * cstride;
+    const double* r1 = C + (int64_t)c1 * cstride;
     int ip[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) ip[q] = min(pb * 4 + q, m - 1);
@@ -455,10 +485,11 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     const int c = idx / D, ch = idx % D;
     Mn[(int64_t)c * MS + ch] = xval(X, xs, s.seeds[c], ch, XS, scaled);
   }
+  for (int c = threadIdx.x; c < K; c += NT) s.colsrc[c] = s.seeds[c];  // centroids are points
   __syncthreads();
   for (int iter = 0; iter < 50; ++iter) {
     kstm(st, m, 4, 1);
-    fill_d2<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D);
+    fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D);
     __syncthreads();
     for (int i = threadIdx.x; i < m; i += NT) {
       const double* row = D2 + (int64_t)i * K;
@@ -505,6 +536,8 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
         d = __dadd_rn(d, __dmul_rn(t, t));
       }
       s.mv[c] = __dsqrt_rn(d);
+      // next fill: unchanged centroid -> keep; singleton (0 + x) / 1 = x -> pd column
+      s.colsrc[c] = d == 0.0 ? kColKeep : (s.sizes[c] == 1 ? s.order[s.offs[c]] : kColCompute);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -534,7 +567,8 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     Mn[(int64_t)c * MS + ch] = div_n(acc, s.sizes[c]);
   }
   __syncthreads();
-  if (s.cost != 0.0) fill_d2<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D);
+  // Lloyd's last update left colsrc describing the final centroids (= these means)
+  if (s.cost != 0.0) fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D);
   __syncthreads();
   kstm(st, m, 6, (unsigned long long)(clock64() - t1));
   long long tmove = 0, tswap = 0;
