@@ -112,6 +112,13 @@ int tkv_step(tkv_run* run, const void* q, const void* k, const void* v, float* o
 /* Same with HOST buffers: copies q/k/v in, steps, copies out back (synchronous). */
 int tkv_step_host(tkv_run* run, const void* q, const void* k, const void* v, float* out);
 
+/* Pipelined HOST-buffer step: enqueues the upload, the step and the download
+ * and returns.  Uploads/downloads run on a copy stream through two device
+ * staging slots, so step t's transfers overlap the kernels of steps t-1/t+1.
+ * q/k/v must stay valid and unmodified, and out must not be read, until
+ * tkv_synchronize returns (use page-locked host memory for overlap). */
+int tkv_step_host_async(tkv_run* run, const void* q, const void* k, const void* v, float* out);
+
 /* Replaces ThinkvMethod::finish (sim.cpp:871-958): final partial window,
  * final budget pass, metrics. */
 int tkv_finish(tkv_run* run);

@@ -74,6 +74,10 @@ class DecodeRun {
   void process_host(const void* q, const void* k, const void* v, float* out) {
     check(tkv_step_host(h_, q, k, v, out));
   }
+  // Pipelined host-buffer step: buffers stay owned by the run until synchronize().
+  void process_host_async(const void* q, const void* k, const void* v, float* out) {
+    check(tkv_step_host_async(h_, q, k, v, out));
+  }
   void finish() { check(tkv_finish(h_)); }
   void synchronize() { check(tkv_synchronize(h_)); }
   int64_t position() const { return tkv_position(h_); }

@@ -160,6 +160,12 @@ class DecodeRun:
         ptr = (lambda a: a.ctypes.data) if hasattr(q, "ctypes") else (lambda a: a.data_ptr())
         check(lib.tkv_step_host(self._h, ptr(q), ptr(k), ptr(v), ptr(out)))
 
+    def step_host_async(self, q, k, v, out):
+        """Pipelined host-buffer step (tkv_step_host_async): returns after
+        enqueueing; buffers stay owned by the run until synchronize()."""
+        ptr = (lambda a: a.ctypes.data) if hasattr(q, "ctypes") else (lambda a: a.data_ptr())
+        check(lib.tkv_step_host_async(self._h, ptr(q), ptr(k), ptr(v), ptr(out)))
+
     def synth_inputs(self, seed: int, step: int, q, k, v, stream=None, unit0: int = 0):
         """Synthetic bf16 inputs of global units unit0.. for `step` (csrc/synth.h)."""
         s = self._stream(stream)

@@ -191,11 +191,15 @@ struct tkv_run {
   double acc_ms[5] = {0, 0, 0, 0, 0};
   int64_t acc_n[5] = {0, 0, 0, 0, 0};
   int64_t launches = 0;
-  // host-pointer step staging
-  void* d_q = nullptr;
-  void* d_k = nullptr;
-  void* d_v = nullptr;
-  float* d_out = nullptr;
+  // host-pointer step staging: two slots, copies on their own stream so the
+  // transfers of one step overlap the kernels of its neighbours
+  void* d_q[2] = {nullptr, nullptr};
+  void* d_k[2] = {nullptr, nullptr};
+  void* d_v[2] = {nullptr, nullptr};
+  float* d_out[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t h2d_done[2]{}, step_done[2]{}, d2h_done[2]{};
+  int hslot = 0;
   std::vector<void*> allocations;
 };
 
@@ -806,6 +810,7 @@ json tables_json(const tkv_run* r, const std::vector<UnitSnap>& snaps) {
 
 void check_device_errors(tkv_run* r) {
   CUDA_OK(cudaStreamSynchronize(r->stream));
+  if (r->copy_stream) CUDA_OK(cudaStreamSynchronize(r->copy_stream));
   std::vector<int32_t> err(r->st.dm.U);
   CUDA_OK(cudaMemcpy(err.data(), r->st.err, err.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
   for (size_t u = 0; u < err.size(); ++u) {
@@ -1110,6 +1115,15 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
 
 void destroy_run(tkv_run* r) {
   if (r->stream) cudaStreamSynchronize(r->stream);
+  if (r->copy_stream) {
+    cudaStreamSynchronize(r->copy_stream);
+    cudaStreamDestroy(r->copy_stream);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(r->h2d_done[i]);
+      cudaEventDestroy(r->step_done[i]);
+      cudaEventDestroy(r->d2h_done[i]);
+    }
+  }
   for (void* p : r->allocations) cudaFree(p);
   if (r->km_scratch) cudaFree(r->km_scratch);
   for (auto& t : r->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
@@ -1240,23 +1254,59 @@ int tkv_step(tkv_run* run, const void* q, const void* k, const void* v, float* o
   }
 }
 
+// Host-buffer step: H2D of this step's inputs and D2H of its output run on
+// the copy stream through one of two device staging slots; the kernels run
+// on the run's stream.  Step t's upload overlaps step t-1's kernels and step
+// t-1's download overlaps step t's kernels.
+void step_host_async(tkv_run* run, const void* q, const void* k, const void* v, float* out) {
+  const TkvDims& dm = run->st.dm;
+  const size_t qb = (size_t)dm.U * dm.G * dm.D * dm.in_bytes, kb = (size_t)dm.U * dm.D * dm.in_bytes;
+  const size_t ob = (size_t)dm.U * (dm.maxpool ? 1 : dm.G) * dm.D * sizeof(float);
+  if (!run->copy_stream) {
+    CUDA_OK(cudaStreamCreateWithFlags(&run->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      run->d_q[i] = dalloc<uint8_t>(run, qb);
+      run->d_k[i] = dalloc<uint8_t>(run, kb);
+      run->d_v[i] = dalloc<uint8_t>(run, kb);
+      run->d_out[i] = dalloc<float>(run, ob / sizeof(float));
+      CUDA_OK(cudaEventCreateWithFlags(&run->h2d_done[i], cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&run->step_done[i], cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&run->d2h_done[i], cudaEventDisableTiming));
+      CUDA_OK(cudaEventRecord(run->step_done[i], run->stream));
+    }
+  }
+  const int sl = run->hslot;
+  run->hslot ^= 1;
+  // the slot's previous step must be done reading its inputs / writing its output
+  CUDA_OK(cudaStreamWaitEvent(run->copy_stream, run->step_done[sl], 0));
+  CUDA_OK(cudaMemcpyAsync(run->d_q[sl], q, qb, cudaMemcpyHostToDevice, run->copy_stream));
+  CUDA_OK(cudaMemcpyAsync(run->d_k[sl], k, kb, cudaMemcpyHostToDevice, run->copy_stream));
+  CUDA_OK(cudaMemcpyAsync(run->d_v[sl], v, kb, cudaMemcpyHostToDevice, run->copy_stream));
+  CUDA_OK(cudaEventRecord(run->h2d_done[sl], run->copy_stream));
+  CUDA_OK(cudaStreamWaitEvent(run->stream, run->h2d_done[sl], 0));
+  CUDA_OK(cudaStreamWaitEvent(run->stream, run->d2h_done[sl], 0));  // d_out[sl] drained
+  do_step(run, run->d_q[sl], run->d_k[sl], run->d_v[sl], run->d_out[sl]);
+  CUDA_OK(cudaEventRecord(run->step_done[sl], run->stream));
+  CUDA_OK(cudaStreamWaitEvent(run->copy_stream, run->step_done[sl], 0));
+  CUDA_OK(cudaMemcpyAsync(out, run->d_out[sl], ob, cudaMemcpyDeviceToHost, run->copy_stream));
+  CUDA_OK(cudaEventRecord(run->d2h_done[sl], run->copy_stream));
+}
+
 int tkv_step_host(tkv_run* run, const void* q, const void* k, const void* v, float* out) {
   try {
-    const TkvDims& dm = run->st.dm;
-    const size_t qb = (size_t)dm.U * dm.G * dm.D * dm.in_bytes, kb = (size_t)dm.U * dm.D * dm.in_bytes;
-    const size_t ob = (size_t)dm.U * (dm.maxpool ? 1 : dm.G) * dm.D * sizeof(float);
-    if (!run->d_q) {
-      run->d_q = dalloc<uint8_t>(run, qb);
-      run->d_k = dalloc<uint8_t>(run, kb);
-      run->d_v = dalloc<uint8_t>(run, kb);
-      run->d_out = dalloc<float>(run, ob / sizeof(float));
-    }
-    CUDA_OK(cudaMemcpyAsync(run->d_q, q, qb, cudaMemcpyHostToDevice, run->stream));
-    CUDA_OK(cudaMemcpyAsync(run->d_k, k, kb, cudaMemcpyHostToDevice, run->stream));
-    CUDA_OK(cudaMemcpyAsync(run->d_v, v, kb, cudaMemcpyHostToDevice, run->stream));
-    do_step(run, run->d_q, run->d_k, run->d_v, run->d_out);
-    CUDA_OK(cudaMemcpyAsync(out, run->d_out, ob, cudaMemcpyDeviceToHost, run->stream));
-    CUDA_OK(cudaStreamSynchronize(run->stream));
+    step_host_async(run, q, k, v, out);
+    CUDA_OK(cudaStreamSynchronize(run->copy_stream));
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_step_host_async(tkv_run* run, const void* q, const void* k, const void* v, float* out) {
+  try {
+    step_host_async(run, q, k, v, out);
     return TKV_OK;
   } catch (const TkvError& e) {
     return fail(e);

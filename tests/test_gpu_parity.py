@@ -128,3 +128,32 @@ def test_device_synth_matches_host_generator():
         torch.cuda.synchronize()
         for got, want in ((q, hq), (k, hk), (v, hv)):
             assert np.array_equal(got.cpu().view(torch.int16).numpy().view(np.uint16), want)
+
+
+def test_host_buffer_steps_match_device_steps():
+    """tkv_step_host / tkv_step_host_async (staged uploads on a copy stream)
+    produce the same outputs and cache state as device-pointer steps."""
+    cfg = ThinkvConfig(num_seqs=2, units_per_seq=2, num_q_heads=4, head_dim=128, tau=32, group_size=16,
+                       block_size=16, budget=64, levels=(16, 8, 4), max_gen_len=200, script=script(2, 8),
+                       record_events=True)
+    dev = torch.device("cuda:0")
+    a, b, c = DecodeRun(cfg), DecodeRun(cfg), DecodeRun(cfg)
+    out = torch.empty((cfg.units, 4, 128), device=dev)
+    outs_b = [torch.empty((cfg.units, 4, 128)).pin_memory() for _ in range(2)]
+    out_c = torch.empty((cfg.units, 4, 128)).pin_memory()
+    for t in range(cfg.max_gen_len):
+        q, k, v = O.synth_step(0x71534B56, cfg.units_per_seq, cfg.tau, cfg.units, 4, 128, t)
+        tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16) for x in (q, k, v))
+        a.step(tq.to(dev), tk.to(dev), tv.to(dev), out)
+        pq, pk, pv = tq.pin_memory(), tk.pin_memory(), tv.pin_memory()
+        b.step_host_async(pq, pk, pv, outs_b[t % 2])
+        c.step_host(tq.contiguous(), tk.contiguous(), tv.contiguous(), out_c)
+        b.synchronize()  # pq/pk/pv are released at the end of the iteration
+        ref = out.cpu()
+        assert torch.equal(outs_b[t % 2], ref)
+        assert torch.equal(out_c, ref)
+    for r in (a, b, c):
+        r.finish()
+    for s in range(2):
+        assert b.tables(s) == a.tables(s) and c.tables(s) == a.tables(s)
+        assert b.events(s) == a.events(s)
