@@ -1,34 +1,49 @@
 // K1 (tensor-core variant): paged mixed-precision decode attention for
 // head_dim 64/128, bf16 inputs, G <= 8 query heads per KV head.
 //
-// One CTA (4 warps) per unit.  The live slots (compacted per storage format,
-// with their window indices) plus the raw tail (the unit's fp buffer and the
-// incoming token, sim.cpp:546-563, 762-765) are cut into 16-token tiles that
-// are dealt round-robin to the warps:
+// Reference semantics (what one unit computes per step): the live pager slots
+// in physical (block, slot) order (BlockPager::read_active, proj/src/
+// pager.cpp:261-271), then the fp buffer, then the incoming token at full
+// precision (sim.cpp:546-563, 762-765); gqa_attend (attention.cpp:124-138):
+// logits q.k / sqrt(d), per-head rows or the max over the G rows
+// (gqa_aggregate, :110-122), softmax, probability-weighted values.  The
+// output does not depend on the key order, so the kernel is free to group the
+// live slots by storage format.
+//
+// One CTA (4 warps) per unit.  Prologue: scan the unit's block table, build
+// per-format live lists (slot, window) in shared memory, each padded to a
+// whole 16-token tile with copies of its first entry (padding rows are masked
+// to -inf logits, so they contribute exactly zero); the fp buffer and the
+// incoming token form the raw "tail" list.  Tiles are numbered across formats
+// and dealt round-robin to the warps.  Per tile:
 //
 //   QK^T   mma.m16n8k16 -> f32, A = dequantised K tile (16 tokens x 16
-//          channels per k-step), B = q^T (16 channels x 8 heads, heads >= G
-//          zero).  The dot product is permutation-invariant, so k-step j of
-//          thread (gid, tig) is mapped to physical channels tig*D/4 + 4j..4j+3:
-//          every thread's K codes are ONE contiguous 128/64-bit load per row.
+//          channels per k-step), B = q^T (heads >= G are zero).  k-step j of
+//          thread (gid, tig) is mapped to physical channels tig*D/4 + 4j..4j+3
+//          (the dot product is order-free), so each thread's K codes and key
+//          scales of a row are contiguous vector loads.
 //   PV     mma.m16n8k16 with A = V^T (channels x tokens), B = P (tokens x
-//          heads) split into hi + lo parts (two mmas) so the probabilities
-//          keep ~22 (f16) / ~16 (bf16) bits; thread gid owns the contiguous
-//          channels [gid*D/8, (gid+1)*D/8), which is exactly one E4M3
-//          value-chunk scale (g = 16) and one 64/32-bit code load per token.
+//          heads) split into hi + lo halves (two mmas) so probabilities keep
+//          ~22 (f16) / ~16 (bf16) bits; thread gid owns channels
+//          [gid*D/8, (gid+1)*D/8) = one E4M3 value-chunk scale (g = 16).
 //
-// Quantised tiles (NVFP4 / ternary / FP8) run f16 MMAs: codes are expanded in
-// registers with the sm_100 converters (F2FP.F16.E2M1 / F2FP.F16.E4M3) and one
-// HMUL2 by the E4M3 group scale; every code x scale product is exact in f16
-// (<= 8 significant bits, range 2^-10 .. 2688), so QK^T products are exact and
-// accumulate in fp32.  FP8 windows keep their fp32 per-window scale out of the
-// MMA (applied to the logit / folded into P).  Raw tiles -- 16-bit passthrough
-// slots and the tail -- run bf16 MMAs on the stored bf16 words directly (q, K
-// and V are exact in bf16).  Online softmax runs in the log2 domain in fp32.
-// Loads of tile t+1 are issued before tile t is computed (register double
-// buffering).
+// Dequantisation uses the sm_100 converters F2FP.F16.E2M1 / F2FP.F16.E4M3
+// with their byte / half-word operand selectors (PTX mov.b32 unpack), so no
+// shift/mask instruction extracts a code.  Ternary codes are spread to e2m1
+// nibbles (+-1.0) with a Morton bit spread.  code x E4M3 scale products are
+// exact in f16 (<= 8 significant bits, range 2^-10 .. 2688): QK^T products
+// are exact, accumulated in fp32.  FP8 windows keep their fp32 per-window
+// scale out of the MMA (applied to the logit / folded into P).  Raw tiles
+// (16-bit passthrough slots and the tail) run bf16 MMAs on the stored words.
+// Online softmax in the log2 domain with lazy rescaling: the running max is
+// only raised when a tile exceeds it by more than 2^8, so the accumulators
+// are rescaled rarely; O and l always share the same reference max, so the
+// result is the same softmax.  Loads of the next tile are issued before the
+// current one is computed (two register tiles, ping-pong without copies).
 #include <cuda_runtime.h>
 #include <math_constants.h>
+
+#include <cstdlib>
 
 #include "tkv_kernels.h"
 #include "tkv_state.h"
@@ -38,29 +53,47 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int kWarps = 4;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kFmtTail = 4;  // pseudo-format: raw bf16 tiles (RAW slots + tail)
+constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
+constexpr int kFmtTail = 4;       // pseudo-format: raw bf16 tiles (RAW slots + tail)
 
-__device__ __forceinline__ uint32_t fp4x2_f16x2(uint32_t b) {
-  uint32_t r;
-  asm("{\n .reg .b8 t;\n cvt.u8.u32 t, %1;\n cvt.rn.f16x2.e2m1x2 %0, t;\n}" : "=r"(r) : "r"(b));
-  return r;
+// ---- converters (byte / half selectors come free with mov.b32 unpack) -------
+__device__ __forceinline__ void e2m1x8(uint32_t w, uint32_t (&r)[4]) {
+  asm("{\n .reg .b8 b0, b1, b2, b3;\n mov.b32 {b0, b1, b2, b3}, %4;\n"
+      " cvt.rn.f16x2.e2m1x2 %0, b0;\n cvt.rn.f16x2.e2m1x2 %1, b1;\n"
+      " cvt.rn.f16x2.e2m1x2 %2, b2;\n cvt.rn.f16x2.e2m1x2 %3, b3;\n}"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(w));
 }
-__device__ __forceinline__ uint32_t e4m3x2_f16x2(uint32_t h) {
-  uint32_t r;
-  asm("{\n .reg .b16 t;\n cvt.u16.u32 t, %1;\n cvt.rn.f16x2.e4m3x2 %0, t;\n}" : "=r"(r) : "r"(h));
-  return r;
+__device__ __forceinline__ void e2m1x2_b(uint32_t w, int byte, uint32_t& r) {
+  // byte is a compile-time constant after unrolling
+  if (byte == 0) asm("{\n .reg .b8 b0, b1, b2, b3;\n mov.b32 {b0, b1, b2, b3}, %1;\n cvt.rn.f16x2.e2m1x2 %0, b0;\n}" : "=r"(r) : "r"(w));
+  else if (byte == 1) asm("{\n .reg .b8 b0, b1, b2, b3;\n mov.b32 {b0, b1, b2, b3}, %1;\n cvt.rn.f16x2.e2m1x2 %0, b1;\n}" : "=r"(r) : "r"(w));
+  else if (byte == 2) asm("{\n .reg .b8 b0, b1, b2, b3;\n mov.b32 {b0, b1, b2, b3}, %1;\n cvt.rn.f16x2.e2m1x2 %0, b2;\n}" : "=r"(r) : "r"(w));
+  else asm("{\n .reg .b8 b0, b1, b2, b3;\n mov.b32 {b0, b1, b2, b3}, %1;\n cvt.rn.f16x2.e2m1x2 %0, b3;\n}" : "=r"(r) : "r"(w));
+}
+__device__ __forceinline__ void e4m3x4(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  asm("{\n .reg .b16 h0, h1;\n mov.b32 {h0, h1}, %2;\n"
+      " cvt.rn.f16x2.e4m3x2 %0, h0;\n cvt.rn.f16x2.e4m3x2 %1, h1;\n}"
+      : "=r"(lo), "=r"(hi) : "r"(w));
+}
+__device__ __forceinline__ void e4m3x2_b(uint32_t w, int byte, uint32_t& r) {
+  // one E4M3 byte duplicated into both f16 halves: (b, b) -> f16x2
+  const uint32_t b = __byte_perm(w, 0u, byte == 0 ? 0x4400 : byte == 1 ? 0x4411 : byte == 2 ? 0x4422 : 0x4433);
+  asm("{\n .reg .b16 h0, h1;\n mov.b32 {h0, h1}, %1;\n cvt.rn.f16x2.e4m3x2 %0, h0;\n}" : "=r"(r) : "r"(b));
 }
 __device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
   return r;
 }
-// Two ternary 2-bit codes (sign/magnitude, quant.cpp:219-236) -> f16x2.
-__device__ __forceinline__ uint32_t tern2_f16x2(uint32_t nib) {
-  const uint32_t c0 = nib & 3u, c1 = (nib >> 2) & 3u;
-  const uint32_t h0 = (c0 & 1u) ? (0x3C00u | ((c0 & 2u) << 14)) : 0u;
-  const uint32_t h1 = (c1 & 1u) ? (0x3C00u | ((c1 & 2u) << 14)) : 0u;
-  return h0 | (h1 << 16);
+// 8 ternary sign/magnitude codes (2 bits each, quant.cpp:219-236) -> 8 e2m1
+// nibbles: magnitude bit -> e2m1 bit 1 (1.0), sign bit -> bit 3.
+__device__ __forceinline__ uint32_t tern_spread(uint32_t h16) {
+  uint32_t x = h16 & 0xffffu;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x << 1;
 }
 __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
   uint32_t r;
@@ -136,7 +169,8 @@ struct Geo {
   static constexpr int VBYTES = VPT * BITS / 8;  // per token per thread
   static constexpr int KW = KBYTES / 4;
   static constexpr int VW = VBYTES >= 4 ? VBYTES / 4 : 1;
-  static constexpr int SW = FMT == kFmtTail ? 1 : CPT / 4;  // key-scale words per row per thread
+  static constexpr bool SCALED = FMT == TKV_FMT_NVFP4 || FMT == TKV_FMT_TERNARY;
+  static constexpr int SW = SCALED ? CPT / 4 : 1;  // key-scale words per row per thread
   static constexpr bool BF16 = FMT == kFmtTail;
 };
 
@@ -146,60 +180,55 @@ struct Tile {
   Words<Gm::KW> k[2];
   Words<Gm::SW> ks[2];
   Words<Gm::VW> v[4];
-  uint32_t vs[4];     // value scale code (grouped) per PV token
+  uint32_t vs[4];     // value-chunk scale byte per PV token (grouped formats)
   float kf[2];        // fp8 key scale per row
   float vf[4];        // fp8 value scale per PV token
-  bool krow_ok[2];
-  bool vtok_ok[4];
 };
 
-// Row addresses.  Tail entries are encoded as (-1 - t, 0): t < nbuf is buffer
-// row t, t == nbuf the incoming token.
-struct TailSrc {
-  const uint8_t* bk;
+// Per-unit base pointers (computed once per CTA).
+struct UnitPtrs {
+  const uint8_t* k;   // slot_k of the unit
+  const uint8_t* v;
+  const uint8_t* vs;  // slot_vs
+  const uint8_t* ks;  // win_ks
+  const float* kf;
+  const float* vf;
+  const uint8_t* bk;  // fp buffer keys / values (current half)
   const uint8_t* bv;
-  const uint8_t* kc;
+  const uint8_t* kc;  // incoming token
   const uint8_t* vc;
-  int nbuf;
+  int kstride, vchunks, nbuf, vsel;  // vsel: value-chunk index of this thread
 };
 
+// List entries: (slot, window).  Tail entries are (-1 - t, 0): t < nbuf is
+// buffer row t, t == nbuf the incoming token.
 template <int D, int FMT>
-__device__ __forceinline__ void load_tile(const TkvState& st, int u, const int2* lst, int n, int t0, int gid,
-                                          int tig, const TailSrc& ts, Tile<D, FMT>& T) {
+__device__ __forceinline__ void load_tile(const UnitPtrs& up, const int2* lst, int t0, int gid, int tig,
+                                          Tile<D, FMT>& T) {
   using Gm = Geo<D, FMT>;
-  const TkvDims& dm = st.dm;
-  const int64_t ubase = (int64_t)u * dm.NS;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int idx = t0 + gid + 8 * r;
-    T.krow_ok[r] = idx < n;
-    const int2 e = lst[T.krow_ok[r] ? idx : 0];
+    const int2 e = lst[t0 + gid + 8 * r];
     const uint8_t* kr;
     if constexpr (FMT == kFmtTail) {
-      if (e.x >= 0) kr = st.slot_k + (ubase + e.x) * dm.kstride;
-      else kr = (-1 - e.x) < ts.nbuf ? ts.bk + (int64_t)(-1 - e.x) * D * 2 : ts.kc;
+      if (e.x >= 0) kr = up.k + e.x * up.kstride;
+      else kr = (-1 - e.x) < up.nbuf ? up.bk + (-1 - e.x) * (D * 2) : up.kc;
     } else {
-      kr = st.slot_k + (ubase + e.x) * dm.kstride;
+      kr = up.k + e.x * up.kstride;
     }
     T.k[r] = ldg_words<Gm::KW>(kr + tig * Gm::KBYTES);
-    if constexpr (FMT == TKV_FMT_FP8) {
-      T.kf[r] = __ldg(st.win_kf + (int64_t)u * dm.NW + e.y);
-    } else if constexpr (FMT != kFmtTail) {
-      const uint8_t* sc = st.win_ks + ((int64_t)u * dm.NW + e.y) * D + tig * Gm::CPT;
-      T.ks[r] = ldg_words<Gm::SW>(sc);
-    }
+    if constexpr (FMT == TKV_FMT_FP8) T.kf[r] = __ldg(up.kf + e.y);
+    if constexpr (Gm::SCALED) T.ks[r] = ldg_words<Gm::SW>(up.ks + e.y * D + tig * Gm::CPT);
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int idx = t0 + tig * 2 + (i & 1) + 8 * (i >> 1);
-    T.vtok_ok[i] = idx < n;
-    const int2 e = lst[T.vtok_ok[i] ? idx : 0];
+    const int2 e = lst[t0 + tig * 2 + (i & 1) + 8 * (i >> 1)];
     const uint8_t* vr;
     if constexpr (FMT == kFmtTail) {
-      if (e.x >= 0) vr = st.slot_v + (ubase + e.x) * dm.kstride;
-      else vr = (-1 - e.x) < ts.nbuf ? ts.bv + (int64_t)(-1 - e.x) * D * 2 : ts.vc;
+      if (e.x >= 0) vr = up.v + e.x * up.kstride;
+      else vr = (-1 - e.x) < up.nbuf ? up.bv + (-1 - e.x) * (D * 2) : up.vc;
     } else {
-      vr = st.slot_v + (ubase + e.x) * dm.kstride;
+      vr = up.v + e.x * up.kstride;
     }
     vr += gid * Gm::VBYTES;
     if constexpr (Gm::VBYTES >= 4) {
@@ -207,60 +236,75 @@ __device__ __forceinline__ void load_tile(const TkvState& st, int u, const int2*
     } else {
       T.v[i].w[0] = Gm::VBYTES == 2 ? (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(vr)) : (uint32_t)__ldg(vr);
     }
-    if constexpr (FMT == TKV_FMT_FP8) {
-      T.vf[i] = __ldg(st.win_vf + (int64_t)u * dm.NW + e.y);
-    } else if constexpr (FMT != kFmtTail) {
-      T.vs[i] = __ldg(st.slot_vs + (ubase + e.x) * dm.vchunks + (gid * Gm::VPT) / dm.g);
-    }
+    if constexpr (FMT == TKV_FMT_FP8) T.vf[i] = __ldg(up.vf + e.y);
+    if constexpr (Gm::SCALED) T.vs[i] = __ldg(up.vs + e.x * up.vchunks + up.vsel);
   }
 }
 
 template <int D>
 struct Acc {
   float o[D / 16][4];
-  float m[2], l[2];  // heads tig*2, tig*2+1
+  float m[2], l[2];  // heads tig*2, tig*2+1 (log2 domain reference max, denominator)
 };
 
 template <int D, int FMT>
 __device__ __forceinline__ void compute_tile(const Tile<D, FMT>& T, const uint32_t (&qb)[D / 16][2],
-                                             const uint32_t* qbb, float qscale, int G, bool maxpool, int gid,
-                                             int tig, float* ps, Acc<D>& A) {
+                                             const uint32_t* qbb, float qscale, int G, bool maxpool, int nvalid,
+                                             int gid, int tig, float* ps, Acc<D>& A) {
   using Gm = Geo<D, FMT>;
   // ---- S = K q^T ----------------------------------------------------------
   float s[4] = {0.f, 0.f, 0.f, 0.f};
+  if constexpr (FMT == TKV_FMT_TERNARY) {
+    // 8 codes per 16-bit half -> 8 e2m1 nibbles (one word), 4 k-steps per code word
 #pragma unroll
-  for (int j = 0; j < Gm::KT; ++j) {
-    uint32_t a[4];
+    for (int jw = 0; jw < Gm::KW; ++jw) {
+      uint32_t nib[2][2];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      uint32_t lo, hi;
-      if constexpr (FMT == TKV_FMT_NVFP4) {
-        const uint32_t byte2 = (T.k[r].w[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-        lo = fp4x2_f16x2(byte2 & 0xffu);
-        hi = fp4x2_f16x2(byte2 >> 8);
-      } else if constexpr (FMT == TKV_FMT_FP8) {
-        lo = e4m3x2_f16x2(T.k[r].w[j] & 0xffffu);
-        hi = e4m3x2_f16x2(T.k[r].w[j] >> 16);
-      } else if constexpr (FMT == TKV_FMT_TERNARY) {
-        const uint32_t byte = (T.k[r].w[j >> 2] >> ((j & 3) * 8)) & 0xffu;
-        lo = tern2_f16x2(byte & 15u);
-        hi = tern2_f16x2(byte >> 4);
-      } else {  // raw bf16 words: channels 4j, 4j+1 | 4j+2, 4j+3
-        lo = T.k[r].w[2 * j];
-        hi = T.k[r].w[2 * j + 1];
+      for (int r = 0; r < 2; ++r) {
+        nib[r][0] = tern_spread(T.k[r].w[jw]);
+        nib[r][1] = tern_spread(T.k[r].w[jw] >> 16);
       }
-      if constexpr (FMT == TKV_FMT_NVFP4 || FMT == TKV_FMT_TERNARY) {
-        const uint32_t sw = T.ks[r].w[j];
-        lo = hmul2(lo, e4m3x2_f16x2(sw & 0xffffu));
-        hi = hmul2(hi, e4m3x2_f16x2(sw >> 16));
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = jw * 4 + jj;
+        uint32_t a[4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          uint32_t lo, hi, slo, shi;
+          e2m1x2_b(nib[r][jj >> 1], (jj & 1) * 2, lo);
+          e2m1x2_b(nib[r][jj >> 1], (jj & 1) * 2 + 1, hi);
+          e4m3x4(T.ks[r].w[j], slo, shi);
+          a[r] = hmul2(lo, slo);
+          a[2 + r] = hmul2(hi, shi);
+        }
+        mma16816<false>(s, a[0], a[1], a[2], a[3], qb[j][0], qb[j][1]);
       }
-      a[r] = lo;       // a0a1 (row gid) / a2a3 (row gid+8), cols tig*2..+1
-      a[2 + r] = hi;   // a4a5 / a6a7, cols tig*2+8..+9
     }
-    if constexpr (Gm::BF16) {
-      mma16816<true>(s, a[0], a[1], a[2], a[3], qbb[j * 2], qbb[j * 2 + 1]);
-    } else {
-      mma16816<false>(s, a[0], a[1], a[2], a[3], qb[j][0], qb[j][1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < Gm::KT; ++j) {
+      uint32_t a[4];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        uint32_t lo, hi;
+        if constexpr (FMT == TKV_FMT_NVFP4) {
+          e2m1x2_b(T.k[r].w[j >> 1], (j & 1) * 2, lo);
+          e2m1x2_b(T.k[r].w[j >> 1], (j & 1) * 2 + 1, hi);
+          uint32_t slo, shi;
+          e4m3x4(T.ks[r].w[j], slo, shi);
+          lo = hmul2(lo, slo);
+          hi = hmul2(hi, shi);
+        } else if constexpr (FMT == TKV_FMT_FP8) {
+          e4m3x4(T.k[r].w[j], lo, hi);
+        } else {  // raw bf16 words: channels 4j, 4j+1 | 4j+2, 4j+3
+          lo = T.k[r].w[2 * j];
+          hi = T.k[r].w[2 * j + 1];
+        }
+        a[r] = lo;       // a0a1 (row gid) / a2a3 (row gid+8), cols tig*2..+1
+        a[2 + r] = hi;   // a4a5 / a6a7, cols tig*2+8..+9
+      }
+      if constexpr (Gm::BF16) mma16816<true>(s, a[0], a[1], a[2], a[3], qbb[j * 2], qbb[j * 2 + 1]);
+      else mma16816<false>(s, a[0], a[1], a[2], a[3], qb[j][0], qb[j][1]);
     }
   }
   // logits (log2 domain); rows: s0,s1 -> token gid, s2,s3 -> token gid+8
@@ -270,7 +314,7 @@ __device__ __forceinline__ void compute_tile(const Tile<D, FMT>& T, const uint32
     const int r = i >> 1, h = tig * 2 + (i & 1);
     float x = s[i] * qscale;
     if constexpr (FMT == TKV_FMT_FP8) x *= T.kf[r];
-    L[i] = (T.krow_ok[r] && h < G) ? x : -CUDART_INF_F;
+    L[i] = (gid + 8 * r < nvalid && h < G) ? x : -CUDART_INF_F;
   }
   if (maxpool) {
     // one pooled row per token: max over the G heads, kept in column 0
@@ -283,29 +327,44 @@ __device__ __forceinline__ void compute_tile(const Tile<D, FMT>& T, const uint32
       L[2 * r + 1] = -CUDART_INF_F;
     }
   }
-  // ---- online softmax per head column --------------------------------------
+  // ---- online softmax per head column (lazy rescale) -------------------------
   float p[4];
+  bool grow = false;
+  float mnew[2];
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     float tmax = fmaxf(L[c], L[2 + c]);
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
-    const float mnew = fmaxf(A.m[c], tmax);
-    const float corr = mnew == -CUDART_INF_F ? 1.0f : exp2f(A.m[c] - mnew);
-    p[c] = mnew == -CUDART_INF_F ? 0.0f : exp2f(L[c] - mnew);
-    p[2 + c] = mnew == -CUDART_INF_F ? 0.0f : exp2f(L[2 + c] - mnew);
+    mnew[c] = tmax > A.m[c] + kRescale ? tmax : A.m[c];
+    grow = grow || mnew[c] != A.m[c];
+  }
+  if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const float corr = A.m[c] == -CUDART_INF_F ? 0.0f : exp2f(A.m[c] - mnew[c]);
+      if (mnew[c] != A.m[c]) {
+        A.l[c] *= corr;
+#pragma unroll
+        for (int mt = 0; mt < Gm::MT; ++mt) {
+          A.o[mt][c] *= corr;
+          A.o[mt][2 + c] *= corr;
+        }
+        A.m[c] = mnew[c];
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const bool live = A.m[c] != -CUDART_INF_F;
+    p[c] = live ? exp2f(L[c] - A.m[c]) : 0.0f;
+    p[2 + c] = live ? exp2f(L[2 + c] - A.m[c]) : 0.0f;
     float sum = p[c] + p[2 + c];
     sum += __shfl_xor_sync(0xffffffffu, sum, 4);
     sum += __shfl_xor_sync(0xffffffffu, sum, 8);
     sum += __shfl_xor_sync(0xffffffffu, sum, 16);
-    A.l[c] = A.l[c] * corr + sum;
-    A.m[c] = mnew;
-#pragma unroll
-    for (int mt = 0; mt < Gm::MT; ++mt) {
-      A.o[mt][c] *= corr;
-      A.o[mt][2 + c] *= corr;
-    }
+    A.l[c] += sum;
   }
   // ---- P: C layout (token, head) -> B layout (token = k, head = n) -----------
   ps[gid * 8 + tig * 2] = p[0];
@@ -316,9 +375,8 @@ __device__ __forceinline__ void compute_tile(const Tile<D, FMT>& T, const uint32
   float pb[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int tok = tig * 2 + (i & 1) + 8 * (i >> 1);
-    pb[i] = ps[tok * 8 + gid];
-    if constexpr (FMT == TKV_FMT_FP8) pb[i] *= T.vtok_ok[i] ? T.vf[i] : 0.0f;
+    pb[i] = ps[(tig * 2 + (i & 1) + 8 * (i >> 1)) * 8 + gid];
+    if constexpr (FMT == TKV_FMT_FP8) pb[i] *= T.vf[i];
   }
   __syncwarp();
   uint32_t bh0, bh1, bl0, bl1;
@@ -335,26 +393,38 @@ __device__ __forceinline__ void compute_tile(const Tile<D, FMT>& T, const uint32
   }
   // ---- O^T += V^T P ----------------------------------------------------------
   uint32_t vsc[4];
-  if constexpr (FMT == TKV_FMT_NVFP4 || FMT == TKV_FMT_TERNARY) {
+  if constexpr (Gm::SCALED) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) vsc[i] = e4m3x2_f16x2(T.vs[i] | (T.vs[i] << 8));
+    for (int i = 0; i < 4; ++i) e4m3x2_b(T.vs[i], 0, vsc[i]);
+  }
+  uint32_t tsp[4][(Gm::MT + 3) / 4];  // ternary: e2m1 nibbles of each 8-code half-word
+  if constexpr (FMT == TKV_FMT_TERNARY) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int h = 0; h < (Gm::MT + 3) / 4; ++h) tsp[i][h] = tern_spread(T.v[i].w[0] >> (16 * h));
   }
 #pragma unroll
   for (int mt = 0; mt < Gm::MT; ++mt) {
-    uint32_t x[4];  // per PV token: x2 of channels (2mt, 2mt+1) of the thread's range
+    uint32_t x[4];  // per PV token: f16x2 / bf16x2 of channels (2mt, 2mt+1) of the thread's range
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      uint32_t h;
       if constexpr (FMT == TKV_FMT_NVFP4) {
-        h = hmul2(fp4x2_f16x2((T.v[i].w[mt >> 2] >> ((mt & 3) * 8)) & 0xffu), vsc[i]);
+        uint32_t h;
+        e2m1x2_b(T.v[i].w[mt >> 2], mt & 3, h);
+        x[i] = hmul2(h, vsc[i]);
       } else if constexpr (FMT == TKV_FMT_FP8) {
-        h = e4m3x2_f16x2((T.v[i].w[mt >> 1] >> ((mt & 1) * 16)) & 0xffffu);
+        uint32_t lo, hi;
+        e4m3x4(T.v[i].w[mt >> 1], lo, hi);
+        x[i] = (mt & 1) ? hi : lo;
       } else if constexpr (FMT == TKV_FMT_TERNARY) {
-        h = hmul2(tern2_f16x2((T.v[i].w[0] >> (mt * 4)) & 15u), vsc[i]);
+        // codes 2mt, 2mt+1 = byte mt & 3 of the spread of half-word mt >> 2
+        uint32_t h;
+        e2m1x2_b(tsp[i][mt >> 2], mt & 3, h);
+        x[i] = hmul2(h, vsc[i]);
       } else {
-        h = T.v[i].w[mt];
+        x[i] = T.v[i].w[mt];
       }
-      x[i] = T.vtok_ok[i] ? h : 0u;
     }
     const uint32_t a0 = __byte_perm(x[0], x[1], 0x5410);  // row gid (ch 2mt), tokens tig*2, tig*2+1
     const uint32_t a1 = __byte_perm(x[0], x[1], 0x7632);  // row gid+8 (ch 2mt+1)
@@ -365,35 +435,39 @@ __device__ __forceinline__ void compute_tile(const Tile<D, FMT>& T, const uint32
   }
 }
 
-// Tiles of one format with index (global) g = warp + k * kWarps in [g0, g1).
+// Tiles of one format with global tile index g = warp + k * kWarps in
+// [g0, g0 + tiles); the list is padded to whole tiles.
 template <int D, int FMT>
-__device__ __forceinline__ void run_format(const TkvState& st, int u, const int2* lst, int n, int g0, int warp,
+__device__ __forceinline__ void run_format(const UnitPtrs& up, const int2* lst, int n, int g0, int warp,
                                            const uint32_t (&qb)[D / 16][2], const uint32_t* qbb, float qscale,
-                                           bool maxpool, int gid, int tig, const TailSrc& ts, float* ps, Acc<D>& A) {
+                                           int G, bool maxpool, int gid, int tig, float* ps, Acc<D>& A) {
   const int tiles = (n + 15) / 16;
-  // first tile index of this format handled by this warp
   int t = ((warp - g0) % kWarps + kWarps) % kWarps;
   if (t >= tiles) return;
   if constexpr (FMT == kFmtTail) {  // few tiles, wide rows: no double buffering (registers)
     for (; t < tiles; t += kWarps) {
       Tile<D, FMT> cur;
-      load_tile<D, FMT>(st, u, lst, n, t * 16, gid, tig, ts, cur);
-      compute_tile<D, FMT>(cur, qb, qbb, qscale, st.dm.G, maxpool, gid, tig, ps, A);
+      load_tile<D, FMT>(up, lst, t * 16, gid, tig, cur);
+      compute_tile<D, FMT>(cur, qb, qbb, qscale, G, maxpool, n - t * 16, gid, tig, ps, A);
     }
     return;
   }
-  Tile<D, FMT> cur, nxt;
-  load_tile<D, FMT>(st, u, lst, n, t * 16, gid, tig, ts, cur);
-  for (; t < tiles; t += kWarps) {
-    const bool more = t + kWarps < tiles;
-    if (more) load_tile<D, FMT>(st, u, lst, n, (t + kWarps) * 16, gid, tig, ts, nxt);
-    compute_tile<D, FMT>(cur, qb, qbb, qscale, st.dm.G, maxpool, gid, tig, ps, A);
-    if (more) cur = nxt;
+  Tile<D, FMT> ta, tb;
+  load_tile<D, FMT>(up, lst, t * 16, gid, tig, ta);
+  while (true) {
+    if (t + kWarps < tiles) load_tile<D, FMT>(up, lst, (t + kWarps) * 16, gid, tig, tb);
+    compute_tile<D, FMT>(ta, qb, qbb, qscale, G, maxpool, n - t * 16, gid, tig, ps, A);
+    t += kWarps;
+    if (t >= tiles) break;
+    if (t + kWarps < tiles) load_tile<D, FMT>(up, lst, (t + kWarps) * 16, gid, tig, ta);
+    compute_tile<D, FMT>(tb, qb, qbb, qscale, G, maxpool, n - t * 16, gid, tig, ps, A);
+    t += kWarps;
+    if (t >= tiles) break;
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads, 3) attend_mma_kernel(TkvState st, const void* __restrict__ qin,
+template <int D, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st, const void* __restrict__ qin,
                                                                   const void* __restrict__ kin,
                                                                   const void* __restrict__ vin,
                                                                   float* __restrict__ out, int buf_half, int nbuf,
@@ -407,7 +481,8 @@ __global__ void __launch_bounds__(kThreads, 3) attend_mma_kernel(TkvState st, co
   float* red = reinterpret_cast<float*>(dyn);                       // [kWarps * 8][2 + D]
   float* ps_all = red + kWarps * 8 * (2 + D);                         // [kWarps][16 * 8]
   uint32_t* qbb_all = reinterpret_cast<uint32_t*>(ps_all + kWarps * 128);  // [32 lanes][D/8] bf16 B frags
-  int2* list = reinterpret_cast<int2*>(qbb_all + 32 * (D / 8));        // [NS + g + 1] (slot, window)
+  int2* list = reinterpret_cast<int2*>(qbb_all + 32 * (D / 8));        // [NS + g + 1 + 4*16] (slot, window)
+  int2* binfo = list + (dm.NS + dm.g + 1 + 4 * 16);                    // [P] (live mask, list position)
   __shared__ int cnt[5], off[5], wsum[kWarps][4];
   const float qscale = dm.scale * kLog2e;
 
@@ -426,8 +501,11 @@ __global__ void __launch_bounds__(kThreads, 3) attend_mma_kernel(TkvState st, co
       qb[j][1] = pack_f16x2(bf16lo(w.y), bf16hi(w.y));
     }
   }
-  // Live-slot list per format with window indices (physical order), then the
-  // raw tail appended to the raw list.
+  // Live-slot lists per format with window indices (physical order), each
+  // padded to a multiple of 16 entries; the raw tail follows the raw list.
+  //   pass 1: thread -> contiguous blocks: live masks + per-format counts;
+  //           block-wide scan -> each block's offset in its format's list
+  //   pass 2: thread -> slots (stride kThreads): coalesced slot->window loads
   const int P = dm.P, bs = dm.bs;
   const int8_t* th = st.blk_thought + (int64_t)u * P;
   const uint8_t* fl = st.blk_filled + (int64_t)u * P;
@@ -437,9 +515,14 @@ __global__ void __launch_bounds__(kThreads, 3) attend_mma_kernel(TkvState st, co
   int c[4] = {0, 0, 0, 0};
   for (int b = b0; b < b1; ++b) {
     const int t = th[b];
-    if (t < 0) continue;
-    const uint32_t live = ~ev[b] & (fl[b] >= 32 ? 0xffffffffu : ((1u << fl[b]) - 1u));
-    c[dm.band_fmt[t]] += __popc(live);
+    uint32_t live = 0;
+    int f = 0;
+    if (t >= 0) {
+      live = ~ev[b] & (fl[b] >= 32 ? 0xffffffffu : ((1u << fl[b]) - 1u));
+      f = dm.band_fmt[t];
+      c[f] += __popc(live);
+    }
+    binfo[b] = make_int2((int)live, f);
   }
   int incl[4];  // warp-inclusive scans
 #pragma unroll
@@ -457,15 +540,13 @@ __global__ void __launch_bounds__(kThreads, 3) attend_mma_kernel(TkvState st, co
   if (threadIdx.x == 0) {
     int run = 0;
     for (int f = 0; f < 4; ++f) {
-      off[f] = run;
       int tot = 0;
       for (int w = 0; w < kWarps; ++w) tot += wsum[w][f];
+      if (f == TKV_FMT_RAW) tot += nbuf + 1;  // tail tokens ride in the raw list
+      off[f] = run;
       cnt[f] = tot;
-      run += tot;
+      run += (tot + 15) & ~15;  // padded to whole tiles
     }
-    cnt[TKV_FMT_RAW] += nbuf + 1;  // tail tokens ride in the raw list
-    off[kFmtTail] = 0;
-    cnt[kFmtTail] = 0;
   }
   __syncthreads();
   {
@@ -476,31 +557,57 @@ __global__ void __launch_bounds__(kThreads, 3) attend_mma_kernel(TkvState st, co
       for (int ww = 0; ww < warp; ++ww) before += wsum[ww][f];
       w[f] = off[f] + before + incl[f] - c[f];
     }
-    const int32_t* swin = st.slot_win + (int64_t)u * dm.NS;
     for (int b = b0; b < b1; ++b) {
-      const int t = th[b];
-      if (t < 0) continue;
-      uint32_t live = ~ev[b] & (fl[b] >= 32 ? 0xffffffffu : ((1u << fl[b]) - 1u));
-      const int f = dm.band_fmt[t];
-      while (live) {
-        const int s = __ffs(live) - 1;
-        live &= live - 1;
-        const int slot = b * bs + s;
-        list[w[f]++] = make_int2(slot, max(0, swin[slot]));
-      }
+      const int2 bi = binfo[b];
+      int pos = 0;
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        if (bi.y == f) { pos = w[f]; w[f] += __popc((uint32_t)bi.x); }
+      binfo[b].y = pos;
     }
     const int rawn = cnt[TKV_FMT_RAW] - (nbuf + 1);
     for (int t = threadIdx.x; t <= nbuf; t += kThreads) list[off[TKV_FMT_RAW] + rawn + t] = make_int2(-1 - t, 0);
   }
   __syncthreads();
-  TailSrc ts;
   {
+    const int32_t* swin = st.slot_win + (int64_t)u * dm.NS;
+    const int NSu = P * bs, qb_ = kThreads / bs, rb_ = kThreads % bs;
+    int b = threadIdx.x / bs, l = threadIdx.x % bs;
+#pragma unroll 6
+    for (int sl = threadIdx.x; sl < NSu; sl += kThreads) {
+      const int2 bi = binfo[b];
+      const uint32_t live = (uint32_t)bi.x;
+      if ((live >> l) & 1u) list[bi.y + __popc(live & ((1u << l) - 1u))] = make_int2(sl, max(0, __ldg(swin + sl)));
+      b += qb_;
+      l += rb_;
+      if (l >= bs) { l -= bs; ++b; }
+    }
+  }
+  __syncthreads();
+  // padding entries: copies of each list's first entry (masked to -inf logits)
+  if (threadIdx.x < 4 * 16) {
+    const int f = threadIdx.x >> 4, i = threadIdx.x & 15;
+    const int n = cnt[f];
+    if (n > 0 && n + i < ((n + 15) & ~15)) list[off[f] + n + i] = list[off[f]];
+  }
+  __syncthreads();
+  UnitPtrs up;
+  {
+    up.kstride = dm.kstride;
+    up.vchunks = dm.vchunks;
+    up.k = st.slot_k + (int64_t)u * dm.NS * dm.kstride;
+    up.v = st.slot_v + (int64_t)u * dm.NS * dm.kstride;
+    up.vs = st.slot_vs + (int64_t)u * dm.NS * dm.vchunks;
+    up.ks = st.win_ks + (int64_t)u * dm.NW * D;
+    up.kf = st.win_kf + (int64_t)u * dm.NW;
+    up.vf = st.win_vf + (int64_t)u * dm.NW;
     const int64_t row = (int64_t)dm.g * D * 2;
-    ts.bk = st.buf + ((int64_t)u * 4 + buf_half * 2 + 0) * row;
-    ts.bv = st.buf + ((int64_t)u * 4 + buf_half * 2 + 1) * row;
-    ts.kc = reinterpret_cast<const uint8_t*>(kin) + (int64_t)u * D * 2;
-    ts.vc = reinterpret_cast<const uint8_t*>(vin) + (int64_t)u * D * 2;
-    ts.nbuf = nbuf;
+    up.bk = st.buf + ((int64_t)u * 4 + buf_half * 2 + 0) * row;
+    up.bv = st.buf + ((int64_t)u * 4 + buf_half * 2 + 1) * row;
+    up.kc = reinterpret_cast<const uint8_t*>(kin) + (int64_t)u * D * 2;
+    up.vc = reinterpret_cast<const uint8_t*>(vin) + (int64_t)u * D * 2;
+    up.nbuf = nbuf;
+    up.vsel = (gid * (D / 8)) / dm.g;
   }
   Acc<D> A;
 #pragma unroll
@@ -515,22 +622,22 @@ __global__ void __launch_bounds__(kThreads, 3) attend_mma_kernel(TkvState st, co
   // Tiles are numbered globally across formats and dealt round-robin.
   int g0 = 0;
   if (cnt[TKV_FMT_NVFP4]) {
-    run_format<D, TKV_FMT_NVFP4>(st, u, list + off[TKV_FMT_NVFP4], cnt[TKV_FMT_NVFP4], g0, warp, qb, qbb, qscale, mp,
-                                 gid, tig, ts, ps, A);
+    run_format<D, TKV_FMT_NVFP4>(up, list + off[TKV_FMT_NVFP4], cnt[TKV_FMT_NVFP4], g0, warp, qb, qbb, qscale, G,
+                                 mp, gid, tig, ps, A);
     g0 += (cnt[TKV_FMT_NVFP4] + 15) / 16;
   }
   if (cnt[TKV_FMT_TERNARY]) {
-    run_format<D, TKV_FMT_TERNARY>(st, u, list + off[TKV_FMT_TERNARY], cnt[TKV_FMT_TERNARY], g0, warp, qb, qbb,
-                                   qscale, mp, gid, tig, ts, ps, A);
+    run_format<D, TKV_FMT_TERNARY>(up, list + off[TKV_FMT_TERNARY], cnt[TKV_FMT_TERNARY], g0, warp, qb, qbb,
+                                   qscale, G, mp, gid, tig, ps, A);
     g0 += (cnt[TKV_FMT_TERNARY] + 15) / 16;
   }
   if (cnt[TKV_FMT_FP8]) {
-    run_format<D, TKV_FMT_FP8>(st, u, list + off[TKV_FMT_FP8], cnt[TKV_FMT_FP8], g0, warp, qb, qbb, qscale, mp, gid,
-                               tig, ts, ps, A);
+    run_format<D, TKV_FMT_FP8>(up, list + off[TKV_FMT_FP8], cnt[TKV_FMT_FP8], g0, warp, qb, qbb, qscale, G, mp,
+                               gid, tig, ps, A);
     g0 += (cnt[TKV_FMT_FP8] + 15) / 16;
   }
-  run_format<D, kFmtTail>(st, u, list + off[TKV_FMT_RAW], cnt[TKV_FMT_RAW], g0, warp, qb, qbb, qscale, mp, gid, tig,
-                          ts, ps, A);
+  run_format<D, kFmtTail>(up, list + off[TKV_FMT_RAW], cnt[TKV_FMT_RAW], g0, warp, qb, qbb, qscale, G, mp, gid,
+                          tig, ps, A);
   // Per-warp partial state -> smem: red[(warp*8 + h)][0]=m, [1]=l, [2+ch]=acc.
   const int stride = 2 + D;
 #pragma unroll
@@ -582,19 +689,28 @@ bool tkv_attend_mma_supported(const TkvDims& dm) {
   return true;
 }
 
+template <int D, int MINB>
+cudaError_t launch_k1(const TkvState& st, const void* q, const void* k, const void* v, float* out, int buf_half,
+                      int nbuf, int put_half, int put_slot, size_t smem, cudaStream_t s) {
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(attend_mma_kernel<D, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cfg = true;
+  }
+  attend_mma_kernel<D, MINB><<<st.dm.U, kThreads, smem, s>>>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot);
+  return cudaGetLastError();
+}
+
 cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void* k, const void* v, float* out,
                                   int buf_half, int nbuf, int put_half, int put_slot, cudaStream_t s) {
   const int D = st.dm.D;
   const size_t smem = (size_t)kWarps * 8 * (2 + D) * 4 + (size_t)kWarps * 128 * 4 + (size_t)32 * (D / 8) * 4 +
-                      (size_t)(st.dm.NS + st.dm.g + 1) * 8;
-  if (D == 128) {
-    static bool cfg = false;
-    if (!cfg) { cudaFuncSetAttribute(attend_mma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
-    attend_mma_kernel<128><<<st.dm.U, kThreads, smem, s>>>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot);
-  } else {
-    static bool cfg = false;
-    if (!cfg) { cudaFuncSetAttribute(attend_mma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
-    attend_mma_kernel<64><<<st.dm.U, kThreads, smem, s>>>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot);
-  }
-  return cudaGetLastError();
+                      (size_t)(st.dm.NS + st.dm.g + 1 + 4 * 16) * 8 + (size_t)st.dm.P * 8;
+  const char* e = getenv("TKV_K1_MINB");
+  const bool four = e && e[0] == '4';
+  if (D == 128)
+    return four ? launch_k1<128, 4>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s)
+                : launch_k1<128, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s);
+  return four ? launch_k1<64, 4>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s)
+              : launch_k1<64, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s);
 }

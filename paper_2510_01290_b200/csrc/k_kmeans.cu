@@ -411,6 +411,86 @@ __device__ void members(SM& s, int m, int K) {
   __syncthreads();
 }
 
+// Parallel member lists (sizes, offs, order ascending within each cluster)
+// from s.assign: match_any ranks inside each 32-point warp, per-warp counts
+// scanned per cluster, offsets scanned by warp 0.  Needs NT >= m; s.cand is
+// the [point-warps][K] count scratch (free outside the swap scan).
+template <int NT, typename SM>
+__device__ void members_par(SM& s, int m, int K) {
+  const int W = (m + 31) / 32;
+  int* wc = s.cand;
+  if (W * K > (int)(sizeof(s.cand) / sizeof(int))) {  // (not reached for tau <= 128)
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < K; ++c) s.sizes[c] = 0;
+      for (int i = 0; i < m; ++i) ++s.sizes[s.assign[i]];
+    }
+    __syncthreads();
+    members(s, m, K);
+    return;
+  }
+  for (int t = threadIdx.x; t < W * K; t += NT) wc[t] = 0;
+  __syncthreads();
+  const int i = threadIdx.x, ln = threadIdx.x & 31;
+  int a = -1, rank = 0;
+  if (i < W * 32) {  // whole warps
+    a = i < m ? s.assign[i] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, a);
+    rank = __popc(peers & ((1u << ln) - 1u));
+    if (i < m && rank == 0) wc[(i >> 5) * K + a] = __popc(peers);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < K; c += NT) {
+    int run = 0;
+    for (int w = 0; w < W; ++w) {
+      const int x = wc[w * K + c];
+      wc[w * K + c] = run;
+      run += x;
+    }
+    s.sizes[c] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int carry = 0;
+    for (int c0 = 0; c0 < K; c0 += 32) {
+      const int c = c0 + ln;
+      const int x = c < K ? s.sizes[c] : 0;
+      int incl = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (ln >= o) incl += y;
+      }
+      if (c < K) s.offs[c] = carry + incl - x;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (ln == 0) s.offs[K] = carry;
+  }
+  __syncthreads();
+  if (i < m) s.order[s.offs[a] + wc[(i >> 5) * K + a] + rank] = i;
+  __syncthreads();
+}
+
+// Lloyd assignment: nearest centroid per point, ties to the lowest index
+// (evictor.cpp:106-117); up to 8 lanes per point scan interleaved columns.
+template <int NT, typename SM>
+__device__ void assign_nearest(SM& s, const double* D2, int m, int K) {
+  int tpp = 1;
+  while (tpp < 8 && tpp * 2 * m <= NT) tpp *= 2;
+  const int i = threadIdx.x / tpp, part = threadIdx.x % tpp;
+  double bd = CUDART_INF;
+  int best = 0x7fffffff;
+  if (i < m) {
+    const double* row = D2 + (int64_t)i * K;
+    for (int c = part; c < K; c += tpp)
+      if (best == 0x7fffffff || row[c] < bd) { bd = row[c]; best = c; }
+  }
+  for (int o = 1; o < tpp; o <<= 1) {
+    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+    const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+    if (od < bd || (od == bd && ob < best)) { bd = od; best = ob; }
+  }
+  if (i < m && part == 0) s.assign[i] = best;
+}
+
 template <int NT, int MAXM>
 __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
                                                         const int32_t* __restrict__ rprefix, int nruns, int run0,
@@ -491,18 +571,11 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     kstm(st, m, 4, 1);
     fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D);
     __syncthreads();
-    for (int i = threadIdx.x; i < m; i += NT) {
-      const double* row = D2 + (int64_t)i * K;
-      int best = 0;
-      double bd = row[0];
-      for (int c = 1; c < K; ++c)
-        if (row[c] < bd) { bd = row[c]; best = c; }
-      s.assign[i] = best;
-    }
+    assign_nearest<NT>(s, D2, m, K);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int c = 0; c < K; ++c) s.sizes[c] = 0;
-      for (int i = 0; i < m; ++i) ++s.sizes[s.assign[i]];
+    members_par<NT>(s, m, K);
+    if (__syncthreads_or(threadIdx.x < K && s.sizes[threadIdx.x] == 0)) {
+      if (threadIdx.x == 0) {
       for (int c = 0; c < K; ++c) {  // empty-cluster repair (evictor.cpp:123-141)
         if (s.sizes[c] > 0) continue;
         int donor = 0;
@@ -519,9 +592,10 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
         --s.sizes[donor];
         ++s.sizes[c];
       }
+      }
+      __syncthreads();
+      members_par<NT>(s, m, K);
     }
-    __syncthreads();
-    members(s, m, K);
     for (int idx = threadIdx.x; idx < K * D; idx += NT) {
       const int c = idx / D, ch = idx % D;
       double acc = 0.0;
@@ -553,12 +627,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   const long long t1 = clock64();
   kstm(st, m, 5, (unsigned long long)(t1 - t0));
   // ---- Hartigan (evictor.cpp:167-243) --------------------------------------
-  if (threadIdx.x == 0) {
-    for (int c = 0; c < K; ++c) s.sizes[c] = 0;
-    for (int i = 0; i < m; ++i) ++s.sizes[s.assign[i]];
-  }
-  __syncthreads();
-  members(s, m, K);
+  members_par<NT>(s, m, K);
   for (int idx = threadIdx.x; idx < K * D; idx += NT) {
     const int c = idx / D, ch = idx % D;
     double acc = 0.0;
@@ -608,13 +677,15 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
         if (lane == 0) s.res[warp] = mto;
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int mi = -1, mt = -1;
-        for (int w = 0; w < NT / 32 && start + w < m; ++w)
-          if (s.res[w] >= 0) { mi = start + w; mt = s.res[w]; break; }
-        s.move_i = mi;
-        s.move_to = mt;
-        s.flag = mi >= 0 ? mi + 1 : start + NT / 32;
+      if (warp == 0) {  // first warp (point order) holding an improving move
+        const int r = (lane < NT / 32 && start + lane < m) ? s.res[lane] : -1;
+        const unsigned any = __ballot_sync(0xffffffffu, r >= 0);
+        if (lane == 0) {
+          const int fw = any ? __ffs(any) - 1 : -1;
+          s.move_i = fw >= 0 ? start + fw : -1;
+          s.move_to = fw >= 0 ? s.res[fw] : -1;
+          s.flag = fw >= 0 ? start + fw + 1 : start + NT / 32;
+        }
       }
       __syncthreads();
       const int i = s.move_i, to = s.move_to;
@@ -899,7 +970,7 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
     if (mmax <= 16) e = go(km_restart_kernel<32, 16>, 32);
     else if (mmax <= 32) e = go(km_restart_kernel<64, 32>, 64);
     else if (mmax <= 64) e = go(km_restart_kernel<128, 64>, 128);
-    else e = go(km_restart_kernel<256, kMaxM>, 256);
+    else e = go(km_restart_kernel<512, kMaxM>, 512);
     if (e != cudaSuccess) return e;
     e = cudaGetLastError();
     if (e != cudaSuccess) {
