@@ -197,7 +197,9 @@ struct UnitPtrs {
   const uint8_t* bv;
   const uint8_t* kc;  // incoming token
   const uint8_t* vc;
+  const int32_t* win; // slot -> window (v3)
   int kstride, vchunks, nbuf, vsel;  // vsel: value-chunk index of this thread
+  int NS;             // v3: list entries >= NS are tail rows (NS + t)
 };
 
 // List entries: (slot, window).  Tail entries are (-1 - t, 0): t < nbuf is
@@ -503,9 +505,9 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st,
   }
   // Live-slot lists per format with window indices (physical order), each
   // padded to a multiple of 16 entries; the raw tail follows the raw list.
-  //   pass 1: thread -> contiguous blocks: live masks + per-format counts;
-  //           block-wide scan -> each block's offset in its format's list
-  //   pass 2: thread -> slots (stride kThreads): coalesced slot->window loads
+  //   pass 1: thread -> contiguous blocks: live masks + per-format counts
+  //   scan:   per-format offsets of each thread's first block
+  //   pass 2: each thread writes its blocks' live slots (with their windows)
   const int P = dm.P, bs = dm.bs;
   const int8_t* th = st.blk_thought + (int64_t)u * P;
   const uint8_t* fl = st.blk_filled + (int64_t)u * P;
@@ -557,31 +559,22 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st,
       for (int ww = 0; ww < warp; ++ww) before += wsum[ww][f];
       w[f] = off[f] + before + incl[f] - c[f];
     }
+    const int32_t* swin = st.slot_win + (int64_t)u * dm.NS;
     for (int b = b0; b < b1; ++b) {
       const int2 bi = binfo[b];
+      uint32_t live = (uint32_t)bi.x;
       int pos = 0;
 #pragma unroll
       for (int f = 0; f < 4; ++f)
-        if (bi.y == f) { pos = w[f]; w[f] += __popc((uint32_t)bi.x); }
-      binfo[b].y = pos;
+        if (bi.y == f) { pos = w[f]; w[f] += __popc(live); }
+      while (live) {
+        const int sl = __ffs(live) - 1;
+        live &= live - 1;
+        list[pos++] = make_int2(b * bs + sl, max(0, __ldg(swin + b * bs + sl)));
+      }
     }
     const int rawn = cnt[TKV_FMT_RAW] - (nbuf + 1);
     for (int t = threadIdx.x; t <= nbuf; t += kThreads) list[off[TKV_FMT_RAW] + rawn + t] = make_int2(-1 - t, 0);
-  }
-  __syncthreads();
-  {
-    const int32_t* swin = st.slot_win + (int64_t)u * dm.NS;
-    const int NSu = P * bs, qb_ = kThreads / bs, rb_ = kThreads % bs;
-    int b = threadIdx.x / bs, l = threadIdx.x % bs;
-#pragma unroll 6
-    for (int sl = threadIdx.x; sl < NSu; sl += kThreads) {
-      const int2 bi = binfo[b];
-      const uint32_t live = (uint32_t)bi.x;
-      if ((live >> l) & 1u) list[bi.y + __popc(live & ((1u << l) - 1u))] = make_int2(sl, max(0, __ldg(swin + sl)));
-      b += qb_;
-      l += rb_;
-      if (l >= bs) { l -= bs; ++b; }
-    }
   }
   __syncthreads();
   // padding entries: copies of each list's first entry (masked to -inf logits)
@@ -680,6 +673,268 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st,
   }
 }
 
+
+// ===========================================================================
+// v3: one warp per unit.  No block-level barriers: the warp builds its own
+// live list (u16 slot ids; tail rows are NS + t), walks every tile of its
+// unit, and writes the normalised output itself.  Window indices are not in
+// the list: they are fetched two tiles ahead (slot -> window), so the scale
+// loads of tile t+1 are issued while tile t computes.
+// ===========================================================================
+template <int D, int FMT>
+__device__ __forceinline__ void load_wins3(const UnitPtrs& up, const uint16_t* lst, int t0, int gid, int tig,
+                                           int (&wk)[2], int (&wv)[4]) {
+  if constexpr (Geo<D, FMT>::SCALED || FMT == TKV_FMT_FP8) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) wk[r] = __ldg(up.win + lst[t0 + gid + 8 * r]);  // live quantised slots: >= 0
+  }
+  if constexpr (FMT == TKV_FMT_FP8) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) wv[i] = __ldg(up.win + lst[t0 + tig * 2 + (i & 1) + 8 * (i >> 1)]);
+  }
+}
+
+template <int D, int FMT>
+__device__ __forceinline__ void load_tile3(const UnitPtrs& up, const uint16_t* lst, int t0, int gid, int tig,
+                                           const int (&wk)[2], const int (&wv)[4], Tile<D, FMT>& T) {
+  using Gm = Geo<D, FMT>;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int e = lst[t0 + gid + 8 * r];
+    const uint8_t* kr;
+    if constexpr (FMT == kFmtTail) {
+      if (e < up.NS) kr = up.k + e * up.kstride;
+      else kr = e - up.NS < up.nbuf ? up.bk + (e - up.NS) * (D * 2) : up.kc;
+    } else {
+      kr = up.k + e * up.kstride;
+    }
+    T.k[r] = ldg_words<Gm::KW>(kr + tig * Gm::KBYTES);
+    if constexpr (FMT == TKV_FMT_FP8) T.kf[r] = __ldg(up.kf + wk[r]);
+    if constexpr (Gm::SCALED) T.ks[r] = ldg_words<Gm::SW>(up.ks + wk[r] * D + tig * Gm::CPT);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = lst[t0 + tig * 2 + (i & 1) + 8 * (i >> 1)];
+    const uint8_t* vr;
+    if constexpr (FMT == kFmtTail) {
+      if (e < up.NS) vr = up.v + e * up.kstride;
+      else vr = e - up.NS < up.nbuf ? up.bv + (e - up.NS) * (D * 2) : up.vc;
+    } else {
+      vr = up.v + e * up.kstride;
+    }
+    vr += gid * Gm::VBYTES;
+    if constexpr (Gm::VBYTES >= 4) {
+      T.v[i] = ldg_words<Gm::VW>(vr);
+    } else {
+      T.v[i].w[0] = Gm::VBYTES == 2 ? (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(vr)) : (uint32_t)__ldg(vr);
+    }
+    if constexpr (FMT == TKV_FMT_FP8) T.vf[i] = __ldg(up.vf + wv[i]);
+    if constexpr (Gm::SCALED) T.vs[i] = __ldg(up.vs + e * up.vchunks + up.vsel);
+  }
+}
+
+template <int D, int FMT>
+__device__ __forceinline__ void run_format3(const UnitPtrs& up, const uint16_t* lst, int n,
+                                            const uint32_t (&qb)[D / 16][2], const uint32_t* qbb, float qscale,
+                                            int G, bool maxpool, int gid, int tig, float* ps, Acc<D>& A) {
+  const int tiles = (n + 15) / 16;
+  if (tiles == 0) return;
+  if constexpr (FMT == kFmtTail) {  // few tiles, wide rows: no double buffering (registers)
+    int wk[2] = {0, 0}, wv[4] = {0, 0, 0, 0};
+    for (int t = 0; t < tiles; ++t) {
+      Tile<D, FMT> cur;
+      load_tile3<D, FMT>(up, lst, t * 16, gid, tig, wk, wv, cur);
+      compute_tile<D, FMT>(cur, qb, qbb, qscale, G, maxpool, n - t * 16, gid, tig, ps, A);
+    }
+    return;
+  }
+  int wk0[2] = {0, 0}, wv0[4] = {0, 0, 0, 0}, wk1[2] = {0, 0}, wv1[4] = {0, 0, 0, 0};
+  Tile<D, FMT> ta, tb;
+  load_wins3<D, FMT>(up, lst, 0, gid, tig, wk0, wv0);
+  load_tile3<D, FMT>(up, lst, 0, gid, tig, wk0, wv0, ta);
+  if (tiles > 1) load_wins3<D, FMT>(up, lst, 16, gid, tig, wk1, wv1);
+  int t = 0;
+  while (true) {
+    // ta holds tile t; wk1 the windows of tile t + 1
+    if (t + 1 < tiles) {
+      load_tile3<D, FMT>(up, lst, (t + 1) * 16, gid, tig, wk1, wv1, tb);
+      if (t + 2 < tiles) load_wins3<D, FMT>(up, lst, (t + 2) * 16, gid, tig, wk0, wv0);
+    }
+    compute_tile<D, FMT>(ta, qb, qbb, qscale, G, maxpool, n - t * 16, gid, tig, ps, A);
+    if (++t >= tiles) break;
+    // tb holds tile t; wk0 the windows of tile t + 1
+    if (t + 1 < tiles) {
+      load_tile3<D, FMT>(up, lst, (t + 1) * 16, gid, tig, wk0, wv0, ta);
+      if (t + 2 < tiles) load_wins3<D, FMT>(up, lst, (t + 2) * 16, gid, tig, wk1, wv1);
+    }
+    compute_tile<D, FMT>(tb, qb, qbb, qscale, G, maxpool, n - t * 16, gid, tig, ps, A);
+    if (++t >= tiles) break;
+  }
+}
+
+// Per-warp shared memory of the v3 kernel.
+template <int D>
+struct WarpSmem {
+  static constexpr int kQbb = 32 * (D / 8);  // u32: bf16 q fragments
+  static __host__ __device__ size_t bytes(int NS, int g, int P) {
+    const size_t lst = ((size_t)(NS + g + 1 + 4 * 16) * 2 + 15) / 16 * 16;
+    return (size_t)kQbb * 4 + 128 * 4 + (size_t)P * 8 + lst;
+  }
+};
+
+template <int D, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st, const void* __restrict__ qin,
+                                                                    const void* __restrict__ kin,
+                                                                    const void* __restrict__ vin,
+                                                                    float* __restrict__ out, int buf_half, int nbuf,
+                                                                    int put_half, int put_slot) {
+  const TkvDims& dm = st.dm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u = blockIdx.x * kWarps + warp;
+  if (u >= dm.U) return;
+  const int G = dm.G, R = dm.maxpool ? 1 : G;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int P = dm.P, bs = dm.bs, NS = dm.NS;
+  extern __shared__ __align__(16) uint8_t dyn[];
+  uint8_t* mine = dyn + (size_t)warp * WarpSmem<D>::bytes(NS, dm.g, P);
+  uint32_t* qbb = reinterpret_cast<uint32_t*>(mine) + lane * (D / 8);
+  float* ps = reinterpret_cast<float*>(mine + WarpSmem<D>::kQbb * 4);
+  int2* binfo = reinterpret_cast<int2*>(mine + WarpSmem<D>::kQbb * 4 + 128 * 4);
+  uint16_t* list = reinterpret_cast<uint16_t*>(binfo + P);
+  const float qscale = dm.scale * kLog2e;
+
+  uint32_t qb[D / 16][2];
+  {
+    const uint16_t* qq = reinterpret_cast<const uint16_t*>(qin) + ((int64_t)u * G + gid) * D + tig * (D / 4);
+#pragma unroll
+    for (int j = 0; j < D / 16; ++j) {
+      uint2 w = make_uint2(0u, 0u);
+      if (gid < G) w = *reinterpret_cast<const uint2*>(qq + 4 * j);
+      qbb[2 * j] = w.x;
+      qbb[2 * j + 1] = w.y;
+      qb[j][0] = pack_f16x2(bf16lo(w.x), bf16hi(w.x));
+      qb[j][1] = pack_f16x2(bf16lo(w.y), bf16hi(w.y));
+    }
+  }
+  // ---- live lists: lane -> contiguous blocks ----------------------------------
+  const int8_t* th = st.blk_thought + (int64_t)u * P;
+  const uint8_t* fl = st.blk_filled + (int64_t)u * P;
+  const uint32_t* ev = st.blk_evict + (int64_t)u * P;
+  const int per = (P + 31) / 32;
+  const int b0 = lane * per, b1 = min(P, b0 + per);
+  int c[4] = {0, 0, 0, 0};
+#pragma unroll 4
+  for (int b = b0; b < b1; ++b) {
+    const int t = th[b];
+    const int f = t >= 0 ? dm.band_fmt[t] : 0;
+    const uint32_t live = t >= 0 ? ~ev[b] & (fl[b] >= 32 ? 0xffffffffu : ((1u << fl[b]) - 1u)) : 0u;
+#pragma unroll
+    for (int ff = 0; ff < 4; ++ff) c[ff] += ff == f ? __popc(live) : 0;
+    binfo[b] = make_int2((int)live, f);
+  }
+  int w[4], cnt[4], off[4];
+  {
+    int run = 0;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      int x = c[f];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int tot = __shfl_sync(0xffffffffu, x, 31);
+      if (f == TKV_FMT_RAW) tot += nbuf + 1;  // tail rows ride in the raw list
+      off[f] = run;
+      cnt[f] = tot;
+      w[f] = run + x - c[f];
+      run += (tot + 15) & ~15;  // padded to whole tiles
+    }
+  }
+  for (int b = b0; b < b1; ++b) {
+    const int2 bi = binfo[b];
+    uint32_t live = (uint32_t)bi.x;
+    int pos = 0;
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+      if (bi.y == f) { pos = w[f]; w[f] += __popc(live); }
+    while (live) {
+      const int sl = __ffs(live) - 1;
+      live &= live - 1;
+      list[pos++] = (uint16_t)(b * bs + sl);
+    }
+  }
+  {
+    const int rawn = cnt[TKV_FMT_RAW] - (nbuf + 1);
+    for (int t = lane; t <= nbuf; t += 32) list[off[TKV_FMT_RAW] + rawn + t] = (uint16_t)(NS + t);
+  }
+  __syncwarp();
+  // padding entries: copies of each list's first entry (masked to -inf logits)
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int n = cnt[f];
+    if (lane < 16 && n > 0 && n + lane < ((n + 15) & ~15)) list[off[f] + n + lane] = list[off[f]];
+  }
+  __syncwarp();
+  UnitPtrs up;
+  up.kstride = dm.kstride;
+  up.vchunks = dm.vchunks;
+  up.NS = NS;
+  up.k = st.slot_k + (int64_t)u * NS * dm.kstride;
+  up.v = st.slot_v + (int64_t)u * NS * dm.kstride;
+  up.vs = st.slot_vs + (int64_t)u * NS * dm.vchunks;
+  up.win = st.slot_win + (int64_t)u * NS;
+  up.ks = st.win_ks + (int64_t)u * dm.NW * D;
+  up.kf = st.win_kf + (int64_t)u * dm.NW;
+  up.vf = st.win_vf + (int64_t)u * dm.NW;
+  {
+    const int64_t row = (int64_t)dm.g * D * 2;
+    up.bk = st.buf + ((int64_t)u * 4 + buf_half * 2 + 0) * row;
+    up.bv = st.buf + ((int64_t)u * 4 + buf_half * 2 + 1) * row;
+  }
+  up.kc = reinterpret_cast<const uint8_t*>(kin) + (int64_t)u * D * 2;
+  up.vc = reinterpret_cast<const uint8_t*>(vin) + (int64_t)u * D * 2;
+  up.nbuf = nbuf;
+  up.vsel = (gid * (D / 8)) / dm.g;
+  Acc<D> A;
+#pragma unroll
+  for (int mt = 0; mt < D / 16; ++mt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) A.o[mt][i] = 0.f;
+  A.m[0] = A.m[1] = -CUDART_INF_F;
+  A.l[0] = A.l[1] = 0.f;
+  const bool mp = dm.maxpool != 0;
+  run_format3<D, TKV_FMT_NVFP4>(up, list + off[TKV_FMT_NVFP4], cnt[TKV_FMT_NVFP4], qb, qbb, qscale, G, mp, gid, tig,
+                                ps, A);
+  run_format3<D, TKV_FMT_TERNARY>(up, list + off[TKV_FMT_TERNARY], cnt[TKV_FMT_TERNARY], qb, qbb, qscale, G, mp, gid,
+                                  tig, ps, A);
+  run_format3<D, TKV_FMT_FP8>(up, list + off[TKV_FMT_FP8], cnt[TKV_FMT_FP8], qb, qbb, qscale, G, mp, gid, tig, ps,
+                              A);
+  run_format3<D, kFmtTail>(up, list + off[TKV_FMT_RAW], cnt[TKV_FMT_RAW], qb, qbb, qscale, G, mp, gid, tig, ps, A);
+  // ---- epilogue: heads tig*2 + cc, channels gid*D/8 + 2mt (+1) ------------------
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    const int h = tig * 2 + cc;
+    if (h >= R) continue;
+    const float inv = 1.0f / A.l[cc];
+    float* o = out + ((int64_t)u * R + h) * D + gid * (D / 8);
+#pragma unroll
+    for (int mt = 0; mt < D / 16; ++mt)
+      *reinterpret_cast<float2*>(o + 2 * mt) = make_float2(A.o[mt][cc] * inv, A.o[mt][2 + cc] * inv);
+  }
+  if (put_slot >= 0) {  // buffer the incoming token (sim.cpp:796-808)
+    const int64_t row = (int64_t)dm.g * D;
+    uint16_t* bk = reinterpret_cast<uint16_t*>(st.buf) + ((int64_t)u * 4 + put_half * 2 + 0) * row + (int64_t)put_slot * D;
+    uint16_t* bv = reinterpret_cast<uint16_t*>(st.buf) + ((int64_t)u * 4 + put_half * 2 + 1) * row + (int64_t)put_slot * D;
+    const uint16_t* ks = reinterpret_cast<const uint16_t*>(kin) + (int64_t)u * D;
+    const uint16_t* vs = reinterpret_cast<const uint16_t*>(vin) + (int64_t)u * D;
+    for (int i = lane; i < D; i += 32) {
+      bk[i] = ks[i];
+      bv[i] = vs[i];
+    }
+  }
+}
+
 }  // namespace
 
 bool tkv_attend_mma_supported(const TkvDims& dm) {
@@ -701,16 +956,35 @@ cudaError_t launch_k1(const TkvState& st, const void* q, const void* k, const vo
   return cudaGetLastError();
 }
 
+template <int D, int MINB>
+cudaError_t launch_k1_warp(const TkvState& st, const void* q, const void* k, const void* v, float* out, int buf_half,
+                           int nbuf, int put_half, int put_slot, cudaStream_t s) {
+  const size_t smem = (size_t)kWarps * WarpSmem<D>::bytes(st.dm.NS, st.dm.g, st.dm.P);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(attend_warp_kernel<D, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cfg = true;
+  }
+  attend_warp_kernel<D, MINB><<<(st.dm.U + kWarps - 1) / kWarps, kThreads, smem, s>>>(st, q, k, v, out, buf_half,
+                                                                                     nbuf, put_half, put_slot);
+  return cudaGetLastError();
+}
+
 cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void* k, const void* v, float* out,
                                   int buf_half, int nbuf, int put_half, int put_slot, cudaStream_t s) {
   const int D = st.dm.D;
+  // v3 (warp per unit, u16 slot lists) whenever slot ids fit in 16 bits and
+  // the per-warp lists fit in shared memory; v2 (CTA per unit) otherwise.
+  const bool v3 = st.dm.NS + st.dm.g + 1 + 4 * 16 < 65536 &&
+                  (size_t)kWarps * (D == 128 ? WarpSmem<128>::bytes(st.dm.NS, st.dm.g, st.dm.P)
+                                             : WarpSmem<64>::bytes(st.dm.NS, st.dm.g, st.dm.P)) <= 200 * 1024 &&
+                  getenv("TKV_K1_V2") == nullptr;
+  if (v3) {
+    if (D == 128) return launch_k1_warp<128, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+    return launch_k1_warp<64, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+  }
   const size_t smem = (size_t)kWarps * 8 * (2 + D) * 4 + (size_t)kWarps * 128 * 4 + (size_t)32 * (D / 8) * 4 +
                       (size_t)(st.dm.NS + st.dm.g + 1 + 4 * 16) * 8 + (size_t)st.dm.P * 8;
-  const char* e = getenv("TKV_K1_MINB");
-  const bool four = e && e[0] == '4';
-  if (D == 128)
-    return four ? launch_k1<128, 4>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s)
-                : launch_k1<128, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s);
-  return four ? launch_k1<64, 4>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s)
-              : launch_k1<64, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s);
+  if (D == 128) return launch_k1<128, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s);
+  return launch_k1<64, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, smem, s);
 }

@@ -6,7 +6,7 @@ import torch
 from paper_2510_01290_b200 import DecodeRun, ThinkvConfig
 from paper_2510_01290_b200.synth import band_script
 ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 2600
-variants = sys.argv[2].split(',') if len(sys.argv) > 2 else ['3', '4']
+variants = sys.argv[2].split(',') if len(sys.argv) > 2 else ['v2', 'v3']
 script = band_script(0x71534B56, 32, 300, 3, 100)
 cfg = ThinkvConfig(num_seqs=32, units_per_seq=256, num_q_heads=4, head_dim=128, tau=128, group_size=16,
                    block_size=16, budget=1024, levels=(64, 32, 16, 8, 4), psi_bits=(4, 4, 2),
@@ -27,7 +27,8 @@ print(f"ctx {ctx} built in {time.time() - t0:.1f}s; bytes {run.bytes()['algorith
 pos = ctx
 for rep in range(3):
     for var in variants:
-        os.environ['TKV_K1_MINB'] = var
+        if var == 'v2': os.environ['TKV_K1_V2'] = '1'
+        else: os.environ.pop('TKV_K1_V2', None)
         run.timing_enable(True)
         for i in range(20):
             if (pos + 1) % 128 == 0 or pos % 128 == 0:  # keep refresh/eviction steps out of the window

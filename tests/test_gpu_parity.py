@@ -157,3 +157,12 @@ def test_host_buffer_steps_match_device_steps():
     for s in range(2):
         assert b.tables(s) == a.tables(s) and c.tables(s) == a.tables(s)
         assert b.events(s) == a.events(s)
+
+
+def test_parity_cta_per_unit_attention_variant(monkeypatch):
+    """The CTA-per-unit K1 variant (used when slot ids exceed 16 bits) stays
+    parity-green: forced here through TKV_K1_V2 on a small configuration."""
+    monkeypatch.setenv("TKV_K1_V2", "1")
+    cfg = CONFIGS["llama_shape"]
+    res = run_parity(cfg, check_every=3)
+    compare_state(res, cfg)
