@@ -27,6 +27,7 @@
 //            earlier one, evictor.cpp:319-325) supplies the retained set.
 // The file is compiled with --fmad=false and every order-sensitive value uses
 // explicit _rn intrinsics.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -80,8 +81,14 @@ __device__ __forceinline__ double div_n(double x, int n) {
   return __ddiv_rn(x, (double)n);
 }
 
-__device__ __forceinline__ double xval(const float* X, const double* xs, int i, int ch, int xstride, bool scaled) {
-  const double v = (double)X[(int64_t)i * xstride + ch];
+__device__ __forceinline__ double xget(const float* X, int64_t k) { return (double)X[k]; }
+__device__ __forceinline__ double xget(const __half* X, int64_t k) { return (double)__half2float(X[k]); }
+// Decoded key channel: f32 store, or f16 when every band is a quantised
+// format (code x E4M3 scale <= 8 significant bits in [2^-10, 2688], FP8 codes
+// in [2^-9, 448]: exact in f16).
+template <typename XT>
+__device__ __forceinline__ double xval(const XT* X, const double* xs, int i, int ch, int xstride, bool scaled) {
+  const double v = xget(X, (int64_t)i * xstride + ch);
   return scaled ? __dmul_rn(v, xs[i]) : v;
 }
 
@@ -305,8 +312,8 @@ constexpr int kColCompute = -1;  // recompute the column from the centroid
 // the same order (t = x_i - x_p, channel-sequential sum) -- so its column is
 // copied from the prep kernel's pairwise matrix; unchanged centroids keep
 // their column; only the rest are evaluated.
-template <int NT, typename SM>
-__device__ void fill_sel(SM& s, const float* X, int XS, const double* xs, bool scaled, const double* C, int cstride,
+template <int NT, typename SM, typename XT>
+__device__ void fill_sel(SM& s, const XT* X, int XS, const double* xs, bool scaled, const double* C, int cstride,
                          double* D2, const double* __restrict__ pd, int pstride, int m, int K, int D) {
   if (threadIdx.x < 32) {
     int base = 0;
@@ -382,8 +389,8 @@ __device__ void fill_sel(SM& s, const float* X, int XS, const double* xs, bool s
 }
 
 // Recompute D2 columns a and b (after a move or swap changed those means).
-template <int NT>
-__device__ void refresh_cols(const float* X, int XS, const double* xs, bool scaled, const double* C, int cstride,
+template <int NT, typename XT>
+__device__ void refresh_cols(const XT* X, int XS, const double* xs, bool scaled, const double* C, int cstride,
                              double* D2, int m, int K, int D, int a, int b) {
   for (int t = threadIdx.x; t < 2 * m; t += NT) {
     const int i = t >> 1, c = (t & 1) ? b : a;
@@ -491,7 +498,7 @@ __device__ void assign_nearest(SM& s, const double* D2, int m, int K) {
   if (i < m && part == 0) s.assign[i] = best;
 }
 
-template <int NT, int MAXM>
+template <int NT, int MAXM, typename XT>
 __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
                                                         const int32_t* __restrict__ rprefix, int nruns, int run0,
                                                         const int32_t* __restrict__ item_prefix, int item0,
@@ -516,18 +523,18 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   extern __shared__ __align__(16) uint8_t dyn[];
   __shared__ RsSmem<MAXM> s;
   double* xs = s.xs;
-  // smem: X f32 [m][D+1] | means f64 [K][D+1] | D2 f64 [m][K]  (rows padded
-  // by one element so column-wise accesses across lanes are conflict-free)
-  const int XS = D + 1, MS = D + 1;
-  float* X = reinterpret_cast<float*>(dyn);
-  double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)geo.mmax * XS * 4 + 15) / 16 * 16));
+  // smem: X f32/f16 [m][XS] | means f64 [K][D+1] | D2 f64 [m][K]  (rows
+  // padded by one word so column-wise accesses across lanes are conflict-free)
+  const int XS = D + 4 / (int)sizeof(XT), MS = D + 1;
+  XT* X = reinterpret_cast<XT*>(dyn);
+  double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)geo.mmax * XS * sizeof(XT) + 15) / 16 * 16));
   double* D2 = Mn + (int64_t)geo.kmax * MS;
   // sums / next: shared memory for small instances, else a global row block per CTA
   double* S = MAXM <= 32 ? D2 + (int64_t)geo.mmax * geo.kmax : gsums + (int64_t)blockIdx.x * geo.kmax * D;
   const float* gX = reinterpret_cast<const float*>(base + geo.x_off());
   const double* gxs = reinterpret_cast<const double*>(base + geo.xs_off());
   const double* pd = reinterpret_cast<const double*>(base + geo.pd_off());
-  for (int i = threadIdx.x; i < m * D; i += NT) X[(i / D) * XS + i % D] = gX[i];
+  for (int i = threadIdx.x; i < m * D; i += NT) X[(i / D) * XS + i % D] = (XT)gX[i];
   for (int i = threadIdx.x; i < m; i += NT) xs[i] = gxs[i];
   for (int n = threadIdx.x; n <= MAXM; n += NT) {
     const double dn = (double)n;
@@ -925,14 +932,15 @@ int64_t tkv_km_instance_bytes(int mmax, int kmax, int D, int W, int R) {
   return g.bytes();
 }
 
-size_t tkv_km_restart_smem(int mmax, int kmax, int D) {
-  return (size_t)(((int64_t)mmax * (D + 1) * 4 + 15) / 16 * 16) + (size_t)kmax * (D + 1) * 8 + (size_t)mmax * kmax * 8;
+size_t tkv_km_restart_smem(int mmax, int kmax, int D, int xbytes) {
+  return (size_t)(((int64_t)mmax * (D + 4 / xbytes) * xbytes + 15) / 16 * 16) + (size_t)kmax * (D + 1) * 8 +
+         (size_t)mmax * kmax * 8;
 }
 
 cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int nops, const int32_t* item_prefix,
                               int nitems, const int32_t* run_prefix, int nruns, int item0, int item_count,
                               int run0, int run_count, int mmax, int kmax, int R, uint8_t* scratch, double* gsums,
-                              int gsums_ctas, uint32_t* log, int scaled_any, cudaStream_t stream) {
+                              int gsums_ctas, uint32_t* log, int scaled_any, int x16, cudaStream_t stream) {
   KmGeo geo{mmax, kmax, st.dm.D, st.dm.W, R};
   const size_t psmem = (size_t)mmax * (st.dm.D + 1) * 4;
   if (psmem > 160 * 1024) return cudaErrorInvalidConfiguration;
@@ -947,7 +955,7 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
     fprintf(stderr, "[kmeans] prep launch failed: items=%d: %s\n", item_count, cudaGetErrorString(e));
     return e;
   }
-  const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D);
+  const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D, x16 ? 2 : 4);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // tau x d beyond the smem design point
   // runs are processed in chunks of gsums_ctas CTAs (one global sums buffer each)
   // Small classes keep their sums in shared memory: one launch for all runs.
@@ -967,10 +975,17 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
                                     scratch, geo, gsums, scaled_any);
       return cudaSuccess;
     };
-    if (mmax <= 16) e = go(km_restart_kernel<32, 16>, 32);
-    else if (mmax <= 32) e = go(km_restart_kernel<64, 32>, 64);
-    else if (mmax <= 64) e = go(km_restart_kernel<128, 64>, 128);
-    else e = go(km_restart_kernel<512, kMaxM>, 512);
+    if (x16) {
+      if (mmax <= 16) e = go(km_restart_kernel<32, 16, __half>, 32);
+      else if (mmax <= 32) e = go(km_restart_kernel<64, 32, __half>, 64);
+      else if (mmax <= 64) e = go(km_restart_kernel<128, 64, __half>, 128);
+      else e = go(km_restart_kernel<512, kMaxM, __half>, 512);
+    } else {
+      if (mmax <= 16) e = go(km_restart_kernel<32, 16, float>, 32);
+      else if (mmax <= 32) e = go(km_restart_kernel<64, 32, float>, 64);
+      else if (mmax <= 64) e = go(km_restart_kernel<128, 64, float>, 128);
+      else e = go(km_restart_kernel<512, kMaxM, float>, 512);
+    }
     if (e != cudaSuccess) return e;
     e = cudaGetLastError();
     if (e != cudaSuccess) {

@@ -197,7 +197,8 @@ struct tkv_run {
   void* d_k[2] = {nullptr, nullptr};
   void* d_v[2] = {nullptr, nullptr};
   float* d_out[2] = {nullptr, nullptr};
-  cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // uploads
+  cudaStream_t d2h_stream = nullptr;   // downloads (separate, so step t's download never delays step t+1's upload)
   cudaEvent_t h2d_done[2]{}, step_done[2]{}, d2h_done[2]{};
   int hslot = 0;
   std::vector<void*> allocations;
@@ -440,18 +441,20 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
     }
   }
   const TkvDims& dm = r->st.dm;
-  bool f64_raw = false, fp8 = false;
+  bool f64_raw = false, fp8 = false, raw = false;
   for (int b = 0; b < dm.num_bands; ++b) {
     f64_raw = f64_raw || (dm.band_fmt[b] == TKV_FMT_RAW && dm.in_dtype == TKV_IN_F64);
     fp8 = fp8 || dm.band_fmt[b] == TKV_FMT_FP8;
+    raw = raw || dm.band_fmt[b] == TKV_FMT_RAW;
   }
   // Ops of one wave are independent; split each wave by instance-size class
   // so small instances get the small (high-occupancy) restart variant
   // instead of inheriting the shared-memory footprint of the largest op.
   std::vector<std::vector<TkvAnnealOp>> subwaves;
   for (auto& wv : waves) {
-    std::vector<TkvAnnealOp> cls[4];
-    for (const TkvAnnealOp& op : wv) cls[op.m <= 16 ? 0 : op.m <= 32 ? 1 : op.m <= 64 ? 2 : 3].push_back(op);
+    std::vector<TkvAnnealOp> cls[5];
+    for (const TkvAnnealOp& op : wv)
+      cls[op.m <= 8 ? 0 : op.m <= 16 ? 1 : op.m <= 32 ? 2 : op.m <= 64 ? 3 : 4].push_back(op);
     for (auto& c : cls)
       if (!c.empty()) subwaves.push_back(std::move(c));
   }
@@ -502,7 +505,7 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
       launch(r, CAT_ANNEAL, "kmeans kernels", [&] {
         return tkv_launch_kmeans(r->st, d_ops, (int)wv.size(), d_pre, items, d_rpre, runs, i0, cnt, run0,
                                  run1 - run0, mmax, kmax, R, r->km_scratch, r->km_sums, r->km_sums_ctas, r->d_log,
-                                 fp8 ? 1 : 0, r->stream);
+                                 fp8 ? 1 : 0, raw ? 0 : 1, r->stream);
       });
     }
   }
@@ -811,6 +814,7 @@ json tables_json(const tkv_run* r, const std::vector<UnitSnap>& snaps) {
 void check_device_errors(tkv_run* r) {
   CUDA_OK(cudaStreamSynchronize(r->stream));
   if (r->copy_stream) CUDA_OK(cudaStreamSynchronize(r->copy_stream));
+  if (r->d2h_stream) CUDA_OK(cudaStreamSynchronize(r->d2h_stream));
   std::vector<int32_t> err(r->st.dm.U);
   CUDA_OK(cudaMemcpy(err.data(), r->st.err, err.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
   for (size_t u = 0; u < err.size(); ++u) {
@@ -1117,7 +1121,9 @@ void destroy_run(tkv_run* r) {
   if (r->stream) cudaStreamSynchronize(r->stream);
   if (r->copy_stream) {
     cudaStreamSynchronize(r->copy_stream);
+    cudaStreamSynchronize(r->d2h_stream);
     cudaStreamDestroy(r->copy_stream);
+    cudaStreamDestroy(r->d2h_stream);
     for (int i = 0; i < 2; ++i) {
       cudaEventDestroy(r->h2d_done[i]);
       cudaEventDestroy(r->step_done[i]);
@@ -1264,6 +1270,7 @@ void step_host_async(tkv_run* run, const void* q, const void* k, const void* v, 
   const size_t ob = (size_t)dm.U * (dm.maxpool ? 1 : dm.G) * dm.D * sizeof(float);
   if (!run->copy_stream) {
     CUDA_OK(cudaStreamCreateWithFlags(&run->copy_stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&run->d2h_stream, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
       run->d_q[i] = dalloc<uint8_t>(run, qb);
       run->d_k[i] = dalloc<uint8_t>(run, kb);
@@ -1287,15 +1294,15 @@ void step_host_async(tkv_run* run, const void* q, const void* k, const void* v, 
   CUDA_OK(cudaStreamWaitEvent(run->stream, run->d2h_done[sl], 0));  // d_out[sl] drained
   do_step(run, run->d_q[sl], run->d_k[sl], run->d_v[sl], run->d_out[sl]);
   CUDA_OK(cudaEventRecord(run->step_done[sl], run->stream));
-  CUDA_OK(cudaStreamWaitEvent(run->copy_stream, run->step_done[sl], 0));
-  CUDA_OK(cudaMemcpyAsync(out, run->d_out[sl], ob, cudaMemcpyDeviceToHost, run->copy_stream));
-  CUDA_OK(cudaEventRecord(run->d2h_done[sl], run->copy_stream));
+  CUDA_OK(cudaStreamWaitEvent(run->d2h_stream, run->step_done[sl], 0));
+  CUDA_OK(cudaMemcpyAsync(out, run->d_out[sl], ob, cudaMemcpyDeviceToHost, run->d2h_stream));
+  CUDA_OK(cudaEventRecord(run->d2h_done[sl], run->d2h_stream));
 }
 
 int tkv_step_host(tkv_run* run, const void* q, const void* k, const void* v, float* out) {
   try {
     step_host_async(run, q, k, v, out);
-    CUDA_OK(cudaStreamSynchronize(run->copy_stream));
+    CUDA_OK(cudaStreamSynchronize(run->d2h_stream));
     return TKV_OK;
   } catch (const TkvError& e) {
     return fail(e);
