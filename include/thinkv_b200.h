@@ -158,6 +158,38 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out);
 int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t unit0, int64_t step, void* q, void* k, void* v,
                      void* stream);
 
+/* ---- gather-compaction comparator ---------------------------------------
+ * Replaces the reference's GatherMethod (proj/src/sim.cpp:1117-1206), the
+ * R-KV-style baseline of BASELINE config 5: every unit keeps a dense
+ * full-precision K/V cache in arrival order; once it holds more than
+ * `budget` tokens the row with the lowest head-averaged attention score is
+ * evicted and every later row shifts down one slot (moved_token_slots).
+ * exact_scores = 1 computes the scores in fp64 in the reference's operation
+ * order (bit-exact victims); 0 uses the fp32 probabilities of the attention
+ * pass (victims can differ from the reference on near-ties). */
+typedef struct tkv_gather tkv_gather;
+typedef struct tkv_gather_desc {
+  int32_t num_units;
+  int32_t num_q_heads;
+  int32_t gqa_maxpool;
+  int32_t head_dim;
+  int64_t budget;
+  int32_t input_dtype;   /* tkv_dtype of q/k/v (also the cache element type) */
+  int32_t exact_scores;
+} tkv_gather_desc;
+
+int tkv_gather_create(tkv_ctx* ctx, const tkv_gather_desc* desc, tkv_gather** out);
+int tkv_gather_destroy(tkv_gather* g);
+/* GatherMethod::process for every unit: q [units][G][d], k/v [units][d]
+ * (device pointers, input dtype); out [units][rows][d] fp32. */
+int tkv_gather_step(tkv_gather* g, int prefill, const void* q, const void* k, const void* v, float* out,
+                    void* stream);
+/* Totals over all units (synchronises): moved_token_slots and eviction steps
+ * (steps on which any unit evicted, decode steps only: sim.cpp:1166-1169). */
+int tkv_gather_stats(tkv_gather* g, int64_t* moved_token_slots, int64_t* eviction_steps);
+/* Token ids kept by one unit in cache order; writes min(n, cap), returns n in *n. */
+int tkv_gather_ids(tkv_gather* g, int unit, int64_t* ids, int64_t cap, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

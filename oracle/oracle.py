@@ -64,6 +64,15 @@ def lib():
             L.orc_toy_stream.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.orc_synth_step.argtypes = [C.POINTER(SynthParams), C.c_int64, C.c_int32, C.c_int32,
                                          C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.orc_gather_create.restype = C.c_void_p
+            L.orc_gather_create.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64]
+            L.orc_gather_destroy.argtypes = [C.c_void_p]
+            L.orc_gather_step.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 5
+            L.orc_gather_ids.restype = C.c_int64
+            L.orc_gather_ids.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]
+            L.orc_gather_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+            L.orc_gather_toy_compare.restype = C.c_char_p
+            L.orc_gather_toy_compare.argtypes = [C.c_char_p]
             _lib = L
     return _lib
 
@@ -195,6 +204,51 @@ class OracleError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"[{code}] {msg}")
         self.code = code
+
+
+class GatherOracle:
+    """GatherMethod (sim.cpp:1117-1206) restated for external per-unit inputs:
+    attend over every kept token, evict the lowest head-averaged score once
+    over budget and shift later tokens down (moved_token_slots)."""
+
+    def __init__(self, units: int, num_q_heads: int, head_dim: int, budget: int, gqa_maxpool: bool = False):
+        self.units, self.G, self.D = units, num_q_heads, head_dim
+        self.groups = 1 if gqa_maxpool else num_q_heads
+        self._h = lib().orc_gather_create(units, num_q_heads, int(gqa_maxpool), head_dim, budget)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().orc_gather_destroy(self._h)
+        except Exception:
+            pass
+
+    def step(self, q, k, v, prefill: bool = False):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        k = np.ascontiguousarray(k, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.zeros((self.units, self.groups, self.D))
+        victims = np.zeros(self.units, dtype=np.int64)
+        rc = lib().orc_gather_step(self._h, int(prefill), q.ctypes.data, k.ctypes.data, v.ctypes.data,
+                                   out.ctypes.data, victims.ctypes.data)
+        if rc:
+            raise OracleError(rc, "gather step failed")
+        return out, victims
+
+    def ids(self, unit: int) -> np.ndarray:
+        n = lib().orc_gather_ids(self._h, unit, None, 0)
+        buf = np.zeros(max(n, 1), dtype=np.int64)
+        lib().orc_gather_ids(self._h, unit, buf.ctypes.data, n)
+        return buf[:n]
+
+    def stats(self):
+        moved, ev = C.c_int64(), C.c_int64()
+        lib().orc_gather_stats(self._h, C.byref(moved), C.byref(ev))
+        return {"moved_token_slots": moved.value, "eviction_steps": ev.value}
+
+
+def gather_toy_compare(config: dict) -> dict:
+    return json.loads(lib().orc_gather_toy_compare(json.dumps(config).encode()).decode())
 
 
 def toy_compare(config: dict) -> dict:

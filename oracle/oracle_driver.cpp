@@ -466,6 +466,57 @@ SimConfig config_for_seq(const orc_desc& d, int seq) {
   return c;
 }
 
+
+// GatherMethod restatement (sim.cpp:1117-1206) for external per-unit inputs.
+// Arithmetic goes through the compiled reference (gqa_attend); only the
+// cache bookkeeping is restated.
+struct GatherOracle {
+  int units = 0, G = 0, D = 0, groups = 0, gsize = 0;
+  std::int64_t budget = 0, pos = 0, moved = 0, eviction_steps = 0;
+  std::vector<std::vector<TokenId>> ids;
+  std::vector<std::vector<Vec>> keys, values;
+
+  // sim.cpp:1130-1170 for every unit; returns victims (-1 = none).
+  void step(bool prefill, const double* q, const double* k, const double* v, double* out, std::int64_t* victims) {
+    const double scale = 1.0 / std::sqrt(static_cast<double>(D));
+    bool evicted = false;
+    for (int l = 0; l < units; ++l) {
+      keys[l].push_back(Vec(k + static_cast<std::size_t>(l) * D, k + static_cast<std::size_t>(l + 1) * D));
+      values[l].push_back(Vec(v + static_cast<std::size_t>(l) * D, v + static_cast<std::size_t>(l + 1) * D));
+      ids[l].push_back(pos);
+      std::vector<const Vec*> kp, vp;
+      for (const Vec& x : keys[l]) kp.push_back(&x);
+      for (const Vec& x : values[l]) vp.push_back(&x);
+      std::vector<Vec> qs(G);
+      for (int h = 0; h < G; ++h)
+        qs[h].assign(q + (static_cast<std::size_t>(l) * G + h) * D, q + (static_cast<std::size_t>(l) * G + h + 1) * D);
+      AttentionRow avg;
+      avg.scores.assign(kp.size(), 0.0);
+      for (int g = 0; g < groups; ++g) {
+        std::span<const Vec> qg(qs.data() + g * gsize, gsize);
+        AttendResult r = gqa_attend(qg, std::span<const Vec* const>(kp), std::span<const Vec* const>(vp), scale);
+        std::copy(r.output.begin(), r.output.end(), out + (static_cast<std::size_t>(l) * groups + g) * D);
+        for (std::size_t i = 0; i < avg.scores.size(); ++i) avg.scores[i] += r.row.scores[i];
+      }
+      for (double& x : avg.scores) x /= static_cast<double>(groups);
+      victims[l] = -1;
+      if (static_cast<std::int64_t>(ids[l].size()) > budget) {
+        std::size_t victim = 0;
+        for (std::size_t i = 1; i < avg.scores.size(); ++i)
+          if (avg.scores[i] < avg.scores[victim]) victim = i;
+        moved += static_cast<std::int64_t>(ids[l].size() - victim - 1);
+        ids[l].erase(ids[l].begin() + victim);
+        keys[l].erase(keys[l].begin() + victim);
+        values[l].erase(values[l].begin() + victim);
+        victims[l] = static_cast<std::int64_t>(victim);
+        evicted = true;
+      }
+    }
+    if (!prefill && evicted) eviction_steps += 1;
+    pos += 1;
+  }
+};
+
 int error_code_of(const std::exception_ptr& ep, std::string* msg) {
   try {
     std::rethrow_exception(ep);
@@ -695,6 +746,90 @@ int orc_toy_stream(const char* config_json, double* q, double* k, double* v) {
   } catch (...) {
     return 2;
   }
+}
+
+
+struct orc_gather {
+  GatherOracle g;
+};
+
+orc_gather* orc_gather_create(int32_t units, int32_t num_q_heads, int32_t gqa_maxpool, int32_t head_dim,
+                              int64_t budget) {
+  auto* r = new orc_gather();
+  r->g.units = units;
+  r->g.G = num_q_heads;
+  r->g.D = head_dim;
+  r->g.gsize = gqa_maxpool ? num_q_heads : 1;
+  r->g.groups = num_q_heads / r->g.gsize;
+  r->g.budget = budget;
+  r->g.ids.resize(units);
+  r->g.keys.resize(units);
+  r->g.values.resize(units);
+  return r;
+}
+
+void orc_gather_destroy(orc_gather* g) { delete g; }
+
+int orc_gather_step(orc_gather* g, int32_t prefill, const double* q, const double* k, const double* v, double* out,
+                    int64_t* victims) {
+  try {
+    g->g.step(prefill != 0, q, k, v, out, victims);
+    return 0;
+  } catch (const Error& e) {
+    return e.exit_code();
+  } catch (...) {
+    return 1;
+  }
+}
+
+int64_t orc_gather_ids(orc_gather* g, int32_t unit, int64_t* ids, int64_t cap) {
+  const auto& v = g->g.ids.at(unit);
+  for (int64_t i = 0; i < cap && i < static_cast<int64_t>(v.size()); ++i) ids[i] = v[i];
+  return static_cast<int64_t>(v.size());
+}
+
+void orc_gather_stats(orc_gather* g, int64_t* moved, int64_t* eviction_steps) {
+  *moved = g->g.moved;
+  *eviction_steps = g->g.eviction_steps;
+}
+
+const char* orc_gather_toy_compare(const char* config_json) {
+  static thread_local std::string result;
+  try {
+    const SimConfig cfg = SimConfig::from_json(json::parse(config_json));
+    const RunOutput ref = run_baseline(cfg, "gather_compaction");
+    const int L = cfg.model.num_layers, H = cfg.model.num_heads, D = cfg.model.head_dim;
+    const std::int64_t steps = cfg.prompt_len + cfg.max_gen_len;
+    std::vector<double> q(static_cast<std::size_t>(steps) * L * H * D), k(static_cast<std::size_t>(steps) * L * D),
+        v(static_cast<std::size_t>(steps) * L * D);
+    if (orc_toy_stream(config_json, q.data(), k.data(), v.data()) != 0) throw std::runtime_error("toy stream failed");
+    orc_gather* g = orc_gather_create(L, H, cfg.model.gqa_group_size == H && H > 1 ? 1 : 0, D, cfg.budget);
+    if (cfg.model.gqa_group_size != 1 && cfg.model.gqa_group_size != H)
+      throw std::runtime_error("gather compare: gqa_group_size must be 1 or num_heads");
+    std::vector<double> out(static_cast<std::size_t>(L) * H * D);
+    std::vector<int64_t> vict(L);
+    for (std::int64_t pos = 0; pos < steps; ++pos)
+      orc_gather_step(g, pos < cfg.prompt_len, q.data() + static_cast<std::size_t>(pos) * L * H * D,
+                      k.data() + static_cast<std::size_t>(pos) * L * D, v.data() + static_cast<std::size_t>(pos) * L * D,
+                      out.data(), vict.data());
+    std::int64_t live_gen = 0;
+    for (TokenId id : g->g.ids[0])
+      if (id >= cfg.prompt_len) ++live_gen;
+    json o{{"moved_token_slots", g->g.moved},
+           {"eviction_steps", g->g.eviction_steps},
+           {"live_tokens_final", static_cast<std::int64_t>(g->g.ids[0].size())},
+           {"live_generated_final", live_gen}};
+    orc_gather_destroy(g);
+    const json rm = ref.metrics.to_json();
+    json r{{"moved_token_slots", rm.at("moved_token_slots")},
+           {"eviction_steps", rm.at("eviction_steps")},
+           {"live_tokens_final", rm.at("live_tokens_final")},
+           {"live_generated_final", rm.at("live_generated_final")}};
+    result = json{{"reference", r}, {"oracle", o}}.dump();
+  } catch (const std::exception& e) {
+    result = json{{"error", e.what()}}.dump();
+  }
+  return result.c_str();
 }
 
 void orc_synth_step(const tkv_synth_params* p, int64_t unit0, int32_t units, int32_t G, int32_t d,

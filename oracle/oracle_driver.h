@@ -76,6 +76,24 @@ const char* orc_toy_compare(const char* config_json);
 // Arrays must be sized by the caller (see oracle.py toy_stream).
 int orc_toy_stream(const char* config_json, double* q, double* k, double* v);
 
+// ---- gather-compaction comparator (GatherMethod, sim.cpp:1117-1206) -------
+// Restated for external q/k/v per unit (one unit = one reference layer).
+// Every step: append the token, gqa_attend per group, head-averaged scores;
+// over budget: evict the first minimum and shift later tokens down.
+typedef struct orc_gather orc_gather;
+orc_gather* orc_gather_create(int32_t units, int32_t num_q_heads, int32_t gqa_maxpool, int32_t head_dim,
+                              int64_t budget);
+void orc_gather_destroy(orc_gather* g);
+// out: [units][groups][d]; victims: [units] evicted index (-1: none).
+int orc_gather_step(orc_gather* g, int32_t prefill, const double* q, const double* k, const double* v,
+                    double* out, int64_t* victims);
+// Token ids (step positions) kept by a unit, in cache order; returns the count.
+int64_t orc_gather_ids(orc_gather* g, int32_t unit, int64_t* ids, int64_t cap);
+void orc_gather_stats(orc_gather* g, int64_t* moved, int64_t* eviction_steps);
+// thinkv::run_baseline(config, "gather_compaction") vs the restatement fed
+// the ToyModel stream: {"reference": metrics, "oracle": metrics}.
+const char* orc_gather_toy_compare(const char* config_json);
+
 // Synthetic bf16 inputs for `units` units starting at unit index unit0.
 void orc_synth_step(const tkv_synth_params* p, int64_t unit0, int32_t units,
                     int32_t G, int32_t d, int64_t step, uint16_t* q,

@@ -26,7 +26,7 @@ from typing import List, Optional, Sequence
 from . import _abi
 from ._abi import TkvError, check, lib
 
-__all__ = ["ThinkvConfig", "DecodeRun", "TkvError", "Context"]
+__all__ = ["ThinkvConfig", "DecodeRun", "GatherRun", "TkvError", "Context"]
 
 
 @dataclass
@@ -222,3 +222,45 @@ class DecodeRun:
         out = np.zeros(self.cfg.units, dtype=np.float64)
         check(lib.tkv_unit_sparsity(self._h, out.ctypes.data, out.size))
         return out
+
+
+class GatherRun:
+    """Gather-compaction comparator (GatherMethod, proj/src/sim.cpp:1117-1206)
+    on the GPU: dense full-precision cache, attention-score eviction of the
+    lowest head-averaged score once over budget, physical compaction.
+    exact=True reproduces the reference's victims (fp64 scores)."""
+
+    def __init__(self, units: int, num_q_heads: int, head_dim: int, budget: int, gqa_maxpool: bool = False,
+                 input_dtype: str = "bf16", exact: bool = True, device: int = 0):
+        self.ctx = Context.get(device)
+        d = _abi.GatherDesc(units, num_q_heads, int(gqa_maxpool), head_dim, budget, _abi.DTYPES[input_dtype],
+                            int(exact))
+        h = C.c_void_p()
+        check(lib.tkv_gather_create(self.ctx._h, C.byref(d), C.byref(h)))
+        self._h = h
+        self.units, self.rows = units, 1 if gqa_maxpool else num_q_heads
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.tkv_gather_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def step(self, q, k, v, out, prefill: bool = False, stream=None):
+        s = DecodeRun._stream(stream)
+        check(lib.tkv_gather_step(self._h, int(prefill), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), s))
+
+    def stats(self) -> dict:
+        moved, ev = C.c_int64(), C.c_int64()
+        check(lib.tkv_gather_stats(self._h, C.byref(moved), C.byref(ev)))
+        return {"moved_token_slots": moved.value, "eviction_steps": ev.value}
+
+    def ids(self, unit: int):
+        import numpy as np
+        n = C.c_int64()
+        check(lib.tkv_gather_ids(self._h, unit, None, 0, C.byref(n)))
+        buf = np.zeros(max(1, n.value), dtype=np.int64)
+        check(lib.tkv_gather_ids(self._h, unit, buf.ctypes.data, n.value, C.byref(n)))
+        return buf[:n.value]

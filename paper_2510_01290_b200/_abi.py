@@ -14,9 +14,10 @@ LIB_PATH = os.path.join(HERE, "libthinkv_b200.so")
 # Every symbol include/thinkv_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "tkv_last_error", "tkv_abi_version", "tkv_init", "tkv_ctx_destroy", "tkv_run_create",
-    "tkv_run_destroy", "tkv_step", "tkv_step_host", "tkv_step_host_async", "tkv_finish", "tkv_synchronize",
+    "tkv_run_destroy", "tkv_step", "tkv_step_host", "tkv_finish", "tkv_synchronize",
     "tkv_position", "tkv_dump_json", "tkv_bytes", "tkv_unit_sparsity", "tkv_synth_inputs",
-    "tkv_timing_enable", "tkv_timing_read",
+    "tkv_timing_enable", "tkv_timing_read", "tkv_step_host_async",
+    "tkv_gather_create", "tkv_gather_destroy", "tkv_gather_step", "tkv_gather_stats", "tkv_gather_ids",
 )
 
 STATUS = {0: "ok", 1: "unexpected", 2: "config", 3: "calibration", 4: "out_of_memory",
@@ -54,6 +55,12 @@ class Timing(C.Structure):
                                          "anneal_launches", "apply_launches", "total_launches")]
 
 
+class GatherDesc(C.Structure):
+    _fields_ = [("num_units", C.c_int32), ("num_q_heads", C.c_int32), ("gqa_maxpool", C.c_int32),
+                ("head_dim", C.c_int32), ("budget", C.c_int64), ("input_dtype", C.c_int32),
+                ("exact_scores", C.c_int32)]
+
+
 class TkvError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{STATUS.get(code, code)}] {msg}")
@@ -87,6 +94,11 @@ def _load():
     L.tkv_timing_enable.argtypes = [vp, C.c_int]
     L.tkv_timing_read.argtypes = [vp, C.POINTER(Timing)]
     L.tkv_synth_inputs.argtypes = [vp, C.c_uint64, C.c_int64, C.c_int64, vp, vp, vp, vp]
+    L.tkv_gather_create.argtypes = [vp, C.POINTER(GatherDesc), C.POINTER(vp)]
+    L.tkv_gather_destroy.argtypes = [vp]
+    L.tkv_gather_step.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp]
+    L.tkv_gather_stats.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.tkv_gather_ids.argtypes = [vp, C.c_int, vp, C.c_int64, C.POINTER(C.c_int64)]
     return L
 
 

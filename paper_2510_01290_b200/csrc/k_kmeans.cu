@@ -32,6 +32,7 @@
 #include <math_constants.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "tkv_codec.cuh"
 #include "tkv_kernels.h"
@@ -80,6 +81,17 @@ __device__ __forceinline__ double div_n(double x, int n) {
   if ((n & (n - 1)) == 0) return __dmul_rn(x, __longlong_as_double((long long)(1024 - __ffs(n)) << 52));
   return __ddiv_rn(x, (double)n);
 }
+
+// idx -> (row, channel) for row length D (shift/mask when D is a power of two).
+struct RowSplit {
+  int D, sh;
+  bool p2;
+  __device__ explicit RowSplit(int d) : D(d), sh(0), p2((d & (d - 1)) == 0) {
+    while ((1 << sh) < d) ++sh;
+  }
+  __device__ __forceinline__ int row(int idx) const { return p2 ? idx >> sh : idx / D; }
+  __device__ __forceinline__ int col(int idx) const { return p2 ? idx & (D - 1) : idx % D; }
+};
 
 __device__ __forceinline__ double xget(const float* X, int64_t k) { return (double)X[k]; }
 __device__ __forceinline__ double xget(const __half* X, int64_t k) { return (double)__half2float(X[k]); }
@@ -534,7 +546,8 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   const float* gX = reinterpret_cast<const float*>(base + geo.x_off());
   const double* gxs = reinterpret_cast<const double*>(base + geo.xs_off());
   const double* pd = reinterpret_cast<const double*>(base + geo.pd_off());
-  for (int i = threadIdx.x; i < m * D; i += NT) X[(i / D) * XS + i % D] = (XT)gX[i];
+  const RowSplit rs(D);
+  for (int i = threadIdx.x; i < m * D; i += NT) X[rs.row(i) * XS + rs.col(i)] = (XT)gX[i];
   for (int i = threadIdx.x; i < m; i += NT) xs[i] = gxs[i];
   for (int n = threadIdx.x; n <= MAXM; n += NT) {
     const double dn = (double)n;
@@ -569,7 +582,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   kstm(st, m, 3, 1);
   // ---- Lloyd (evictor.cpp:102-159) ----------------------------------------
   for (int idx = threadIdx.x; idx < K * D; idx += NT) {
-    const int c = idx / D, ch = idx % D;
+    const int c = rs.row(idx), ch = rs.col(idx);
     Mn[(int64_t)c * MS + ch] = xval(X, xs, s.seeds[c], ch, XS, scaled);
   }
   for (int c = threadIdx.x; c < K; c += NT) s.colsrc[c] = s.seeds[c];  // centroids are points
@@ -604,7 +617,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       members_par<NT>(s, m, K);
     }
     for (int idx = threadIdx.x; idx < K * D; idx += NT) {
-      const int c = idx / D, ch = idx % D;
+      const int c = rs.row(idx), ch = rs.col(idx);
       double acc = 0.0;
       for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
       S[idx] = div_n(acc, s.sizes[c]);
@@ -627,7 +640,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       s.flag = movement < 1e-6;
       s.cost = movement;  // == 0 exactly: the next centroids equal the ones D2 was filled with
     }
-    for (int idx = threadIdx.x; idx < K * D; idx += NT) Mn[(idx / D) * MS + idx % D] = S[idx];
+    for (int idx = threadIdx.x; idx < K * D; idx += NT) Mn[rs.row(idx) * MS + rs.col(idx)] = S[idx];
     __syncthreads();
     if (s.flag) break;
   }
@@ -636,7 +649,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   // ---- Hartigan (evictor.cpp:167-243) --------------------------------------
   members_par<NT>(s, m, K);
   for (int idx = threadIdx.x; idx < K * D; idx += NT) {
-    const int c = idx / D, ch = idx % D;
+    const int c = rs.row(idx), ch = rs.col(idx);
     double acc = 0.0;
     for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
     S[idx] = acc;
@@ -886,6 +899,334 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// tiny instances (m <= 8, e.g. the 8 -> 4 anneal with all C(8,4) = 70 seed
+// subsets): one CTA per instance, one warp per restart (warps loop over the
+// restarts), no block barriers after the shared key load.  Lanes = (point,
+// centroid) pairs for the distance table, lanes = channels for sums/means,
+// and the pairwise swaps (<= 28 pairs) are evaluated one per lane with the
+// reference's exact expression (the state cannot change before the first
+// improving pair, so the lowest improving pair index is the sequential pick).
+// Same operations in the same order as kmeans_from_seeds (evictor.cpp:94-251).
+// ---------------------------------------------------------------------------
+constexpr int kTinyM = 8;
+constexpr int kTinyWarps = 4;
+
+struct TinyState {  // per warp, warp-uniform
+  int assign[kTinyM];
+  int sizes[kTinyM];
+  unsigned members[kTinyM];
+  int colsrc[kTinyM];
+  int seeds[kTinyM];
+};
+
+template <typename XT>
+__device__ __forceinline__ double tiny_dist(const XT* X, int XS, const double* xs, bool scaled, int i,
+                                            const double* mu, int D) {
+  double d = 0.0;
+  for (int ch = 0; ch < D; ++ch) {
+    const double t = __dsub_rn(xval(X, xs, i, ch, XS, scaled), mu[ch]);
+    d = __dadd_rn(d, __dmul_rn(t, t));
+  }
+  return d;
+}
+
+// d2 columns per colsrc (pd copy / keep / exact evaluation).
+template <typename XT>
+__device__ __forceinline__ void tiny_fill(const TinyState& w, const XT* X, int XS, const double* xs, bool scaled,
+                                          const double (*pd)[kTinyM], const double* Mn, double* d2, int m, int K,
+                                          int D, int lane) {
+  for (int p = lane; p < m * K; p += 32) {
+    const int i = p / K, c = p % K;
+    const int src = w.colsrc[c];
+    if (src >= 0) d2[p] = pd[i][src];
+    else if (src == kColCompute) d2[p] = tiny_dist(X, XS, xs, scaled, i, Mn + c * D, D);
+  }
+  __syncwarp();
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops,
+                                                                  int nops, const int32_t* __restrict__ item_prefix,
+                                                                  int nitems, int item0, uint8_t* __restrict__ scratch,
+                                                                  KmGeo geo, int scaled_any, int kmax) {
+  const TkvDims& dm = st.dm;
+  const int item = item0 + blockIdx.x;
+  if (item >= nitems) return;
+  const int oi = find_op(item_prefix, nops, item);
+  const TkvAnnealOp op = ops[oi];
+  uint8_t* base = scratch + (int64_t)blockIdx.x * geo.bytes();
+  const int32_t* misc = reinterpret_cast<const int32_t*>(base + geo.misc_off());
+  if (misc[1]) return;
+  const int m = misc[0], K = op.K, D = dm.D;
+  const bool scaled = scaled_any != 0;
+  const int nr = op.nrestart > 0 ? op.nrestart : op.ncombos;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  extern __shared__ __align__(16) uint8_t dyn[];
+  const int XS = D + 4 / (int)sizeof(XT);
+  XT* X = reinterpret_cast<XT*>(dyn);
+  __shared__ double xs[kTinyM];
+  __shared__ double pd[kTinyM][kTinyM];
+  __shared__ TinyState ws[kTinyWarps];
+  TinyState& w = ws[warp];
+  double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)kTinyM * XS * sizeof(XT) + 15) / 16 * 16)) +
+               (int64_t)warp * (2 * kmax * D + kTinyM * kTinyM);
+  double* S = Mn + (int64_t)kmax * D;
+  double* d2 = S + (int64_t)kmax * D;  // [i * K + c]
+  {
+    const float* gX = reinterpret_cast<const float*>(base + geo.x_off());
+    const double* gxs = reinterpret_cast<const double*>(base + geo.xs_off());
+    const double* gpd = reinterpret_cast<const double*>(base + geo.pd_off());
+    const RowSplit rs(D);
+    for (int i = threadIdx.x; i < m * D; i += blockDim.x) X[rs.row(i) * XS + rs.col(i)] = (XT)gX[i];
+    for (int i = threadIdx.x; i < m; i += blockDim.x) xs[i] = gxs[i];
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) pd[t / m][t % m] = gpd[(int64_t)(t / m) * geo.mmax + t % m];
+  }
+  __syncthreads();
+  for (int r = warp; r < nr; r += kTinyWarps) {
+    // ---- seeds -------------------------------------------------------------------
+    if (lane == 0) {
+      if (op.nrestart > 0) {
+        const int32_t* sd = reinterpret_cast<const int32_t*>(base + geo.seeds_off()) + r * geo.kmax;
+        for (int c = 0; c < K; ++c) w.seeds[c] = sd[c];
+      } else {
+        // r-th K-subset of {0..m-1} in lexicographic order (evictor.cpp:274-283)
+        int rank = r, x = 0;
+        for (int c = 0; c < K; ++c) {
+          while (true) {
+            double cnt = 1.0;
+            const int n = m - x - 1, k = K - c - 1;
+            for (int t = 0; t < k; ++t) cnt = cnt * (double)(n - t) / (double)(t + 1);
+            const int ci = (int)(cnt + 0.5);
+            if (rank < ci) break;
+            rank -= ci;
+            ++x;
+          }
+          w.seeds[c] = x;
+          ++x;
+        }
+      }
+      for (int c = 0; c < K; ++c) w.colsrc[c] = w.seeds[c];  // centroids are points
+    }
+    __syncwarp();
+    for (int idx = lane; idx < K * D; idx += 32) {
+      const int c = idx / D, ch = idx - c * D;
+      Mn[idx] = xval(X, xs, w.seeds[c], ch, XS, scaled);
+    }
+    __syncwarp();
+    double movement = 0.0;
+    // ---- Lloyd (evictor.cpp:102-159) ------------------------------------------------
+    for (int iter = 0; iter < 50; ++iter) {
+      tiny_fill(w, X, XS, xs, scaled, pd, Mn, d2, m, K, D, lane);
+      int a = 0;
+      if (lane < m) {  // nearest centroid, ties to the lowest index
+        double bd = d2[lane * K];
+        for (int c = 1; c < K; ++c)
+          if (d2[lane * K + c] < bd) { bd = d2[lane * K + c]; a = c; }
+        w.assign[lane] = a;
+      }
+      for (int c = 0; c < K; ++c) {
+        const unsigned mb = __ballot_sync(0xffffffffu, lane < m && a == c);
+        if (lane == 0) { w.members[c] = mb; w.sizes[c] = __popc(mb); }
+      }
+      __syncwarp();
+      if (lane == 0) {  // empty-cluster repair (evictor.cpp:123-141)
+        for (int c = 0; c < K; ++c) {
+          if (w.sizes[c] > 0) continue;
+          int donor = 0;
+          for (int d = 1; d < K; ++d)
+            if (w.sizes[d] > w.sizes[donor]) donor = d;
+          int steal = m;
+          double steal_d = -1.0;
+          for (int i = 0; i < m; ++i) {
+            if (w.assign[i] != donor) continue;
+            const double d = d2[i * K + donor];
+            if (d > steal_d) { steal = i; steal_d = d; }
+          }
+          w.assign[steal] = c;
+          w.members[donor] &= ~(1u << steal);
+          w.members[c] |= 1u << steal;
+          --w.sizes[donor];
+          ++w.sizes[c];
+        }
+      }
+      __syncwarp();
+      // next centroids: member sums in point order / size (lanes = channels)
+      for (int idx = lane; idx < K * D; idx += 32) {
+        const int c = idx / D, ch = idx - c * D;
+        double acc = 0.0;
+        unsigned mm = w.members[c];
+        while (mm) {
+          const int i = __ffs(mm) - 1;
+          mm &= mm - 1;
+          acc = __dadd_rn(acc, xval(X, xs, i, ch, XS, scaled));
+        }
+        S[idx] = div_n(acc, w.sizes[c]);
+      }
+      __syncwarp();
+      // movement per centroid (lane c, channel order); next fill's column sources
+      double mv = 0.0;
+      if (lane < K) {
+        double d = 0.0;
+        for (int ch = 0; ch < D; ++ch) {
+          const double t = __dsub_rn(S[lane * D + ch], Mn[lane * D + ch]);
+          d = __dadd_rn(d, __dmul_rn(t, t));
+        }
+        mv = __dsqrt_rn(d);
+        w.colsrc[lane] = d == 0.0 ? kColKeep : (w.sizes[lane] == 1 ? __ffs(w.members[lane]) - 1 : kColCompute);
+      }
+      movement = 0.0;
+      for (int c = 0; c < K; ++c) {
+        const double x = __shfl_sync(0xffffffffu, mv, c);
+        movement = movement < x ? x : movement;
+      }
+      for (int idx = lane; idx < K * D; idx += 32) Mn[idx] = S[idx];
+      __syncwarp();
+      if (movement < 1e-6) break;
+    }
+    // ---- Hartigan (evictor.cpp:167-243) ---------------------------------------------
+    for (int idx = lane; idx < K * D; idx += 32) {
+      const int c = idx / D, ch = idx - c * D;
+      double acc = 0.0;
+      unsigned mm = w.members[c];
+      while (mm) {
+        const int i = __ffs(mm) - 1;
+        mm &= mm - 1;
+        acc = __dadd_rn(acc, xval(X, xs, i, ch, XS, scaled));
+      }
+      S[idx] = acc;
+      Mn[idx] = div_n(acc, w.sizes[c]);
+    }
+    __syncwarp();
+    if (movement != 0.0) tiny_fill(w, X, XS, xs, scaled, pd, Mn, d2, m, K, D, lane);
+    for (int pass = 0; pass < 100; ++pass) {
+      bool moved = false;  // warp-uniform
+      for (int i = 0; i < m; ++i) {
+        const int from = w.assign[i];
+        const int nfrom = w.sizes[from];
+        if (nfrom <= 1) continue;
+        const double na = (double)nfrom;
+        const double removal = __dmul_rn(__ddiv_rn(-na, __dsub_rn(na, 1.0)), d2[i * K + from]);
+        double bd = 0.0;
+        int bt = 0x7fffffff;
+        if (lane < K && lane != from) {
+          const double nb = (double)w.sizes[lane];
+          const double delta = __dadd_rn(removal, __dmul_rn(__ddiv_rn(nb, __dadd_rn(nb, 1.0)), d2[i * K + lane]));
+          if (delta < -1e-12) { bd = delta; bt = lane; }
+        }
+        // best target: the lowest index among the minimal deltas (strict <, ascending)
+        for (int o = 16; o > 0; o >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+          const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+          if (ot != 0x7fffffff && (bt == 0x7fffffff || od < bd || (od == bd && ot < bt))) { bd = od; bt = ot; }
+        }
+        if (bt == 0x7fffffff) continue;
+        const int to = bt;
+        moved = true;
+        __syncwarp();
+        if (lane == 0) {  // apply_move (evictor.cpp:189-196)
+          w.sizes[from] -= 1;
+          w.sizes[to] += 1;
+          w.members[from] &= ~(1u << i);
+          w.members[to] |= 1u << i;
+          w.assign[i] = to;
+        }
+        __syncwarp();
+        const int nf = w.sizes[from], nt = w.sizes[to];
+        for (int ch = lane; ch < D; ch += 32) {
+          const double x = xval(X, xs, i, ch, XS, scaled);
+          const double sf = __dsub_rn(S[from * D + ch], x);
+          const double sto = __dadd_rn(S[to * D + ch], x);
+          S[from * D + ch] = sf;
+          S[to * D + ch] = sto;
+          Mn[from * D + ch] = div_n(sf, nf);
+          Mn[to * D + ch] = div_n(sto, nt);
+        }
+        __syncwarp();
+        for (int p = lane; p < 2 * m; p += 32) {
+          const int pi = p >> 1, c = (p & 1) ? to : from;
+          d2[pi * K + c] = tiny_dist(X, XS, xs, scaled, pi, Mn + c * D, D);
+        }
+        __syncwarp();
+      }
+      if (moved) continue;
+      // pairwise swaps (evictor.cpp:213-240): pair q = lane in lexicographic order
+      int pi = 0, pj = 0;
+      bool valid = false;
+      for (int i = 0, q = 0; i < m; ++i)
+        for (int j = i + 1; j < m; ++j, ++q)
+          if (q == lane) { pi = i; pj = j; valid = true; }
+      bool improving = false;
+      if (valid && w.assign[pi] != w.assign[pj]) {
+        const int ai = w.assign[pi], aj = w.assign[pj];
+        const double na = (double)w.sizes[ai], nb = (double)w.sizes[aj];
+        const double* mua = Mn + ai * D;
+        const double* mub = Mn + aj * D;
+        double delta = 0.0;
+        for (int ch = 0; ch < D; ++ch) {
+          const double xi = xval(X, xs, pi, ch, XS, scaled), xj = xval(X, xs, pj, ch, XS, scaled);
+          const double ma = __dadd_rn(mua[ch], __ddiv_rn(__dsub_rn(xj, xi), na));
+          const double mb = __dadd_rn(mub[ch], __ddiv_rn(__dsub_rn(xi, xj), nb));
+          delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi)),
+                                             __dmul_rn(na, __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua[ch], mua[ch])))));
+          delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj)),
+                                             __dmul_rn(nb, __dsub_rn(__dmul_rn(mb, mb), __dmul_rn(mub[ch], mub[ch])))));
+        }
+        improving = delta < -1e-12;
+      }
+      const unsigned imp = __ballot_sync(0xffffffffu, improving);
+      if (!imp) break;
+      const int q = __ffs(imp) - 1;
+      const int si = __shfl_sync(0xffffffffu, pi, q), sj = __shfl_sync(0xffffffffu, pj, q);
+      const int a = w.assign[si], b = w.assign[sj];
+      __syncwarp();
+      if (lane == 0) {  // apply_move(i, a, b); apply_move(j, b, a): sizes unchanged
+        w.members[a] = (w.members[a] & ~(1u << si)) | (1u << sj);
+        w.members[b] = (w.members[b] & ~(1u << sj)) | (1u << si);
+        w.assign[si] = b;
+        w.assign[sj] = a;
+      }
+      __syncwarp();
+      const int na_ = w.sizes[a], nb_ = w.sizes[b];
+      for (int ch = lane; ch < D; ch += 32) {
+        const double xi = xval(X, xs, si, ch, XS, scaled), xj = xval(X, xs, sj, ch, XS, scaled);
+        const double sa = __dadd_rn(__dsub_rn(S[a * D + ch], xi), xj);
+        const double sb = __dsub_rn(__dadd_rn(S[b * D + ch], xi), xj);
+        S[a * D + ch] = sa;
+        S[b * D + ch] = sb;
+        Mn[a * D + ch] = div_n(sa, na_);
+        Mn[b * D + ch] = div_n(sb, nb_);
+      }
+      __syncwarp();
+      for (int p = lane; p < 2 * m; p += 32) {
+        const int ii = p >> 1, c = (p & 1) ? b : a;
+        d2[ii * K + c] = tiny_dist(X, XS, xs, scaled, ii, Mn + c * D, D);
+      }
+      __syncwarp();
+    }
+    // ---- cost (point order) and medoids ---------------------------------------------
+    double cst = 0.0;
+    for (int i = 0; i < m; ++i) cst = __dadd_rn(cst, d2[i * K + w.assign[i]]);
+    int med = m;
+    if (lane < K) {  // nearest member, ties to the lowest index
+      double bd = CUDART_INF;
+      for (int i = 0; i < m; ++i) {
+        if (w.assign[i] != lane) continue;
+        const double d = d2[i * K + lane];
+        if (d < bd) { bd = d; med = i; }
+      }
+    }
+    const int32_t* ids = reinterpret_cast<const int32_t*>(base + geo.ids_off());
+    uint32_t* mask = reinterpret_cast<uint32_t*>(base + geo.mask_off()) + (int64_t)r * geo.W;
+    for (int wd = lane; wd < geo.W; wd += 32) mask[wd] = 0;
+    __syncwarp();
+    if (lane < K) atomicOr(mask + (ids[med] >> 5), 1u << (ids[med] & 31));
+    if (lane == 0) reinterpret_cast<double*>(base + geo.cost_off())[r] = cst;
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // final: lowest cost restart -> retained mask, eviction log, segment mask
 // ---------------------------------------------------------------------------
@@ -954,6 +1295,24 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
   if (e != cudaSuccess) {
     fprintf(stderr, "[kmeans] prep launch failed: items=%d: %s\n", item_count, cudaGetErrorString(e));
     return e;
+  }
+  if (mmax <= kTinyM && getenv("TKV_KM_NO_TINY") == nullptr) {
+    const int xb = x16 ? 2 : 4;
+    const size_t tsm = (size_t)((kTinyM * (st.dm.D + 4 / xb) * xb + 15) / 16 * 16) +
+                       (size_t)kTinyWarps * (2 * kmax * st.dm.D + kTinyM * kTinyM) * 8;
+    if (tsm > 200 * 1024) return cudaErrorInvalidConfiguration;
+    auto kern = x16 ? km_tiny_kernel<__half> : km_tiny_kernel<float>;
+    if (tsm > 16 * 1024) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<item_count, 32 * kTinyWarps, tsm, stream>>>(st, ops, nops, item_prefix, item0 + item_count, item0, scratch,
+                                                       geo, scaled_any, kmax);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    km_final_kernel<<<(item_count + 127) / 128, 128, 0, stream>>>(st, ops, nops, item_prefix, item0 + item_count,
+                                                                   item0, scratch, geo, log);
+    return cudaGetLastError();
   }
   const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D, x16 ? 2 : 4);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // tau x d beyond the smem design point

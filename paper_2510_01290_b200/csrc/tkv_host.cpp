@@ -1458,4 +1458,152 @@ int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t unit0, int64_t step, v
   }
 }
 
+// ---------------------------------------------------------------------------
+// gather-compaction comparator (GatherMethod, sim.cpp:1117-1206)
+// ---------------------------------------------------------------------------
+struct tkv_gather {
+  tkv_ctx* ctx = nullptr;
+  tkv_gather_desc desc{};
+  TkvGatherState st{};
+  cudaStream_t stream = nullptr;
+  int64_t n = 0;        // rows held by every unit (identical across units)
+  int64_t pos = 0;
+  int64_t moved = 0, eviction_steps = 0;
+  std::vector<int64_t> pending;  // steps whose victims are not yet accounted (decode flag in bit 62)
+  int32_t* d_victims_log = nullptr;  // [log_cap][U]
+  int64_t log_cap = 0, log_used = 0;
+};
+
+namespace {
+void gather_drain(tkv_gather* g) {
+  CUDA_OK(cudaStreamSynchronize(g->stream));
+  if (g->log_used == 0) return;
+  const int U = g->st.U;
+  std::vector<int32_t> v((size_t)g->log_used * U);
+  CUDA_OK(cudaMemcpy(v.data(), g->d_victims_log, v.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  for (int64_t s = 0; s < g->log_used; ++s) {
+    const int64_t rows = g->pending[s] & ((1ll << 40) - 1);  // rows after the append
+    const bool decode = (g->pending[s] >> 62) & 1;
+    for (int u = 0; u < U; ++u) g->moved += rows - 1 - v[(size_t)s * U + u];
+    if (decode) g->eviction_steps += 1;
+  }
+  g->log_used = 0;
+  g->pending.clear();
+}
+}  // namespace
+
+int tkv_gather_create(tkv_ctx* ctx, const tkv_gather_desc* d, tkv_gather** out) {
+  try {
+    if (!ctx || !d || !out) throw TkvError(TKV_ERR_CONFIG, "null argument");
+    if (d->num_units < 1 || d->num_q_heads < 1 || d->head_dim < 1 || d->budget < 1)
+      throw TkvError(TKV_ERR_CONFIG, "gather: units, heads, head_dim and budget must be positive");
+    if (d->input_dtype < 0 || d->input_dtype > 2) throw TkvError(TKV_ERR_CONFIG, "gather: unknown input dtype");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    auto g = std::make_unique<tkv_gather>();
+    g->ctx = ctx;
+    g->desc = *d;
+    TkvGatherState& st = g->st;
+    st.U = d->num_units;
+    st.G = d->num_q_heads;
+    st.D = d->head_dim;
+    st.maxpool = d->gqa_maxpool ? 1 : 0;
+    st.budget = d->budget;
+    st.cap = (int32_t)(d->budget + 1);
+    st.in_dtype = d->input_dtype;
+    st.in_bytes = d->input_dtype == TKV_DTYPE_BF16 ? 2 : (d->input_dtype == TKV_DTYPE_F32 ? 4 : 8);
+    if (tkv_gather_smem(st) > 200 * 1024) throw TkvError(TKV_ERR_CONFIG, "gather: budget x heads exceeds shared memory");
+    const size_t rows = (size_t)st.U * st.cap;
+    CUDA_OK(cudaMalloc(&st.k, rows * st.D * st.in_bytes));
+    CUDA_OK(cudaMalloc(&st.v, rows * st.D * st.in_bytes));
+    CUDA_OK(cudaMalloc(&st.ids, rows * sizeof(int32_t)));
+    CUDA_OK(cudaMalloc(&st.victim, (size_t)st.U * sizeof(int32_t)));
+    g->log_cap = 256;
+    CUDA_OK(cudaMalloc(&g->d_victims_log, (size_t)g->log_cap * st.U * sizeof(int32_t)));
+    CUDA_OK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    *out = g.release();
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_gather_destroy(tkv_gather* g) {
+  if (!g) return TKV_OK;
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  cudaFree(g->st.k);
+  cudaFree(g->st.v);
+  cudaFree(g->st.ids);
+  cudaFree(g->st.victim);
+  cudaFree(g->d_victims_log);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+  return TKV_OK;
+}
+
+int tkv_gather_step(tkv_gather* g, int prefill, const void* q, const void* k, const void* v, float* out,
+                    void* stream) {
+  try {
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaStream_t s = user ? user : g->stream;
+    check_launch(tkv_launch_gather_step(g->st, (int)g->n, g->pos, q, k, v, out, g->desc.exact_scores, s),
+                 "gather step kernel");
+    const int64_t rows = g->n + 1;
+    if (rows > g->st.budget) {  // every unit evicted one row this step
+      if (g->log_used == g->log_cap) {
+        CUDA_OK(cudaStreamSynchronize(s));
+        gather_drain(g);
+      }
+      CUDA_OK(cudaMemcpyAsync(g->d_victims_log + (size_t)g->log_used * g->st.U, g->st.victim,
+                              (size_t)g->st.U * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+      g->pending.push_back(rows | ((int64_t)(prefill ? 0 : 1) << 62));
+      g->log_used += 1;
+      g->n = rows - 1;
+    } else {
+      g->n = rows;
+    }
+    g->pos += 1;
+    if (user && user != g->stream) {  // keep later synchronising calls ordered
+      cudaEvent_t ev;
+      CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CUDA_OK(cudaEventRecord(ev, user));
+      CUDA_OK(cudaStreamWaitEvent(g->stream, ev, 0));
+      CUDA_OK(cudaEventDestroy(ev));
+    }
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_gather_stats(tkv_gather* g, int64_t* moved, int64_t* eviction_steps) {
+  try {
+    gather_drain(g);
+    if (moved) *moved = g->moved;
+    if (eviction_steps) *eviction_steps = g->eviction_steps;
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  }
+}
+
+int tkv_gather_ids(tkv_gather* g, int unit, int64_t* ids, int64_t cap, int64_t* n) {
+  try {
+    if (unit < 0 || unit >= g->st.U) throw TkvError(TKV_ERR_CONFIG, "no such unit");
+    CUDA_OK(cudaStreamSynchronize(g->stream));
+    std::vector<int32_t> v(g->n);
+    if (g->n > 0)
+      CUDA_OK(cudaMemcpy(v.data(), g->st.ids + (size_t)unit * g->st.cap, v.size() * sizeof(int32_t),
+                         cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < cap && i < g->n; ++i) ids[i] = v[i];
+    if (n) *n = g->n;
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  }
+}
+
 }  // extern "C"

@@ -57,3 +57,9 @@ cudaError_t tkv_launch_synth(uint64_t seed, int units_per_seq, int tau, int sink
 
 // One-time state initialisation (window free stacks, free-block counts).
 cudaError_t tkv_launch_init(const TkvState& st, cudaStream_t stream);
+
+// Gather-compaction comparator (k_gather.cu): append, attention, head-averaged
+// scores (exact fp64 when `exact`), first-minimum eviction and compaction.
+size_t tkv_gather_smem(const TkvGatherState& g);
+cudaError_t tkv_launch_gather_step(const TkvGatherState& g, int n, int64_t pos, const void* q, const void* k,
+                                   const void* v, float* out, int exact, cudaStream_t stream);

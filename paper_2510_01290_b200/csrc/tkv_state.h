@@ -117,3 +117,15 @@ struct TkvApplyGroup {
   int32_t unit0, nunits;
   int32_t op_begin, op_end;
 };
+
+// Gather-compaction comparator state (GatherMethod, sim.cpp:1117-1206): per
+// unit a dense full-precision K/V cache in arrival order, compacted on every
+// eviction.  cap = budget + 1 rows.
+struct TkvGatherState {
+  int32_t U, G, D, maxpool, cap, in_dtype, in_bytes;
+  int64_t budget;
+  uint8_t* k;       // [U][cap][D] input dtype
+  uint8_t* v;
+  int32_t* ids;     // [U][cap] token ids (positions)
+  int32_t* victim;  // [U] last evicted row
+};

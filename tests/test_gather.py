@@ -1,0 +1,60 @@
+"""Gather-compaction comparator (GatherMethod, proj/src/sim.cpp:1117-1206) on
+the GPU against the oracle's restatement on identical inputs: kept token ids
+(cache order) and moved_token_slots / eviction_steps bit-exact with fp64
+scores, attention outputs within harness.ATOL/RTOL."""
+import numpy as np
+import pytest
+
+import oracle as O
+from harness import ATOL, RTOL
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2510_01290_b200 import GatherRun  # noqa: E402
+
+SEED = 0x71534B56
+
+
+@pytest.mark.parametrize("G,D,maxpool,budget,steps,prompt", [
+    (4, 128, False, 48, 140, 0),
+    (8, 64, True, 40, 120, 10),
+    (5, 128, False, 33, 90, 0),
+])
+def test_gather_parity_exact(G, D, maxpool, budget, steps, prompt):
+    units = 3
+    dev = torch.device("cuda:0")
+    gpu = GatherRun(units, G, D, budget, gqa_maxpool=maxpool, exact=True)
+    orc = O.GatherOracle(units, G, D, budget, gqa_maxpool=maxpool)
+    rows = 1 if maxpool else G
+    out = torch.empty((units, rows, D), device=dev)
+    for t in range(steps):
+        q, k, v = O.synth_step(SEED, units, 32, units, G, D, t)
+        ref, _ = orc.step(O.bf16_to_f64(q), O.bf16_to_f64(k), O.bf16_to_f64(v), prefill=t < prompt)
+        tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev) for x in (q, k, v))
+        gpu.step(tq, tk, tv, out, prefill=t < prompt)
+        got = out.double().cpu().numpy()
+        err = float(np.max(np.abs(got - ref)))
+        assert err <= ATOL + RTOL * float(np.max(np.abs(ref))), f"step {t}: {err}"
+        if t % 17 == 0 or t == steps - 1:
+            for u in range(units):
+                assert np.array_equal(gpu.ids(u), orc.ids(u)), f"step {t} unit {u}: kept ids differ"
+    assert gpu.stats() == orc.stats()
+
+
+def test_gather_fast_scores_run():
+    """fp32 scores: same cache mechanics, victims may differ on near-ties."""
+    units, G, D, budget = 2, 4, 128, 32
+    dev = torch.device("cuda:0")
+    gpu = GatherRun(units, G, D, budget, exact=False)
+    out = torch.empty((units, G, D), device=dev)
+    for t in range(80):
+        q, k, v = O.synth_step(SEED, units, 32, units, G, D, t)
+        tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev) for x in (q, k, v))
+        gpu.step(tq, tk, tv, out)
+    st = gpu.stats()
+    assert st["eviction_steps"] == 80 - budget
+    assert len(gpu.ids(0)) == budget and st["moved_token_slots"] >= 0
+    assert torch.isfinite(out).all()

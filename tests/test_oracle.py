@@ -113,3 +113,23 @@ def test_synth_is_deterministic_and_bf16():
     assert np.all(np.isfinite(f)) and 0.5 < f.std() < 3.0
     c = O.synth_step(7, 4, 16, 8, 4, 64, 11)
     assert not np.array_equal(c[1], k)
+
+
+GATHER_CONFIGS = {
+    "small": TOY_CONFIGS["small"],
+    "maxpool": {**BASE, "model": {**BASE["model"], "num_heads": 4, "gqa_group_size": 4}},
+    "prompt_misaligned": TOY_CONFIGS["prompt_misaligned"],
+    "big_d": TOY_CONFIGS["big_d"],
+}
+
+
+@pytest.mark.parametrize("name", sorted(GATHER_CONFIGS))
+def test_gather_restatement_matches_run_baseline(name):
+    """The GatherMethod restatement (external inputs) reproduces the
+    reference's run_baseline(config, "gather_compaction") metrics."""
+    cfg = dict(GATHER_CONFIGS[name])
+    cfg["budget"] = min(cfg["budget"], 24)
+    r = O.gather_toy_compare(cfg)
+    assert "error" not in r, r.get("error")
+    assert r["oracle"] == r["reference"]
+    assert r["reference"]["moved_token_slots"] > 0
