@@ -48,8 +48,9 @@ __device__ __forceinline__ float block_max(float v, float* red) {
   return r;
 }
 
-// smem: qf [G][D] f32 | lg [G][cap] f32 (logits -> probabilities) |
-//       qd [G][D] f64 | ld [cap] f64 (exact scores of one row) | avg [cap] f64
+// smem: qf [G][D] f32 | lg [G][cap] f32 (logits -> probabilities) | exact
+//       mode only: qd [G][D] f64 | sc [cap] f64 (exact scores of one row) |
+//       avg [cap] f64
 __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g, int n, int64_t pos,
                                                                const void* __restrict__ qin,
                                                                const void* __restrict__ kin,
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g,
   if (threadIdx.x == 0) g.ids[(int64_t)u * cap + n] = (int32_t)pos;
   for (int i = threadIdx.x; i < G * D; i += kThreads) {
     qf[i] = in_f(qin, g.in_dtype, (int64_t)u * G * D + i);
-    qd[i] = in_d(qin, g.in_dtype, (int64_t)u * G * D + i);
+    if (exact) qd[i] = in_d(qin, g.in_dtype, (int64_t)u * G * D + i);
   }
   __syncthreads();
   // 2. fp32 attention: logits per head, row max / softmax, outputs
@@ -172,20 +173,23 @@ __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g,
       __syncthreads();
     }
     for (int i = threadIdx.x; i < rows; i += kThreads) avg[i] = __ddiv_rn(avg[i], (double)R);
-  } else {
-    for (int i = threadIdx.x; i < rows; i += kThreads) {
-      float a = 0.f;
-      for (int r = 0; r < R; ++r) a += lg[(int64_t)r * cap + i];
-      avg[i] = (double)a;
-    }
   }
   __syncthreads();
   // first minimum (strict <, ascending: sim.cpp:1160-1162)
   {
     double bv = CUDART_INF;
     int bi = 0x7fffffff;
-    for (int i = threadIdx.x; i < rows; i += kThreads)
-      if (avg[i] < bv) { bv = avg[i]; bi = i; }
+    for (int i = threadIdx.x; i < rows; i += kThreads) {
+      double a;
+      if (exact) {
+        a = avg[i];
+      } else {  // fp32 head-averaged probabilities of the attention pass
+        float f = 0.f;
+        for (int r = 0; r < R; ++r) f += lg[(int64_t)r * cap + i];
+        a = (double)f;
+      }
+      if (a < bv) { bv = a; bi = i; }
+    }
     for (int o = 16; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
@@ -249,13 +253,14 @@ __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g,
 
 }  // namespace
 
-size_t tkv_gather_smem(const TkvGatherState& g) {
-  return (size_t)g.G * g.D * 4 + (size_t)((g.G * g.cap + 1) & ~1) * 4 + (size_t)g.G * g.D * 8 + (size_t)2 * g.cap * 8;
+size_t tkv_gather_smem(const TkvGatherState& g, int exact) {
+  const size_t base = (size_t)g.G * g.D * 4 + (size_t)((g.G * g.cap + 1) & ~1) * 4;
+  return exact ? base + (size_t)g.G * g.D * 8 + (size_t)2 * g.cap * 8 : base;
 }
 
 cudaError_t tkv_launch_gather_step(const TkvGatherState& g, int n, int64_t pos, const void* q, const void* k,
                                    const void* v, float* out, int exact, cudaStream_t s) {
-  const size_t smem = tkv_gather_smem(g);
+  const size_t smem = tkv_gather_smem(g, exact);
   static bool cfg = false;
   if (!cfg) {
     cudaFuncSetAttribute(gather_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -968,6 +968,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
   XT* X = reinterpret_cast<XT*>(dyn);
   __shared__ double xs[kTinyM];
   __shared__ double pd[kTinyM][kTinyM];
+  __shared__ double tabA[kTinyM + 1], tabR[kTinyM + 1];  // n / (n + 1.0), -n / (n - 1.0) (evictor.cpp:201, 205)
   __shared__ TinyState ws[kTinyWarps];
   TinyState& w = ws[warp];
   double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)kTinyM * XS * sizeof(XT) + 15) / 16 * 16)) +
@@ -982,6 +983,11 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     for (int i = threadIdx.x; i < m * D; i += blockDim.x) X[rs.row(i) * XS + rs.col(i)] = (XT)gX[i];
     for (int i = threadIdx.x; i < m; i += blockDim.x) xs[i] = gxs[i];
     for (int t = threadIdx.x; t < m * m; t += blockDim.x) pd[t / m][t % m] = gpd[(int64_t)(t / m) * geo.mmax + t % m];
+    for (int n = threadIdx.x; n <= kTinyM; n += blockDim.x) {
+      const double dn = (double)n;
+      tabA[n] = __ddiv_rn(dn, __dadd_rn(dn, 1.0));
+      tabR[n] = __ddiv_rn(-dn, __dsub_rn(dn, 1.0));
+    }
   }
   __syncthreads();
   for (int r = warp; r < nr; r += kTinyWarps) {
@@ -1106,13 +1112,11 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
         const int from = w.assign[i];
         const int nfrom = w.sizes[from];
         if (nfrom <= 1) continue;
-        const double na = (double)nfrom;
-        const double removal = __dmul_rn(__ddiv_rn(-na, __dsub_rn(na, 1.0)), d2[i * K + from]);
+        const double removal = __dmul_rn(tabR[nfrom], d2[i * K + from]);
         double bd = 0.0;
         int bt = 0x7fffffff;
         if (lane < K && lane != from) {
-          const double nb = (double)w.sizes[lane];
-          const double delta = __dadd_rn(removal, __dmul_rn(__ddiv_rn(nb, __dadd_rn(nb, 1.0)), d2[i * K + lane]));
+          const double delta = __dadd_rn(removal, __dmul_rn(tabA[w.sizes[lane]], d2[i * K + lane]));
           if (delta < -1e-12) { bd = delta; bt = lane; }
         }
         // best target: the lowest index among the minimal deltas (strict <, ascending)
@@ -1160,20 +1164,30 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
       bool improving = false;
       if (valid && w.assign[pi] != w.assign[pj]) {
         const int ai = w.assign[pi], aj = w.assign[pj];
-        const double na = (double)w.sizes[ai], nb = (double)w.sizes[aj];
-        const double* mua = Mn + ai * D;
-        const double* mub = Mn + aj * D;
-        double delta = 0.0;
-        for (int ch = 0; ch < D; ++ch) {
-          const double xi = xval(X, xs, pi, ch, XS, scaled), xj = xval(X, xs, pj, ch, XS, scaled);
-          const double ma = __dadd_rn(mua[ch], __ddiv_rn(__dsub_rn(xj, xi), na));
-          const double mb = __dadd_rn(mub[ch], __ddiv_rn(__dsub_rn(xi, xj), nb));
-          delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi)),
-                                             __dmul_rn(na, __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua[ch], mua[ch])))));
-          delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj)),
-                                             __dmul_rn(nb, __dsub_rn(__dmul_rn(mb, mb), __dmul_rn(mub[ch], mub[ch])))));
+        const int sa = w.sizes[ai], sb = w.sizes[aj];
+        const double na = (double)sa, nb = (double)sb;
+        // filter: the exact delta equals dja - dia + dib - djb - (1/na + 1/nb) pd[i][j]
+        // up to rounding far below the margin (as in km_restart_kernel)
+        const double wgt = 1.0 / na + 1.0 / nb;
+        const double dja = d2[pj * K + ai], dia = d2[pi * K + ai], dib = d2[pi * K + aj], djb = d2[pj * K + aj];
+        const double pij = pd[pi][pj];
+        const double approx = dja - dia + dib - djb - wgt * pij;
+        const double margin = 1e-6 * (dja + dia + dib + djb + wgt * pij) + 1e-9;
+        if (approx < -1e-12 + margin) {
+          const double* mua = Mn + ai * D;
+          const double* mub = Mn + aj * D;
+          double delta = 0.0;
+          for (int ch = 0; ch < D; ++ch) {
+            const double xi = xval(X, xs, pi, ch, XS, scaled), xj = xval(X, xs, pj, ch, XS, scaled);
+            const double ma = __dadd_rn(mua[ch], div_n(__dsub_rn(xj, xi), sa));
+            const double mb = __dadd_rn(mub[ch], div_n(__dsub_rn(xi, xj), sb));
+            delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi)),
+                                               __dmul_rn(na, __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua[ch], mua[ch])))));
+            delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj)),
+                                               __dmul_rn(nb, __dsub_rn(__dmul_rn(mb, mb), __dmul_rn(mub[ch], mub[ch])))));
+          }
+          improving = delta < -1e-12;
         }
-        improving = delta < -1e-12;
       }
       const unsigned imp = __ballot_sync(0xffffffffu, improving);
       if (!imp) break;

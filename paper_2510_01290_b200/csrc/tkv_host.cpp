@@ -1511,7 +1511,8 @@ int tkv_gather_create(tkv_ctx* ctx, const tkv_gather_desc* d, tkv_gather** out) 
     st.cap = (int32_t)(d->budget + 1);
     st.in_dtype = d->input_dtype;
     st.in_bytes = d->input_dtype == TKV_DTYPE_BF16 ? 2 : (d->input_dtype == TKV_DTYPE_F32 ? 4 : 8);
-    if (tkv_gather_smem(st) > 200 * 1024) throw TkvError(TKV_ERR_CONFIG, "gather: budget x heads exceeds shared memory");
+    if (tkv_gather_smem(st, d->exact_scores) > 200 * 1024)
+      throw TkvError(TKV_ERR_CONFIG, "gather: budget x heads exceeds shared memory");
     const size_t rows = (size_t)st.U * st.cap;
     CUDA_OK(cudaMalloc(&st.k, rows * st.D * st.in_bytes));
     CUDA_OK(cudaMalloc(&st.v, rows * st.D * st.in_bytes));
@@ -1519,7 +1520,7 @@ int tkv_gather_create(tkv_ctx* ctx, const tkv_gather_desc* d, tkv_gather** out) 
     CUDA_OK(cudaMalloc(&st.victim, (size_t)st.U * sizeof(int32_t)));
     g->log_cap = 256;
     CUDA_OK(cudaMalloc(&g->d_victims_log, (size_t)g->log_cap * st.U * sizeof(int32_t)));
-    CUDA_OK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreate(&g->stream));
     *out = g.release();
     return TKV_OK;
   } catch (const TkvError& e) {

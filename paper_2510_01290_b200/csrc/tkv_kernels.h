@@ -60,6 +60,6 @@ cudaError_t tkv_launch_init(const TkvState& st, cudaStream_t stream);
 
 // Gather-compaction comparator (k_gather.cu): append, attention, head-averaged
 // scores (exact fp64 when `exact`), first-minimum eviction and compaction.
-size_t tkv_gather_smem(const TkvGatherState& g);
+size_t tkv_gather_smem(const TkvGatherState& g, int exact);
 cudaError_t tkv_launch_gather_step(const TkvGatherState& g, int n, int64_t pos, const void* q, const void* k,
                                    const void* v, float* out, int exact, cudaStream_t stream);
