@@ -26,6 +26,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kMaxR = 8;    // query heads per unit (G <= 8)
+constexpr int kMaxCPL = 4;  // channels per lane (d <= 128)
 
 __device__ __forceinline__ float in_f(const void* p, int dtype, int64_t i) {
   if (dtype == TKV_IN_BF16) return __uint_as_float(((uint32_t) reinterpret_cast<const uint16_t*>(p)[i]) << 16);
@@ -36,6 +38,11 @@ __device__ __forceinline__ double in_d(const void* p, int dtype, int64_t i) {
   if (dtype == TKV_IN_BF16) return (double)__uint_as_float(((uint32_t) reinterpret_cast<const uint16_t*>(p)[i]) << 16);
   if (dtype == TKV_IN_F32) return (double)reinterpret_cast<const float*>(p)[i];
   return reinterpret_cast<const double*>(p)[i];
+}
+
+__host__ __device__ inline size_t tkv_gather_smem_main(const TkvGatherState& g, int exact) {
+  const size_t base = (size_t)g.G * g.D * 4 + (size_t)((g.G * g.cap + 1) & ~1) * 4;
+  return (exact ? base + (size_t)g.G * g.D * 8 + (size_t)2 * g.cap * 8 : base + 8) / 16 * 16 + 16;
 }
 
 __device__ __forceinline__ float block_max(float v, float* red) {
@@ -51,6 +58,7 @@ __device__ __forceinline__ float block_max(float v, float* red) {
 // smem: qf [G][D] f32 | lg [G][cap] f32 (logits -> probabilities) | exact
 //       mode only: qd [G][D] f64 | sc [cap] f64 (exact scores of one row) |
 //       avg [cap] f64
+template <int GM>  // query heads rounded up to a power of two (>= G)
 __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g, int n, int64_t pos,
                                                                const void* __restrict__ qin,
                                                                const void* __restrict__ kin,
@@ -66,6 +74,7 @@ __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g,
   double* qd = reinterpret_cast<double*>(lg + (((int64_t)G * cap + 1) & ~1ll));
   double* sc = qd + G * D;     // [cap] exact scores of the current group
   double* avg = sc + cap;      // [cap]
+  uint8_t* pv_red = dyn + tkv_gather_smem_main(g, exact);  // [kWarps][R][D] f32
   __shared__ float redf[kWarps];
   __shared__ double redd[kWarps];
   __shared__ double sum_s;
@@ -83,18 +92,50 @@ __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g,
     if (exact) qd[i] = in_d(qin, g.in_dtype, (int64_t)u * G * D + i);
   }
   __syncthreads();
-  // 2. fp32 attention: logits per head, row max / softmax, outputs
+  // 2. fp32 attention: logits per head (warp per row, lanes over channels:
+  //    coalesced row reads), row max / softmax, outputs (warps over rows,
+  //    lanes over channels, partials merged in warp order)
   const float scale = 1.0f / sqrtf((float)D);
-  for (int i = threadIdx.x; i < rows; i += kThreads) {
-    for (int h = 0; h < G; ++h) {
-      float d = 0.f;
-      for (int c = 0; c < D; ++c) d = fmaf(qf[h * D + c], in_f(kc, g.in_dtype, (int64_t)i * D + c), d);
-      lg[(int64_t)h * cap + i] = d * scale;
-    }
-    if (g.maxpool) {  // gqa_aggregate: max over the G heads (row 0)
-      float mx = lg[i];
-      for (int h = 1; h < G; ++h) mx = fmaxf(mx, lg[(int64_t)h * cap + i]);
-      lg[i] = mx;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kRU = 4;  // rows per warp iteration: their loads are in flight together
+  for (int i0 = warp * kRU; i0 < rows; i0 += kWarps * kRU) {
+    float kx[kRU][kMaxCPL];
+#pragma unroll
+    for (int q = 0; q < kRU; ++q)
+#pragma unroll
+      for (int j = 0; j < kMaxCPL; ++j) {
+        const int c = lane + 32 * j;
+        kx[q][j] = (i0 + q < rows && c < D) ? in_f(kc, g.in_dtype, (int64_t)(i0 + q) * D + c) : 0.f;
+      }
+#pragma unroll
+    for (int q = 0; q < kRU; ++q) {
+      float dh[GM];
+#pragma unroll
+      for (int h = 0; h < GM; ++h) dh[h] = 0.f;
+#pragma unroll
+      for (int j = 0; j < kMaxCPL; ++j) {
+        const int c = lane + 32 * j;
+        if (c >= D) break;
+#pragma unroll
+        for (int h = 0; h < GM; ++h) dh[h] = fmaf(qf[h * D + c], kx[q][j], dh[h]);
+      }
+#pragma unroll
+      for (int h = 0; h < GM; ++h)
+        for (int o = 16; o > 0; o >>= 1) dh[h] += __shfl_xor_sync(0xffffffffu, dh[h], o);
+      const int i = i0 + q;
+      if (lane == 0 && i < rows) {
+        if (g.maxpool) {  // gqa_aggregate: max over the G heads (row 0)
+          float mx = dh[0] * scale;
+#pragma unroll
+          for (int h = 1; h < GM; ++h)
+            if (h < G) mx = fmaxf(mx, dh[h] * scale);
+          lg[i] = mx;
+        } else {
+#pragma unroll
+          for (int h = 0; h < GM; ++h)
+            if (h < G) lg[(int64_t)h * cap + i] = dh[h] * scale;
+        }
+      }
     }
   }
   __syncthreads();
@@ -118,10 +159,50 @@ __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g,
     const float inv = 1.0f / tot;
     for (int i = threadIdx.x; i < rows; i += kThreads) L[i] *= inv;
     __syncthreads();
-    for (int c = threadIdx.x; c < D; c += kThreads) {
+  }
+  {
+    constexpr int RM = GM;  // softmax rows held per lane (>= R)
+    float acc[RM][kMaxCPL];
+#pragma unroll
+    for (int r = 0; r < RM; ++r)
+#pragma unroll
+      for (int j = 0; j < kMaxCPL; ++j) acc[r][j] = 0.f;
+    for (int i0 = warp * kRU; i0 < rows; i0 += kWarps * kRU) {
+      float vx[kRU][kMaxCPL];
+#pragma unroll
+      for (int q = 0; q < kRU; ++q)
+#pragma unroll
+        for (int j = 0; j < kMaxCPL; ++j) {
+          const int c = lane + 32 * j;
+          vx[q][j] = (i0 + q < rows && c < D) ? in_f(vc, g.in_dtype, (int64_t)(i0 + q) * D + c) : 0.f;
+        }
+#pragma unroll
+      for (int q = 0; q < kRU; ++q) {
+        if (i0 + q >= rows) break;
+#pragma unroll
+        for (int r = 0; r < RM; ++r) {
+          if (r >= R) break;
+          const float pr = lg[(int64_t)r * cap + i0 + q];
+#pragma unroll
+          for (int j = 0; j < kMaxCPL; ++j) acc[r][j] = fmaf(pr, vx[q][j], acc[r][j]);
+        }
+      }
+    }
+    float* red = reinterpret_cast<float*>(pv_red);  // [kWarps][R][D]
+#pragma unroll
+    for (int r = 0; r < RM; ++r) {
+      if (r >= R) break;
+#pragma unroll
+      for (int j = 0; j < kMaxCPL; ++j) {
+        const int c = lane + 32 * j;
+        if (c < D) red[((int64_t)warp * R + r) * D + c] = acc[r][j];
+      }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < R * D; idx += kThreads) {
       float o = 0.f;
-      for (int i = 0; i < rows; ++i) o = fmaf(L[i], in_f(vc, g.in_dtype, (int64_t)i * D + c), o);
-      out[((int64_t)u * R + r) * D + c] = o;
+      for (int w = 0; w < kWarps; ++w) o += red[(int64_t)w * R * D + idx];
+      out[(int64_t)u * R * D + idx] = o;
     }
     __syncthreads();
   }
@@ -215,18 +296,25 @@ __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g,
   const int64_t rowb = (int64_t)D * eb;
   const int64_t first = (int64_t)vi * rowb, last = (int64_t)n * rowb;  // destination byte range [first, last)
   if (rowb % 16 == 0) {
-    for (int64_t b0 = first; b0 < last; b0 += (int64_t)kThreads * 16) {
-      const int64_t b = b0 + (int64_t)threadIdx.x * 16;
-      uint4 kk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      const bool act = b < last;
-      if (act) {
-        kk = *reinterpret_cast<const uint4*>(kc + b + rowb);
-        vv = *reinterpret_cast<const uint4*>(vc + b + rowb);
+    constexpr int kU = 8;  // 16-byte words per thread per chunk (32 KB per chunk per array)
+    for (int64_t b0 = first; b0 < last; b0 += (int64_t)kThreads * 16 * kU) {
+      uint4 kk[kU], vv[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const int64_t b = b0 + ((int64_t)j * kThreads + threadIdx.x) * 16;
+        if (b < last) {
+          kk[j] = *reinterpret_cast<const uint4*>(kc + b + rowb);
+          vv[j] = *reinterpret_cast<const uint4*>(vc + b + rowb);
+        }
       }
       __syncthreads();
-      if (act) {
-        *reinterpret_cast<uint4*>(kc + b) = kk;
-        *reinterpret_cast<uint4*>(vc + b) = vv;
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const int64_t b = b0 + ((int64_t)j * kThreads + threadIdx.x) * 16;
+        if (b < last) {
+          *reinterpret_cast<uint4*>(kc + b) = kk[j];
+          *reinterpret_cast<uint4*>(vc + b) = vv[j];
+        }
       }
       __syncthreads();
     }
@@ -254,18 +342,19 @@ __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g,
 }  // namespace
 
 size_t tkv_gather_smem(const TkvGatherState& g, int exact) {
-  const size_t base = (size_t)g.G * g.D * 4 + (size_t)((g.G * g.cap + 1) & ~1) * 4;
-  return exact ? base + (size_t)g.G * g.D * 8 + (size_t)2 * g.cap * 8 : base;
+  return tkv_gather_smem_main(g, exact) + (size_t)kWarps * (g.maxpool ? 1 : g.G) * g.D * 4;
 }
 
 cudaError_t tkv_launch_gather_step(const TkvGatherState& g, int n, int64_t pos, const void* q, const void* k,
                                    const void* v, float* out, int exact, cudaStream_t s) {
   const size_t smem = tkv_gather_smem(g, exact);
-  static bool cfg = false;
-  if (!cfg) {
-    cudaFuncSetAttribute(gather_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cfg = true;
-  }
-  gather_step_kernel<<<g.U, kThreads, smem, s>>>(g, n, pos, q, k, v, out, exact);
-  return cudaGetLastError();
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    kern<<<g.U, kThreads, smem, s>>>(g, n, pos, q, k, v, out, exact);
+    return cudaGetLastError();
+  };
+  if (g.G <= 1) return go(gather_step_kernel<1>);
+  if (g.G <= 2) return go(gather_step_kernel<2>);
+  if (g.G <= 4) return go(gather_step_kernel<4>);
+  return go(gather_step_kernel<8>);
 }

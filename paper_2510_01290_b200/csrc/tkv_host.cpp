@@ -1498,6 +1498,8 @@ int tkv_gather_create(tkv_ctx* ctx, const tkv_gather_desc* d, tkv_gather** out) 
     if (d->num_units < 1 || d->num_q_heads < 1 || d->head_dim < 1 || d->budget < 1)
       throw TkvError(TKV_ERR_CONFIG, "gather: units, heads, head_dim and budget must be positive");
     if (d->input_dtype < 0 || d->input_dtype > 2) throw TkvError(TKV_ERR_CONFIG, "gather: unknown input dtype");
+    if (d->num_q_heads > 8 || d->head_dim > 128)
+      throw TkvError(TKV_ERR_CONFIG, "gather: supports up to 8 query heads per kv head and head_dim <= 128");
     CUDA_OK(cudaSetDevice(ctx->device));
     auto g = std::make_unique<tkv_gather>();
     g->ctx = ctx;
