@@ -109,6 +109,17 @@ int tkv_run_destroy(tkv_run* run);
  * stream: cudaStream_t (NULL = the run's own stream). */
 int tkv_step(tkv_run* run, const void* q, const void* k, const void* v, float* out, void* stream);
 
+/* Layer-by-layer form of tkv_step for a model's decode loop:
+ * a step is num_layers calls, layer = 0 .. num_layers-1 in order, each with
+ * that layer's inputs: q [num_seqs][H][G][d], k/v [num_seqs][H][d], out
+ * [num_seqs][H][rows][d], H = units_per_seq / num_layers kv heads (units are
+ * numbered seq, layer, kv-head).  Each call runs that layer's attention (and,
+ * on refresh steps, its sparsity statistics); the last call also runs the
+ * step's refresh boundary, emission and eviction -- the same state
+ * transitions as one tkv_step with all layers' inputs. */
+int tkv_step_layer(tkv_run* run, int layer, int num_layers, const void* q, const void* k, const void* v,
+                   float* out, void* stream);
+
 /* Same with HOST buffers: copies q/k/v in, steps, copies out back (synchronous). */
 int tkv_step_host(tkv_run* run, const void* q, const void* k, const void* v, float* out);
 

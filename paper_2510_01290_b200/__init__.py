@@ -155,6 +155,13 @@ class DecodeRun:
         s = self._stream(stream)
         check(lib.tkv_step(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), s))
 
+    def step_layer(self, layer: int, num_layers: int, q, k, v, out, stream=None):
+        """One layer of a step (tkv_step_layer): q [seqs,H,G,d], k/v [seqs,H,d],
+        out [seqs,H,rows,d]; call layers 0..num_layers-1 in order."""
+        s = self._stream(stream)
+        check(lib.tkv_step_layer(self._h, layer, num_layers, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                 out.data_ptr(), s))
+
     def step_host(self, q, k, v, out):
         """Same with host (numpy / pinned CPU tensor) buffers, synchronous."""
         ptr = (lambda a: a.ctypes.data) if hasattr(q, "ctypes") else (lambda a: a.data_ptr())

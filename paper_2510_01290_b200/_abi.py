@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libthinkv_b200.so")
 # Every symbol include/thinkv_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "tkv_last_error", "tkv_abi_version", "tkv_init", "tkv_ctx_destroy", "tkv_run_create",
-    "tkv_run_destroy", "tkv_step", "tkv_step_host", "tkv_finish", "tkv_synchronize",
+    "tkv_run_destroy", "tkv_step", "tkv_step_layer", "tkv_step_host", "tkv_finish", "tkv_synchronize",
     "tkv_position", "tkv_dump_json", "tkv_bytes", "tkv_unit_sparsity", "tkv_synth_inputs",
     "tkv_timing_enable", "tkv_timing_read", "tkv_step_host_async",
     "tkv_gather_create", "tkv_gather_destroy", "tkv_gather_step", "tkv_gather_stats", "tkv_gather_ids",
@@ -82,6 +82,7 @@ def _load():
     L.tkv_run_destroy.argtypes = [vp]
     L.tkv_step.argtypes = [vp, vp, vp, vp, vp, vp]
     L.tkv_step_host.argtypes = [vp, vp, vp, vp, vp]
+    L.tkv_step_layer.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp]
     L.tkv_step_host_async.argtypes = [vp, vp, vp, vp, vp]
     L.tkv_finish.argtypes = [vp]
     L.tkv_synchronize.argtypes = [vp]

@@ -226,7 +226,7 @@ __device__ __forceinline__ void paged_tile(const TkvState& st, int u, const int*
 
 // Tail tile: buffered tokens [0, nbuf) and the current token (index nbuf).
 template <int CPL, int GM>
-__device__ __forceinline__ void input_tile(const TkvState& st, int u, int t0, int n, int nbuf, int buf_half,
+__device__ __forceinline__ void input_tile(const TkvState& st, int u, int li, int t0, int n, int nbuf, int buf_half,
                                            const void* kin, const void* vin, const float* qs,
                                            WarpState<CPL, GM>& ws) {
   const TkvDims& dm = st.dm;
@@ -242,7 +242,7 @@ __device__ __forceinline__ void input_tile(const TkvState& st, int u, int t0, in
   for (int g = 0; g < GM; ++g) dot[g] = 0.0f;
   if (valid) {
     const void* kp = t < nbuf ? (const void*)(bk + (int64_t)t * D * dm.in_bytes)
-                              : (const void*)((const uint8_t*)kin + (int64_t)u * D * dm.in_bytes);
+                              : (const void*)((const uint8_t*)kin + (int64_t)li * D * dm.in_bytes);
     for (int ch = 0; ch < D; ++ch) {
       const float kv = in_f(kp, dm.in_dtype, ch);
 #pragma unroll
@@ -265,7 +265,7 @@ __device__ __forceinline__ void input_tile(const TkvState& st, int u, int t0, in
   for (int j = 0; j < n; ++j) {
     const int tj = t0 + j;
     const void* vp = tj < nbuf ? (const void*)(bv + (int64_t)tj * D * dm.in_bytes)
-                               : (const void*)((const uint8_t*)vin + (int64_t)u * D * dm.in_bytes);
+                               : (const void*)((const uint8_t*)vin + (int64_t)li * D * dm.in_bytes);
     float pj[GM];
 #pragma unroll
     for (int r = 0; r < GM; ++r) pj[r] = __shfl_sync(0xffffffffu, p[r], j);
@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(kThreads) attend_kernel(TkvState st, const voi
                                                           const void* __restrict__ vin, float* __restrict__ out,
                                                           int buf_half, int nbuf, int put_half, int put_slot) {
   const TkvDims& dm = st.dm;
-  const int u = blockIdx.x;
+  const int li = blockIdx.x;             // launch-local index: q/k/v/out rows
+  const int u = tkv_unit_of(st, li);     // unit: cache state
   const int D = dm.D, G = dm.G, R = dm.maxpool ? 1 : G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   extern __shared__ __align__(16) uint8_t dyn[];
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(kThreads) attend_kernel(TkvState st, const voi
 
   const float qscale = dm.scale * kLog2e;  // logits in the log2 domain
   for (int i = threadIdx.x; i < G * D; i += kThreads)
-    qs[i] = in_f(qin, dm.in_dtype, (int64_t)u * G * D + i) * qscale;
+    qs[i] = in_f(qin, dm.in_dtype, (int64_t)li * G * D + i) * qscale;
   build_live_list(st, u, list, cnt, off, scan);  // ends with __syncthreads
 
   WarpState<CPL, GM> ws;
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(kThreads) attend_kernel(TkvState st, const voi
       }
     } else {
       const int n = min(32, nbuf + 1 - tt * 32);
-      input_tile<CPL, GM>(st, u, tt * 32, n, nbuf, buf_half, kin, vin, qs, ws);
+      input_tile<CPL, GM>(st, u, li, tt * 32, n, nbuf, buf_half, kin, vin, qs, ws);
     }
   }
   // Merge the warps' partial softmax states.
@@ -360,15 +361,15 @@ __global__ void __launch_bounds__(kThreads) attend_kernel(TkvState st, const voi
       Lsum += rr[1] * f;
       O += rr[2 + ch] * f;
     }
-    out[((int64_t)u * R + r) * D + ch] = O / Lsum;
+    out[((int64_t)li * R + r) * D + ch] = O / Lsum;
   }
   // Buffer the incoming token for the next emission (sim.cpp:796-808).
   if (put_slot >= 0) {
     const int64_t row = (int64_t)dm.g * D * dm.in_bytes;
     uint8_t* bk = st.buf + ((int64_t)u * 4 + put_half * 2 + 0) * row + (int64_t)put_slot * D * dm.in_bytes;
     uint8_t* bv = st.buf + ((int64_t)u * 4 + put_half * 2 + 1) * row + (int64_t)put_slot * D * dm.in_bytes;
-    const uint8_t* ks = (const uint8_t*)kin + (int64_t)u * D * dm.in_bytes;
-    const uint8_t* vs = (const uint8_t*)vin + (int64_t)u * D * dm.in_bytes;
+    const uint8_t* ks = (const uint8_t*)kin + (int64_t)li * D * dm.in_bytes;
+    const uint8_t* vs = (const uint8_t*)vin + (int64_t)li * D * dm.in_bytes;
     for (int i = threadIdx.x; i < D * dm.in_bytes; i += kThreads) {
       bk[i] = ks[i];
       bv[i] = vs[i];
@@ -387,7 +388,7 @@ cudaError_t launch_attend_t(const TkvState& st, const void* q, const void* k, co
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
-  kern<<<st.dm.U, kThreads, smem, s>>>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot);
+  kern<<<tkv_launch_units(st), kThreads, smem, s>>>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot);
   return cudaGetLastError();
 }
 

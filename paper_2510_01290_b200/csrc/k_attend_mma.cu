@@ -475,7 +475,8 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st,
                                                                   float* __restrict__ out, int buf_half, int nbuf,
                                                                   int put_half, int put_slot) {
   const TkvDims& dm = st.dm;
-  const int u = blockIdx.x;
+  const int li = blockIdx.x;            // launch-local index: q/k/v/out rows
+  const int u = tkv_unit_of(st, li);    // unit: cache state
   const int G = dm.G, R = dm.maxpool ? 1 : G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gid = lane >> 2, tig = lane & 3;
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st,
   // registers, the raw bf16 words in shared memory for the bf16 tiles.
   uint32_t qb[D / 16][2];
   {
-    const uint16_t* qq = reinterpret_cast<const uint16_t*>(qin) + ((int64_t)u * G + gid) * D + tig * (D / 4);
+    const uint16_t* qq = reinterpret_cast<const uint16_t*>(qin) + ((int64_t)li * G + gid) * D + tig * (D / 4);
     uint32_t* qbb = qbb_all + lane * (D / 8);
 #pragma unroll
     for (int j = 0; j < D / 16; ++j) {
@@ -597,8 +598,8 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st,
     const int64_t row = (int64_t)dm.g * D * 2;
     up.bk = st.buf + ((int64_t)u * 4 + buf_half * 2 + 0) * row;
     up.bv = st.buf + ((int64_t)u * 4 + buf_half * 2 + 1) * row;
-    up.kc = reinterpret_cast<const uint8_t*>(kin) + (int64_t)u * D * 2;
-    up.vc = reinterpret_cast<const uint8_t*>(vin) + (int64_t)u * D * 2;
+    up.kc = reinterpret_cast<const uint8_t*>(kin) + (int64_t)li * D * 2;
+    up.vc = reinterpret_cast<const uint8_t*>(vin) + (int64_t)li * D * 2;
     up.nbuf = nbuf;
     up.vsel = (gid * (D / 8)) / dm.g;
   }
@@ -658,14 +659,14 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st,
       Ls += rr[1] * f;
       O += rr[2 + ch] * f;
     }
-    out[((int64_t)u * R + r) * D + ch] = O / Ls;
+    out[((int64_t)li * R + r) * D + ch] = O / Ls;
   }
   if (put_slot >= 0) {  // buffer the incoming token (sim.cpp:796-808)
     const int64_t row = (int64_t)dm.g * D;
     uint16_t* bk = reinterpret_cast<uint16_t*>(st.buf) + ((int64_t)u * 4 + put_half * 2 + 0) * row + (int64_t)put_slot * D;
     uint16_t* bv = reinterpret_cast<uint16_t*>(st.buf) + ((int64_t)u * 4 + put_half * 2 + 1) * row + (int64_t)put_slot * D;
-    const uint16_t* ks = reinterpret_cast<const uint16_t*>(kin) + (int64_t)u * D;
-    const uint16_t* vs = reinterpret_cast<const uint16_t*>(vin) + (int64_t)u * D;
+    const uint16_t* ks = reinterpret_cast<const uint16_t*>(kin) + (int64_t)li * D;
+    const uint16_t* vs = reinterpret_cast<const uint16_t*>(vin) + (int64_t)li * D;
     for (int i = threadIdx.x; i < D; i += kThreads) {
       bk[i] = ks[i];
       bv[i] = vs[i];
@@ -776,8 +777,8 @@ __device__ __forceinline__ void run_format3(const UnitPtrs& up, const uint16_t* 
 template <int D>
 struct WarpSmem {
   static constexpr int kQbb = 32 * (D / 8);  // u32: bf16 q fragments
-  static __host__ __device__ size_t bytes(int NS, int g, int P) {
-    const size_t lst = ((size_t)(NS + g + 1 + 4 * 16) * 2 + 15) / 16 * 16;
+  static __host__ __device__ size_t bytes(int live_cap, int g, int P) {
+    const size_t lst = ((size_t)(live_cap + g + 1 + 4 * 16) * 2 + 15) / 16 * 16;
     return (size_t)kQbb * 4 + 128 * 4 + (size_t)P * 8 + lst;
   }
 };
@@ -790,13 +791,14 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
                                                                     int put_half, int put_slot) {
   const TkvDims& dm = st.dm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int u = blockIdx.x * kWarps + warp;
-  if (u >= dm.U) return;
+  const int li = blockIdx.x * kWarps + warp;  // launch-local index: q/k/v/out rows
+  if (li >= tkv_launch_units(st)) return;
+  const int u = tkv_unit_of(st, li);          // unit: cache state
   const int G = dm.G, R = dm.maxpool ? 1 : G;
   const int gid = lane >> 2, tig = lane & 3;
   const int P = dm.P, bs = dm.bs, NS = dm.NS;
   extern __shared__ __align__(16) uint8_t dyn[];
-  uint8_t* mine = dyn + (size_t)warp * WarpSmem<D>::bytes(NS, dm.g, P);
+  uint8_t* mine = dyn + (size_t)warp * WarpSmem<D>::bytes(st.max_live, dm.g, P);
   uint32_t* qbb = reinterpret_cast<uint32_t*>(mine) + lane * (D / 8);
   float* ps = reinterpret_cast<float*>(mine + WarpSmem<D>::kQbb * 4);
   int2* binfo = reinterpret_cast<int2*>(mine + WarpSmem<D>::kQbb * 4 + 128 * 4);
@@ -805,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
 
   uint32_t qb[D / 16][2];
   {
-    const uint16_t* qq = reinterpret_cast<const uint16_t*>(qin) + ((int64_t)u * G + gid) * D + tig * (D / 4);
+    const uint16_t* qq = reinterpret_cast<const uint16_t*>(qin) + ((int64_t)li * G + gid) * D + tig * (D / 4);
 #pragma unroll
     for (int j = 0; j < D / 16; ++j) {
       uint2 w = make_uint2(0u, 0u);
@@ -850,6 +852,10 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
       w[f] = run + x - c[f];
       run += (tot + 15) & ~15;  // padded to whole tiles
     }
+    if (run > st.max_live + dm.g + 1 + 4 * 16) {  // host bookkeeping disagrees with the block table
+      if (lane == 0) st.err[u] = TKV_E_INTEGRITY;
+      return;
+    }
   }
   for (int b = b0; b < b1; ++b) {
     const int2 bi = binfo[b];
@@ -892,8 +898,8 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
     up.bk = st.buf + ((int64_t)u * 4 + buf_half * 2 + 0) * row;
     up.bv = st.buf + ((int64_t)u * 4 + buf_half * 2 + 1) * row;
   }
-  up.kc = reinterpret_cast<const uint8_t*>(kin) + (int64_t)u * D * 2;
-  up.vc = reinterpret_cast<const uint8_t*>(vin) + (int64_t)u * D * 2;
+  up.kc = reinterpret_cast<const uint8_t*>(kin) + (int64_t)li * D * 2;
+  up.vc = reinterpret_cast<const uint8_t*>(vin) + (int64_t)li * D * 2;
   up.nbuf = nbuf;
   up.vsel = (gid * (D / 8)) / dm.g;
   Acc<D> A;
@@ -917,7 +923,7 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
     const int h = tig * 2 + cc;
     if (h >= R) continue;
     const float inv = 1.0f / A.l[cc];
-    float* o = out + ((int64_t)u * R + h) * D + gid * (D / 8);
+    float* o = out + ((int64_t)li * R + h) * D + gid * (D / 8);
 #pragma unroll
     for (int mt = 0; mt < D / 16; ++mt)
       *reinterpret_cast<float2*>(o + 2 * mt) = make_float2(A.o[mt][cc] * inv, A.o[mt][2 + cc] * inv);
@@ -926,8 +932,8 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
     const int64_t row = (int64_t)dm.g * D;
     uint16_t* bk = reinterpret_cast<uint16_t*>(st.buf) + ((int64_t)u * 4 + put_half * 2 + 0) * row + (int64_t)put_slot * D;
     uint16_t* bv = reinterpret_cast<uint16_t*>(st.buf) + ((int64_t)u * 4 + put_half * 2 + 1) * row + (int64_t)put_slot * D;
-    const uint16_t* ks = reinterpret_cast<const uint16_t*>(kin) + (int64_t)u * D;
-    const uint16_t* vs = reinterpret_cast<const uint16_t*>(vin) + (int64_t)u * D;
+    const uint16_t* ks = reinterpret_cast<const uint16_t*>(kin) + (int64_t)li * D;
+    const uint16_t* vs = reinterpret_cast<const uint16_t*>(vin) + (int64_t)li * D;
     for (int i = lane; i < D; i += 32) {
       bk[i] = ks[i];
       bv[i] = vs[i];
@@ -952,20 +958,20 @@ cudaError_t launch_k1(const TkvState& st, const void* q, const void* k, const vo
     cudaFuncSetAttribute(attend_mma_kernel<D, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cfg = true;
   }
-  attend_mma_kernel<D, MINB><<<st.dm.U, kThreads, smem, s>>>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot);
+  attend_mma_kernel<D, MINB><<<tkv_launch_units(st), kThreads, smem, s>>>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot);
   return cudaGetLastError();
 }
 
 template <int D, int MINB>
 cudaError_t launch_k1_warp(const TkvState& st, const void* q, const void* k, const void* v, float* out, int buf_half,
                            int nbuf, int put_half, int put_slot, cudaStream_t s) {
-  const size_t smem = (size_t)kWarps * WarpSmem<D>::bytes(st.dm.NS, st.dm.g, st.dm.P);
+  const size_t smem = (size_t)kWarps * WarpSmem<D>::bytes(st.max_live, st.dm.g, st.dm.P);
   static bool cfg = false;
   if (!cfg) {
     cudaFuncSetAttribute(attend_warp_kernel<D, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cfg = true;
   }
-  attend_warp_kernel<D, MINB><<<(st.dm.U + kWarps - 1) / kWarps, kThreads, smem, s>>>(st, q, k, v, out, buf_half,
+  attend_warp_kernel<D, MINB><<<(tkv_launch_units(st) + kWarps - 1) / kWarps, kThreads, smem, s>>>(st, q, k, v, out, buf_half,
                                                                                      nbuf, put_half, put_slot);
   return cudaGetLastError();
 }
@@ -976,8 +982,8 @@ cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void*
   // v3 (warp per unit, u16 slot lists) whenever slot ids fit in 16 bits and
   // the per-warp lists fit in shared memory; v2 (CTA per unit) otherwise.
   const bool v3 = st.dm.NS + st.dm.g + 1 + 4 * 16 < 65536 &&
-                  (size_t)kWarps * (D == 128 ? WarpSmem<128>::bytes(st.dm.NS, st.dm.g, st.dm.P)
-                                             : WarpSmem<64>::bytes(st.dm.NS, st.dm.g, st.dm.P)) <= 200 * 1024 &&
+                  (size_t)kWarps * (D == 128 ? WarpSmem<128>::bytes(st.max_live, st.dm.g, st.dm.P)
+                                             : WarpSmem<64>::bytes(st.max_live, st.dm.g, st.dm.P)) <= 200 * 1024 &&
                   getenv("TKV_K1_V2") == nullptr;
   if (v3) {
     if (D == 128) return launch_k1_warp<128, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);

@@ -77,15 +77,17 @@ __device__ __forceinline__ void dots(const double* __restrict__ qd, int D, int g
 
 template <int NC, bool VEC>
 __global__ void __launch_bounds__(kThreads) score_kernel(TkvState st, const void* __restrict__ qin,
-                                                         const void* __restrict__ kin, int buf_half, int nbuf) {
+                                                         const void* __restrict__ kin, int buf_half, int nbuf,
+                                                         int rp) {
   const TkvDims& dm = st.dm;
-  const int u = blockIdx.x;
+  const int li = blockIdx.x;          // launch-local index: q/k rows
+  const int u = tkv_unit_of(st, li);  // unit: cache state
   const int D = dm.D, G = dm.G, P = dm.P, bs = dm.bs;
-  const int nmax = dm.NS + dm.g + 1;
+  const int nmax = st.max_live + dm.g + 1;  // live slots + buffer + current token
   extern __shared__ __align__(16) uint8_t dyn[];
-  double* lg = reinterpret_cast<double*>(dyn);                 // [kRows][nmax]
-  double* qd = lg + (int64_t)kRows * nmax;                      // [G][D]
-  int* list = reinterpret_cast<int*>(qd + (int64_t)G * D);      // [NS]
+  double* lg = reinterpret_cast<double*>(dyn);                 // [rp][nmax]
+  double* qd = lg + (int64_t)rp * nmax;                         // [G][D]
+  int* list = reinterpret_cast<int*>(qd + (int64_t)G * D);      // [max_live]
   __shared__ int scan[kThreads];
   __shared__ double red[kWarps][kRows];
   __shared__ double rowsum[kRows];
@@ -110,15 +112,22 @@ __global__ void __launch_bounds__(kThreads) score_kernel(TkvState st, const void
   }
   if (lane == 31) scan[warp] = incl;
   for (int i = threadIdx.x; i < G * D; i += kThreads) {
-    const int64_t gi = (int64_t)u * G * D + i;
+    const int64_t gi = (int64_t)li * G * D + i;
     qd[i] = dm.in_dtype == TKV_IN_BF16
                 ? (double)__uint_as_float(((uint32_t) reinterpret_cast<const uint16_t*>(qin)[gi]) << 16)
                 : (dm.in_dtype == TKV_IN_F32 ? (double)reinterpret_cast<const float*>(qin)[gi]
                                              : reinterpret_cast<const double*>(qin)[gi]);
   }
   __syncthreads();
-  int before = 0;
-  for (int w = 0; w < warp; ++w) before += scan[w];
+  int before = 0, total_live = 0;
+  for (int w = 0; w < kWarps; ++w) {
+    if (w < warp) before += scan[w];
+    total_live += scan[w];
+  }
+  if (total_live > st.max_live) {  // host bookkeeping disagrees with the block table
+    if (threadIdx.x == 0) st.err[u] = TKV_E_INTEGRITY;
+    return;
+  }
   if (threadIdx.x == kThreads - 1) s_nlive = before + incl;
   {
     int w = before + incl - c;
@@ -140,11 +149,11 @@ __global__ void __launch_bounds__(kThreads) score_kernel(TkvState st, const void
   const double scale = 1.0 / sqrt((double)D);
   const int64_t brow = (int64_t)dm.g * D * dm.in_bytes;
   const uint8_t* bk = st.buf + ((int64_t)u * 4 + buf_half * 2 + 0) * brow;
-  const uint8_t* kc = reinterpret_cast<const uint8_t*>(kin) + (int64_t)u * D * dm.in_bytes;
+  const uint8_t* kc = reinterpret_cast<const uint8_t*>(kin) + (int64_t)li * D * dm.in_bytes;
   double total = 0.0;
 
-  for (int r0 = 0; r0 < rows; r0 += kRows) {
-    const int nr = min(kRows, rows - r0);
+  for (int r0 = 0; r0 < rows; r0 += rp) {
+    const int nr = min(rp, rows - r0);
     // ---- logits of rows r0 .. r0 + nr ------------------------------------------
     // max-pool: one row from all G heads; per-head: heads r0 .. r0 + nr.
     const int g0 = mp ? 0 : r0;
@@ -287,23 +296,23 @@ __global__ void __launch_bounds__(kThreads) score_kernel(TkvState st, const void
 }
 
 template <int NC, bool VEC>
-cudaError_t launch_t(const TkvState& st, const void* q, const void* k, int buf_half, int nbuf, size_t smem,
+cudaError_t launch_t(const TkvState& st, const void* q, const void* k, int buf_half, int nbuf, size_t smem, int rp,
                      cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(score_kernel<NC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
-  score_kernel<NC, VEC><<<st.dm.U, kThreads, smem, s>>>(st, q, k, buf_half, nbuf);
+  score_kernel<NC, VEC><<<tkv_launch_units(st), kThreads, smem, s>>>(st, q, k, buf_half, nbuf, rp);
   return cudaGetLastError();
 }
 
 template <int NC>
-cudaError_t launch_nc(const TkvState& st, const void* q, const void* k, int buf_half, int nbuf, size_t smem,
+cudaError_t launch_nc(const TkvState& st, const void* q, const void* k, int buf_half, int nbuf, size_t smem, int rp,
                       cudaStream_t s) {
   // 8-channel vector loads need D % 8 == 0 (row and scale-row alignment follows)
-  if (st.dm.D % 8 == 0) return launch_t<NC, true>(st, q, k, buf_half, nbuf, smem, s);
-  return launch_t<NC, false>(st, q, k, buf_half, nbuf, smem, s);
+  if (st.dm.D % 8 == 0) return launch_t<NC, true>(st, q, k, buf_half, nbuf, smem, rp, s);
+  return launch_t<NC, false>(st, q, k, buf_half, nbuf, smem, rp, s);
 }
 
 }  // namespace
@@ -311,12 +320,18 @@ cudaError_t launch_nc(const TkvState& st, const void* q, const void* k, int buf_
 cudaError_t tkv_launch_score(const TkvState& st, const void* q, const void* k, int buf_half, int nbuf,
                              cudaStream_t s) {
   const TkvDims& dm = st.dm;
-  const size_t smem = (size_t)kRows * (dm.NS + dm.g + 1) * 8 + (size_t)dm.G * dm.D * 8 + (size_t)dm.NS * 4;
-  // chains per key and pass: all G heads for max-pool rows, else up to kRows heads
-  const int nc = dm.maxpool ? dm.G : (dm.G < kRows ? dm.G : kRows);
-  if (nc <= 1) return launch_nc<1>(st, q, k, buf_half, nbuf, smem, s);
-  if (nc <= 2) return launch_nc<2>(st, q, k, buf_half, nbuf, smem, s);
-  if (nc <= 4) return launch_nc<4>(st, q, k, buf_half, nbuf, smem, s);
-  if (nc <= 8) return launch_nc<8>(st, q, k, buf_half, nbuf, smem, s);
-  return launch_nc<16>(st, q, k, buf_half, nbuf, smem, s);
+  // rows per pass: as many softmax rows as fit next to q and the live list
+  const size_t nmax = (size_t)st.max_live + dm.g + 1;
+  const size_t fixed = (size_t)dm.G * dm.D * 8 + (size_t)st.max_live * 4;
+  int rp = kRows;
+  while (rp > 1 && (size_t)rp * nmax * 8 + fixed > 200 * 1024) --rp;
+  const size_t smem = (size_t)rp * nmax * 8 + fixed;
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // > ~24K live slots per unit
+  // chains per key and pass: all G heads for max-pool rows, else up to rp heads
+  const int nc = dm.maxpool ? dm.G : (dm.G < rp ? dm.G : rp);
+  if (nc <= 1) return launch_nc<1>(st, q, k, buf_half, nbuf, smem, rp, s);
+  if (nc <= 2) return launch_nc<2>(st, q, k, buf_half, nbuf, smem, rp, s);
+  if (nc <= 4) return launch_nc<4>(st, q, k, buf_half, nbuf, smem, rp, s);
+  if (nc <= 8) return launch_nc<8>(st, q, k, buf_half, nbuf, smem, rp, s);
+  return launch_nc<16>(st, q, k, buf_half, nbuf, smem, rp, s);
 }

@@ -201,6 +201,12 @@ struct tkv_run {
   cudaStream_t d2h_stream = nullptr;   // downloads (separate, so step t's download never delays step t+1's upload)
   cudaEvent_t h2d_done[2]{}, step_done[2]{}, d2h_done[2]{};
   int hslot = 0;
+  // layer-by-layer stepping (tkv_step_layer): the open step, next expected layer
+  int next_layer = 0;
+  int step_layers = 0;
+  int64_t open_pos = -1;
+  bool open_decode = false, open_refresh = false;
+  int open_put_half = 0, open_put_slot = 0;
   std::vector<void*> allocations;
 };
 
@@ -937,29 +943,61 @@ json metrics_json(tkv_run* r, const Group& g, const std::vector<UnitSnap>& snaps
   return m;
 }
 
-// the step (ThinkvMethod::process, sim.cpp:748-843)
-void do_step(tkv_run* r, const void* q, const void* k, const void* v, float* out) {
+// the step (ThinkvMethod::process, sim.cpp:748-843), in three parts so a model
+// can run the attention layer by layer (tkv_step_layer):
+//   step_begin   phase bookkeeping, refresh/put decisions, live-list bound
+//   step_attend  K3a (refresh steps) + K1 for all units or one layer's units
+//   step_end     boundary, buffering, emission, Case-2 eviction, dumps
+struct StepCtx {
+  int64_t pos = 0;
+  bool decode = false, refresh = false;
+  int put_half = 0, put_slot = 0;
+};
+
+StepCtx step_begin(tkv_run* r) {
   const tkv_run_desc& d = r->desc;
   if (r->finished) throw TkvError(TKV_ERR_CONFIG, "run already finished");
   if (r->pos >= r->total_steps) throw TkvError(TKV_ERR_CONFIG, "step beyond prompt_len + max_gen_len");
   begin_phase(r);
   if (!d.record_events) r->log_used = 0;
-  const int64_t pos = r->pos;
-  const bool decode = pos >= d.prompt_len;
-  const int64_t bstep = decode ? pos - d.prompt_len : pos;
-  const bool refresh = bstep % d.tau == 0;
-  const bool flush_first = refresh && r->buf_len > 0;
-  const int put_half = flush_first ? (r->cur_half ^ 1) : r->cur_half;
-  const int put_slot = flush_first ? 0 : r->buf_len;
+  StepCtx c;
+  c.pos = r->pos;
+  c.decode = c.pos >= d.prompt_len;
+  const int64_t bstep = c.decode ? c.pos - d.prompt_len : c.pos;
+  c.refresh = bstep % d.tau == 0;
+  const bool flush_first = c.refresh && r->buf_len > 0;
+  c.put_half = flush_first ? (r->cur_half ^ 1) : r->cur_half;
+  c.put_slot = flush_first ? 0 : r->buf_len;
+  // live pager slots per unit = the sequence's segment members minus its buffered tokens
+  int64_t mx = 0;
+  for (const Group& g : r->groups) mx = std::max(mx, g.total - (int64_t)r->buf_len);
+  r->st.max_live = (int32_t)std::min<int64_t>(mx, r->st.dm.NS);
+  return c;
+}
+
+// lmap_h > 0: the launch covers layer `layer` only (q/k/v/out hold that layer's
+// num_seqs x lmap_h units); lmap_h == 0: every unit.
+void step_attend(tkv_run* r, const StepCtx& c, const void* q, const void* k, const void* v, float* out,
+                 int lmap_h, int layer) {
+  r->st.lmap_h = lmap_h;
+  r->st.lmap_ups = r->desc.units_per_seq;
+  r->st.lmap_off = layer * lmap_h;
+  r->st.lmap_count = r->desc.num_seqs * lmap_h;
   // 1. attention (+ exact sparsity on refresh steps, where it is consumed)
-  if (refresh && decode)
+  if (c.refresh && c.decode)
     launch(r, CAT_SCORE, "score kernel",
            [&] { return tkv_launch_score(r->st, q, k, r->cur_half, r->buf_len, r->stream); });
   launch(r, CAT_ATTEND, "attend kernel", [&] {
-    return tkv_launch_attend(r->st, q, k, v, out, r->cur_half, r->buf_len, put_half, put_slot, r->stream);
+    return tkv_launch_attend(r->st, q, k, v, out, r->cur_half, r->buf_len, c.put_half, c.put_slot, r->stream);
   });
+  r->st.lmap_h = 0;
+}
+
+void step_end(tkv_run* r, const StepCtx& c) {
+  const tkv_run_desc& d = r->desc;
+  const int64_t pos = c.pos;
   // 2. refresh boundary
-  if (refresh) boundary(r, pos, decode);
+  if (c.refresh) boundary(r, pos, c.decode);
   // 3. buffer the token under the open segment
   if (r->buf_len == 0) r->buf_pos0 = pos;
   r->buf_len += 1;
@@ -968,12 +1006,12 @@ void do_step(tkv_run* r, const void* q, const void* k, const void* v, float* out
     open.size += 1;
     open.initial += 1;
     g.total += 1;
-    if (decode) g.gen_by_thought[thought_name(open.band, d.num_thoughts)] += 1;
+    if (c.decode) g.gen_by_thought[thought_name(open.band, d.num_thoughts)] += 1;
   }
   // 4. emission at g tokens
   if (r->buf_len >= d.group_size) flush_all(r, pos);
   // 5. Case-2 budget enforcement
-  overflow_pass(r, pos, decode, false);
+  overflow_pass(r, pos, c.decode, false);
   end_phase(r);
   if (r->dump_at.count(pos)) {
     check_device_errors(r);
@@ -984,6 +1022,13 @@ void do_step(tkv_run* r, const void* q, const void* k, const void* v, float* out
     }
   }
   r->pos += 1;
+}
+
+void do_step(tkv_run* r, const void* q, const void* k, const void* v, float* out) {
+  if (r->next_layer != 0) throw TkvError(TKV_ERR_CONFIG, "a layer-by-layer step is open (tkv_step_layer)");
+  const StepCtx c = step_begin(r);
+  step_attend(r, c, q, k, v, out, 0, 0);
+  step_end(r, c);
 }
 
 void do_finish(tkv_run* r) {
@@ -1081,6 +1126,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   st.buf = dalloc<uint8_t>(r, U * 4 * (size_t)dm.g * dm.D * dm.in_bytes, 0);
   st.sparsity = dalloc<double>(r, U);
   st.kstats = nullptr;
+  st.max_live = st.dm.NS;
   if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 32, 0);
   st.err = dalloc<int32_t>(r, U);
   check_launch(tkv_launch_init(st, r->stream), "init kernel");
@@ -1297,6 +1343,57 @@ void step_host_async(tkv_run* run, const void* q, const void* k, const void* v, 
   CUDA_OK(cudaStreamWaitEvent(run->d2h_stream, run->step_done[sl], 0));
   CUDA_OK(cudaMemcpyAsync(out, run->d_out[sl], ob, cudaMemcpyDeviceToHost, run->d2h_stream));
   CUDA_OK(cudaEventRecord(run->d2h_done[sl], run->d2h_stream));
+}
+
+int tkv_step_layer(tkv_run* run, int layer, int num_layers, const void* q, const void* k, const void* v, float* out,
+                   void* stream) {
+  try {
+    const tkv_run_desc& d = run->desc;
+    if (num_layers < 1 || d.units_per_seq % num_layers != 0)
+      throw TkvError(TKV_ERR_CONFIG, "num_layers must divide units_per_seq");
+    if (layer != run->next_layer || (layer > 0 && num_layers != run->step_layers))
+      throw TkvError(TKV_ERR_CONFIG, "layers of a step must be stepped in order 0 .. num_layers-1");
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaEvent_t ev = nullptr;
+    if (user && user != run->stream) {
+      CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CUDA_OK(cudaEventRecord(ev, user));
+      CUDA_OK(cudaStreamWaitEvent(run->stream, ev, 0));
+    }
+    StepCtx c;
+    if (layer == 0) {
+      c = step_begin(run);
+      run->open_pos = c.pos;
+      run->open_decode = c.decode;
+      run->open_refresh = c.refresh;
+      run->open_put_half = c.put_half;
+      run->open_put_slot = c.put_slot;
+      run->step_layers = num_layers;
+    } else {
+      c.pos = run->open_pos;
+      c.decode = run->open_decode;
+      c.refresh = run->open_refresh;
+      c.put_half = run->open_put_half;
+      c.put_slot = run->open_put_slot;
+    }
+    step_attend(run, c, q, k, v, out, d.units_per_seq / num_layers, layer);
+    if (layer == num_layers - 1) {
+      step_end(run, c);
+      run->next_layer = 0;
+    } else {
+      run->next_layer = layer + 1;
+    }
+    if (ev) {
+      CUDA_OK(cudaEventRecord(ev, run->stream));
+      CUDA_OK(cudaStreamWaitEvent(user, ev, 0));
+      CUDA_OK(cudaEventDestroy(ev));
+    }
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
 }
 
 int tkv_step_host(tkv_run* run, const void* q, const void* k, const void* v, float* out) {

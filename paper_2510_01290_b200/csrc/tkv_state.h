@@ -90,7 +90,21 @@ struct TkvState {
   double* sparsity;      // [U]
   unsigned long long* kstats;  // optional K-means counters (TKV_KSTATS=1), else null
   int32_t* err;          // [U]
+  // Upper bound on live pager slots of any unit at the next attention launch
+  // (host-exact: every unit of a sequence holds its segments' total members
+  // minus the buffered tokens).  Sizes the per-unit live lists in shared memory.
+  int32_t max_live;
+  // Launch-local index i -> unit (per-layer stepping, tkv_step_layer): units
+  // of one layer are strided in the sequence-major unit order, so a layer
+  // launch covers i in [0, num_seqs * lmap_h) and
+  // u = (i / lmap_h) * lmap_ups + lmap_off + i % lmap_h.  lmap_h == 0: u = i.
+  int32_t lmap_h, lmap_ups, lmap_off, lmap_count;
 };
+
+__host__ __device__ inline int tkv_unit_of(const TkvState& st, int i) {
+  return st.lmap_h ? (i / st.lmap_h) * st.lmap_ups + st.lmap_off + i % st.lmap_h : i;
+}
+__host__ __device__ inline int tkv_launch_units(const TkvState& st) { return st.lmap_h ? st.lmap_count : st.dm.U; }
 
 // Per-group (sequence) control values for an emission (flush).
 struct TkvFlushCtl {

@@ -175,3 +175,35 @@ def test_parity_generic_kmeans_for_tiny_instances(monkeypatch):
     cfg = CONFIGS["llama_shape"]
     res = run_parity(cfg, check_every=5)
     compare_state(res, cfg)
+
+
+@pytest.mark.parametrize("maxpool", [False, True])
+def test_layer_by_layer_stepping_matches_full_steps(maxpool):
+    """tkv_step_layer (a model's per-layer decode loop) gives bit-identical
+    outputs and cache state to whole-step tkv_step on the same inputs."""
+    L, H, S, G, D = 3, 2, 2, 4, 128
+    cfg = ThinkvConfig(num_seqs=S, units_per_seq=L * H, num_q_heads=G, gqa_maxpool=maxpool, head_dim=D, tau=32,
+                       group_size=16, block_size=16, budget=80, levels=(16, 8, 4), max_gen_len=300,
+                       script=script(S, 12, seed=11), record_events=True)
+    dev = torch.device("cuda:0")
+    a, b = DecodeRun(cfg), DecodeRun(cfg)
+    rows = cfg.out_rows
+    out_a = torch.empty((cfg.units, rows, D), device=dev)
+    out_b = torch.empty((S, L, H, rows, D), device=dev)
+    for t in range(cfg.max_gen_len):
+        q, k, v = O.synth_step(0x71534B56, cfg.units_per_seq, cfg.tau, cfg.units, G, D, t)
+        tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev) for x in (q, k, v))
+        a.step(tq, tk, tv, out_a)
+        q5, k5, v5 = tq.view(S, L, H, G, D), tk.view(S, L, H, D), tv.view(S, L, H, D)
+        for l in range(L):
+            ol = torch.empty((S, H, rows, D), device=dev)
+            b.step_layer(l, L, q5[:, l].contiguous(), k5[:, l].contiguous(), v5[:, l].contiguous(), ol)
+            out_b[:, l] = ol
+        assert torch.equal(out_b.reshape(cfg.units, rows, D), out_a), f"step {t}"
+    a.finish()
+    b.finish()
+    for s in range(S):
+        assert b.tables(s) == a.tables(s)
+        assert b.segments(s) == a.segments(s)
+        assert b.events(s) == a.events(s)
+        assert b.metrics(s) == a.metrics(s)
