@@ -10,6 +10,7 @@
 //     (proj/include/thinkv/errors.hpp:13-49)           (same numbers: 2 config, 4 OOM, 5 integrity)
 //   ThinkvMethod(const SimConfig&)  sim.cpp:494-508  DecodeRun(const tkv_run_desc&, device)
 //   ThinkvMethod::process(sv)       sim.cpp:748-843  DecodeRun::process(q, k, v, out, stream)
+//                                                      DecodeRun::process_layer(l, L, ...) per layer
 //   ThinkvMethod::finish()          sim.cpp:871-958  DecodeRun::finish()
 //   RunOutput::final_block_tables / final_segments   DecodeRun::dump("tables" | "segments" |
 //     / events_jsonl / metrics / step_dumps             "events" | "metrics" | "step_dumps", seq)
@@ -69,6 +70,11 @@ class DecodeRun {
   // One decode step for every unit; device pointers, asynchronous on `stream`.
   void process(const void* q, const void* k, const void* v, float* out, void* stream = nullptr) {
     check(tkv_step(h_, q, k, v, out, stream));
+  }
+  // One layer of a step for a model's decode loop (layers 0 .. num_layers-1 in order).
+  void process_layer(int layer, int num_layers, const void* q, const void* k, const void* v, float* out,
+                     void* stream = nullptr) {
+    check(tkv_step_layer(h_, layer, num_layers, q, k, v, out, stream));
   }
   // Same with host buffers (synchronous).
   void process_host(const void* q, const void* k, const void* v, float* out) {

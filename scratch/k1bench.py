@@ -27,8 +27,9 @@ print(f"ctx {ctx} built in {time.time() - t0:.1f}s; bytes {run.bytes()['algorith
 pos = ctx
 for rep in range(3):
     for var in variants:
+        os.environ.pop('TKV_K1_V2', None); os.environ.pop('TKV_K1_MINB', None)
         if var == 'v2': os.environ['TKV_K1_V2'] = '1'
-        else: os.environ.pop('TKV_K1_V2', None)
+        if var == 'minb4': os.environ['TKV_K1_MINB'] = '4'
         run.timing_enable(True)
         for i in range(20):
             if (pos + 1) % 128 == 0 or pos % 128 == 0:  # keep refresh/eviction steps out of the window
