@@ -986,11 +986,6 @@ cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void*
                                              : WarpSmem<64>::bytes(st.max_live, st.dm.g, st.dm.P)) <= 200 * 1024 &&
                   getenv("TKV_K1_V2") == nullptr;
   if (v3) {
-    const char* mb = getenv("TKV_K1_MINB");  // (occupancy experiments)
-    if (mb && mb[0] == '4') {
-      if (D == 128) return launch_k1_warp<128, 4>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
-      return launch_k1_warp<64, 4>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
-    }
     if (D == 128) return launch_k1_warp<128, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
     return launch_k1_warp<64, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
   }
