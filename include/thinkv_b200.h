@@ -80,6 +80,8 @@ typedef struct tkv_run_desc {
   int32_t record_events;    /* keep the evict/refresh/emit event log for tkv_dump_json("events") */
   int32_t num_dump_positions;
   const int64_t* dump_positions;  /* SimConfig::dump_positions, copied at create */
+  int32_t record_sparsity_trace;  /* 1: exact per-unit sparsity on every decode step, exported by
+                                     tkv_dump_json(..., "sparsity_trace") in calibration-trace form */
 } tkv_run_desc;
 
 typedef struct tkv_bytes_t {
@@ -141,8 +143,11 @@ int64_t tkv_position(const tkv_run* run);
 /* JSON views in the reference's own formats: "tables" (BlockPager::dump,
  * pager.cpp:327-362, one per unit), "segments" (sim.cpp:919-937), "events"
  * (JSON lines, sim.cpp:643-648/663-670/724-733), "metrics" (RunMetrics::to_json),
- * "step_dumps".  Writes up to cap bytes (NUL-terminated) and the full length
- * to *needed. */
+ * "step_dumps", "sparsity_trace" (one SparsityTrace::to_jsonl line,
+ * thought.cpp:66-75: {"<unit>": [sparsity per decode step]} -- the record
+ * collect_sparsity_record (sim.cpp:1268-1281) feeds offline calibration,
+ * here over the compressed cache; needs record_sparsity_trace).  Writes up
+ * to cap bytes (NUL-terminated) and the full length to *needed. */
 int tkv_dump_json(tkv_run* run, int seq, const char* what, char* buf, size_t cap, size_t* needed);
 
 /* Byte accounting of the attention view for the next step (FragmentationStats,

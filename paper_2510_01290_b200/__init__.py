@@ -55,6 +55,7 @@ class ThinkvConfig:
     input_dtype: str = "bf16"
     record_events: bool = False
     dump_positions: Sequence[int] = ()
+    record_sparsity_trace: bool = False
 
     @property
     def units(self) -> int:
@@ -95,6 +96,7 @@ class ThinkvConfig:
             d.calib_units[i] = u
         d.input_dtype = _abi.DTYPES[self.input_dtype]
         d.record_events = int(self.record_events)
+        d.record_sparsity_trace = int(self.record_sparsity_trace)
         if self.dump_positions:
             dp = np.array(self.dump_positions, dtype=np.int64)
             keep.append(dp)
@@ -210,6 +212,10 @@ class DecodeRun:
 
     def step_dumps(self, seq: int = 0):
         return json.loads(self._dump(seq, "step_dumps"))
+
+    def sparsity_trace(self, seq: int = 0) -> str:
+        """Calibration-trace JSONL line of a sequence (record_sparsity_trace)."""
+        return self._dump(seq, "sparsity_trace")
 
     def bytes(self) -> dict:
         b = _abi.Bytes()

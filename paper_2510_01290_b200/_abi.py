@@ -40,6 +40,7 @@ class RunDesc(C.Structure):
         ("num_calib_units", C.c_int32), ("calib_units", C.c_int32 * 64),
         ("input_dtype", C.c_int32), ("record_events", C.c_int32),
         ("num_dump_positions", C.c_int32), ("dump_positions", C.POINTER(C.c_int64)),
+        ("record_sparsity_trace", C.c_int32),
     ]
 
 

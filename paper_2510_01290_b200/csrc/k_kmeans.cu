@@ -1351,12 +1351,12 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
     if (x16) {
       if (mmax <= 16) e = go(km_restart_kernel<32, 16, __half>, 32);
       else if (mmax <= 32) e = go(km_restart_kernel<64, 32, __half>, 64);
-      else if (mmax <= 64) e = go(km_restart_kernel<128, 64, __half>, 128);
+      else if (mmax <= 64) e = go(km_restart_kernel<256, 64, __half>, 256);
       else e = go(km_restart_kernel<512, kMaxM, __half>, 512);
     } else {
       if (mmax <= 16) e = go(km_restart_kernel<32, 16, float>, 32);
       else if (mmax <= 32) e = go(km_restart_kernel<64, 32, float>, 64);
-      else if (mmax <= 64) e = go(km_restart_kernel<128, 64, float>, 128);
+      else if (mmax <= 64) e = go(km_restart_kernel<256, 64, float>, 256);
       else e = go(km_restart_kernel<512, kMaxM, float>, 512);
     }
     if (e != cudaSuccess) return e;

@@ -178,6 +178,8 @@ struct tkv_run {
   int max_m = 0;
   TkvFlushCtl* d_ctl = nullptr;
   std::vector<double> last_sparsity;
+  double* d_trace = nullptr;  // [max_gen_len][U] sparsity per decode step (record_sparsity_trace)
+  int64_t trace_steps = 0;
   std::vector<std::vector<double>> refresh_sparsity;  // per refresh (record mode)
   std::vector<json> metrics;
   // per-kernel timing (tkv_timing_enable / tkv_timing_read)
@@ -983,8 +985,10 @@ void step_attend(tkv_run* r, const StepCtx& c, const void* q, const void* k, con
   r->st.lmap_ups = r->desc.units_per_seq;
   r->st.lmap_off = layer * lmap_h;
   r->st.lmap_count = r->desc.num_seqs * lmap_h;
-  // 1. attention (+ exact sparsity on refresh steps, where it is consumed)
-  if (c.refresh && c.decode)
+  // 1. attention (+ exact sparsity on refresh steps, where it is consumed, or
+  //    on every decode step when a sparsity trace is recorded)
+  const bool trace = c.decode && r->desc.record_sparsity_trace;
+  if ((c.refresh && c.decode) || trace)
     launch(r, CAT_SCORE, "score kernel",
            [&] { return tkv_launch_score(r->st, q, k, r->cur_half, r->buf_len, r->stream); });
   launch(r, CAT_ATTEND, "attend kernel", [&] {
@@ -993,7 +997,16 @@ void step_attend(tkv_run* r, const StepCtx& c, const void* q, const void* k, con
   r->st.lmap_h = 0;
 }
 
+void trace_sparsity(tkv_run* r, const StepCtx& c) {
+  if (!(c.decode && r->desc.record_sparsity_trace)) return;
+  const int64_t dstep = c.pos - r->desc.prompt_len;
+  CUDA_OK(cudaMemcpyAsync(r->d_trace + dstep * r->st.dm.U, r->st.sparsity, (size_t)r->st.dm.U * sizeof(double),
+                          cudaMemcpyDeviceToDevice, r->stream));
+  r->trace_steps = dstep + 1;
+}
+
 void step_end(tkv_run* r, const StepCtx& c) {
+  trace_sparsity(r, c);
   const tkv_run_desc& d = r->desc;
   const int64_t pos = c.pos;
   // 2. refresh boundary
@@ -1125,6 +1138,8 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   st.seg_mask = dalloc<uint32_t>(r, U * dm.NSEG * dm.W, 0xFF);
   st.buf = dalloc<uint8_t>(r, U * 4 * (size_t)dm.g * dm.D * dm.in_bytes, 0);
   st.sparsity = dalloc<double>(r, U);
+  if (desc->record_sparsity_trace)
+    r->d_trace = dalloc<double>(r, (size_t)desc->max_gen_len * dm.U, 0);
   st.kstats = nullptr;
   st.max_live = st.dm.NS;
   if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 32, 0);
@@ -1460,6 +1475,20 @@ int tkv_dump_json(tkv_run* run, int seq, const char* what, char* buf, size_t cap
       s = run->metrics.at(seq).dump();
     } else if (w == "step_dumps") {
       s = g.step_dumps.dump();
+    } else if (w == "sparsity_trace") {
+      if (!run->desc.record_sparsity_trace)
+        throw TkvError(TKV_ERR_CONFIG, "run was created without record_sparsity_trace");
+      CUDA_OK(cudaStreamSynchronize(run->stream));
+      const int64_t n = run->trace_steps, U = run->st.dm.U;
+      std::vector<double> tr((size_t)std::max<int64_t>(n, 1) * U);
+      if (n > 0) CUDA_OK(cudaMemcpy(tr.data(), run->d_trace, (size_t)n * U * sizeof(double), cudaMemcpyDeviceToHost));
+      json rec = json::object();
+      for (int uu = 0; uu < g.nunits; ++uu) {
+        std::vector<double> col((size_t)n);
+        for (int64_t t = 0; t < n; ++t) col[t] = tr[(size_t)t * U + g.unit0 + uu];
+        rec[std::to_string(uu)] = col;
+      }
+      s = rec.dump() + "\n";
     } else {
       throw TkvError(TKV_ERR_CONFIG, "unknown dump '" + w + "'");
     }

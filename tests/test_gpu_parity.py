@@ -17,7 +17,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import oracle as O  # noqa: E402
-from harness import compare_state, run_parity  # noqa: E402
+from harness import compare_state, oracle_config as harness_oracle_config, run_parity  # noqa: E402
 from paper_2510_01290_b200 import DecodeRun, ThinkvConfig, TkvError  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -207,3 +207,32 @@ def test_layer_by_layer_stepping_matches_full_steps(maxpool):
         assert b.segments(s) == a.segments(s)
         assert b.events(s) == a.events(s)
         assert b.metrics(s) == a.metrics(s)
+
+
+def test_sparsity_trace_matches_reference_every_step():
+    """record_sparsity_trace: the exact per-unit layer_sparsity_average of
+    every decode step (the reference computes it each step, sim.cpp:779),
+    exported in calibration-trace JSONL form (thought.cpp:66-75)."""
+    cfg = ThinkvConfig(num_seqs=2, units_per_seq=3, num_q_heads=4, head_dim=64, tau=32, group_size=16,
+                       block_size=16, budget=90, levels=(16, 8, 4), prompt_len=8, max_gen_len=200,
+                       script=script(2, 8, seed=4), record_sparsity_trace=True)
+    run = DecodeRun(cfg)
+    orc = O.OracleRun(harness_oracle_config(cfg))
+    dev = torch.device("cuda:0")
+    out = torch.empty((cfg.units, 4, 64), device=dev)
+    ref = []
+    for t in range(cfg.prompt_len + cfg.max_gen_len):
+        q, k, v = O.synth_step(0x71534B56, cfg.units_per_seq, cfg.tau, cfg.units, 4, 64, t)
+        _, sp = orc.step(O.bf16_to_f64(q), O.bf16_to_f64(k), O.bf16_to_f64(v))
+        if t >= cfg.prompt_len:
+            ref.append(sp.copy())
+        tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev) for x in (q, k, v))
+        run.step(tq, tk, tv, out)
+    ref = np.array(ref)  # [decode steps, units]
+    for s in range(2):
+        rec = json.loads(run.sparsity_trace(s))
+        assert sorted(rec, key=int) == ["0", "1", "2"]
+        for u in range(3):
+            got = np.array(rec[str(u)])
+            assert got.shape == (cfg.max_gen_len,)
+            assert np.array_equal(got, ref[:, s * 3 + u]), f"seq {s} unit {u}"
