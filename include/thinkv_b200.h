@@ -154,6 +154,16 @@ int tkv_dump_json(tkv_run* run, int seq, const char* what, char* buf, size_t cap
  * pager.cpp:299-325, extended with buffer/q/out/metadata bytes). */
 int tkv_bytes(tkv_run* run, tkv_bytes_t* out);
 
+/* Compressed-cache export: the live pager tokens of units
+ * [unit0, unit0 + nunits) as QuantizedGroups in the reference wire layout of
+ * serialize_group (proj/src/quant.cpp:274-324, quant.hpp:104-110), one byte
+ * stream per unit (layout: k_export.cu header).  dst is DEVICE memory; with
+ * dst == NULL only *needed and unit_offsets (host, nunits + 1 entries, may be
+ * NULL) are produced.  A non-NULL dst smaller than *needed is a config error
+ * (nothing written).  Synchronises the run's stream. */
+int tkv_export_cache(tkv_run* run, int64_t unit0, int64_t nunits, void* dst, size_t cap, int64_t* unit_offsets,
+                     size_t* needed);
+
 /* Last fp64 per-unit sparsity (layer_sparsity_average) computed on a refresh step. */
 int tkv_unit_sparsity(tkv_run* run, double* out, int64_t n);
 

@@ -59,6 +59,8 @@ def lib():
             L.orc_finish.argtypes = [C.c_void_p]
             L.orc_dump.restype = C.c_char_p
             L.orc_dump.argtypes = [C.c_void_p, C.c_int, C.c_char_p]
+            L.orc_export.restype = C.c_int64
+            L.orc_export.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
             L.orc_toy_compare.restype = C.c_char_p
             L.orc_toy_compare.argtypes = [C.c_char_p]
             L.orc_toy_stream.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -192,6 +194,16 @@ class OracleRun:
         rc = lib().orc_finish(self._h)
         if rc != 0:
             raise OracleError(rc, self.dump(0, "error"))
+
+    def export(self, seq: int, unit: int) -> bytes:
+        """Unit `unit` of sequence `seq` in the k_export.cu stream layout, built
+        by the reference's BlockPager::read_active/group_table + serialize_group."""
+        n = lib().orc_export(self._h, seq, unit, None, 0)
+        if n < 0:
+            raise OracleError(-n, self.dump(0, "error"))
+        buf = C.create_string_buffer(max(1, n))
+        lib().orc_export(self._h, seq, unit, buf, n)
+        return buf.raw[:n]
 
     def dump(self, seq: int, what: str):
         s = lib().orc_dump(self._h, seq, what.encode()).decode()

@@ -237,6 +237,91 @@ class SeqOracle {
     return m.to_json();
   }
 
+  // Compressed-cache export (k_export.cu layout) through the reference's own
+  // public pager API and serialize_group (quant.cpp:274-324).
+  std::vector<std::uint8_t> export_unit(int u) const {
+    const BlockPager& pg = pagers_.at(u);
+    std::vector<const SlotPayload*> live = pg.read_active();
+    std::sort(live.begin(), live.end(), [](const SlotPayload* a, const SlotPayload* b) { return a->id < b->id; });
+    const auto& groups = pg.group_table();
+    auto kind = [](const SlotPayload* p) { return p->raw ? 3 : static_cast<int>(p->format); };
+    auto same = [&](const SlotPayload* a, const SlotPayload* b) {
+      return kind(a) == kind(b) && a->thought.band == b->thought.band &&
+             (a->raw || a->key_group_base == b->key_group_base);
+    };
+    std::vector<std::uint8_t> out(12, 0);
+    auto put = [&](std::uint64_t v, int n) {
+      for (int i = 0; i < n; ++i) out.push_back(static_cast<std::uint8_t>(v >> (8 * i)));
+    };
+    auto put_group = [&](const QuantizedGroup& g) {
+      const auto b = serialize_group(g);
+      out.insert(out.end(), b.begin(), b.end());
+    };
+    const int d = cfg_.model.head_dim;
+    std::uint32_t nrec = 0;
+    for (std::size_t i0 = 0; i0 < live.size();) {
+      std::size_t i1 = i0 + 1;
+      while (i1 < live.size() && same(live[i0], live[i1])) ++i1;
+      const SlotPayload* h = live[i0];
+      const int n = static_cast<int>(i1 - i0);
+      ++nrec;
+      put(static_cast<std::uint64_t>(kind(h)), 1);
+      put(static_cast<std::uint64_t>(h->thought.band), 1);
+      put(static_cast<std::uint64_t>(n), 2);
+      for (std::size_t i = i0; i < i1; ++i) put(static_cast<std::uint64_t>(live[i]->id), 8);
+      if (h->raw) {
+        for (std::size_t i = i0; i < i1; ++i)
+          for (const Vec* v : {&live[i]->key_fp, &live[i]->value_fp})
+            for (double x : *v) {
+              std::uint64_t bits;
+              std::memcpy(&bits, &x, 8);
+              put(bits, 8);
+            }
+      } else if (h->format == Format::kFp8E4M3) {
+        for (int side = 0; side < 2; ++side) {
+          QuantizedGroup g;
+          g.format = h->format;
+          g.g = static_cast<std::uint16_t>(n * d);
+          g.scale_f32 = groups.at(side == 0 ? h->key_group_base : h->value_group_base).scale_f32;
+          for (std::size_t i = i0; i < i1; ++i) {
+            const auto& c = side == 0 ? live[i]->key_codes : live[i]->value_codes;
+            g.codes.insert(g.codes.end(), c.begin(), c.end());
+          }
+          put_group(g);
+        }
+      } else {
+        for (int c = 0; c < d; ++c) {
+          QuantizedGroup g;
+          g.format = h->format;
+          g.g = static_cast<std::uint16_t>(n);
+          g.scale_code = groups.at(h->key_group_base + c).scale_code;
+          for (std::size_t i = i0; i < i1; ++i) g.codes.push_back(live[i]->key_codes[c]);
+          put_group(g);
+        }
+        for (std::size_t i = i0; i < i1; ++i) {
+          const SlotPayload* p = live[i];
+          for (int j = 0; j < p->value_chunks; ++j) {
+            const int c0 = j * p->group_size, len = std::min(p->group_size, d - c0);
+            QuantizedGroup g;
+            g.format = p->format;
+            g.g = static_cast<std::uint16_t>(len);
+            g.scale_code = groups.at(p->value_group_base + j).scale_code;
+            g.codes.assign(p->value_codes.begin() + c0, p->value_codes.begin() + c0 + len);
+            put_group(g);
+          }
+        }
+      }
+      i0 = i1;
+    }
+    for (int i = 0; i < 4; ++i) out[i] = static_cast<std::uint8_t>(nrec >> (8 * i));
+    for (int i = 0; i < 4; ++i) out[4 + i] = static_cast<std::uint8_t>(live.size() >> (8 * i));
+    out[8] = static_cast<std::uint8_t>(d);
+    out[9] = static_cast<std::uint8_t>(d >> 8);
+    out[10] = static_cast<std::uint8_t>(cfg_.group_size);
+    out[11] = static_cast<std::uint8_t>(cfg_.group_size >> 8);
+    return out;
+  }
+
   json tables() const {  // sim.cpp:939-943
     json arr = json::array();
     for (const auto& pg : pagers_) arr.push_back(pg.dump());
@@ -560,6 +645,16 @@ orc_run* orc_create(const orc_desc* desc, char* err, int errlen) {
 }
 
 void orc_destroy(orc_run* run) { delete run; }
+int64_t orc_export(orc_run* run, int seq, int unit, uint8_t* buf, int64_t cap) {
+  try {
+    const auto b = run->seqs.at(seq)->export_unit(unit);
+    if (buf && cap >= static_cast<int64_t>(b.size())) std::memcpy(buf, b.data(), b.size());
+    return static_cast<int64_t>(b.size());
+  } catch (...) {
+    return -error_code_of(std::current_exception(), &run->error);
+  }
+}
+
 
 int orc_step(orc_run* run, const double* q, const double* k, const double* v, double* out,
              double* sparsity) {

@@ -65,6 +65,12 @@ int orc_finish(orc_run* run);
 // what: "tables" | "segments" | "events" | "metrics" | "step_dumps" | "error"
 const char* orc_dump(orc_run* run, int seq, const char* what);
 
+// Compressed-cache export of one unit (layout: paper_2510_01290_b200/csrc/
+// k_export.cu) built from BlockPager::read_active / group_table and
+// thinkv::serialize_group.  Returns the byte count (copies when cap
+// suffices) or -(error code).
+int64_t orc_export(orc_run* run, int seq, int unit, uint8_t* buf, int64_t cap);
+
 // Runs thinkv::generation_loop(config_json) and the oracle restatement fed by
 // a ShadowStream restatement (sim.cpp:355-456) on the same config; returns
 // {"reference": {...}, "oracle": {...}} with metrics/events/tables/segments/

@@ -222,6 +222,22 @@ class DecodeRun:
         check(lib.tkv_bytes(self._h, C.byref(b)))
         return {n: getattr(b, n) for n, _ in _abi.Bytes._fields_}
 
+    def export_cache(self, unit0: int = 0, nunits: int = None):
+        """Live pager tokens of units [unit0, unit0 + nunits) in the reference
+        wire layout (serialize_group, proj/src/quant.cpp:274-324; stream layout
+        in csrc/k_export.cu).  Returns (device uint8 tensor, host int64 offsets
+        of the nunits + 1 unit streams).  Parse with paper_2510_01290_b200.wire."""
+        import numpy as np
+        import torch
+        nunits = self.cfg.units - unit0 if nunits is None else nunits
+        offs = np.zeros(nunits + 1, dtype=np.int64)
+        need = C.c_size_t(0)
+        check(lib.tkv_export_cache(self._h, unit0, nunits, None, 0, offs.ctypes.data, C.byref(need)))
+        buf = torch.empty(max(1, need.value), dtype=torch.uint8, device=torch.device("cuda", self.ctx.device))
+        check(lib.tkv_export_cache(self._h, unit0, nunits, buf.data_ptr(), buf.numel(), offs.ctypes.data,
+                                   C.byref(need)))
+        return buf[:need.value], offs
+
     def timing_enable(self, enable: bool = True):
         check(lib.tkv_timing_enable(self._h, int(enable)))
 

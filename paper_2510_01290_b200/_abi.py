@@ -92,6 +92,7 @@ def _load():
     L.tkv_dump_json.argtypes = [vp, C.c_int, C.c_char_p, C.c_char_p, C.c_size_t,
                                 C.POINTER(C.c_size_t)]
     L.tkv_bytes.argtypes = [vp, C.POINTER(Bytes)]
+    L.tkv_export_cache.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_size_t, vp, C.POINTER(C.c_size_t)]
     L.tkv_unit_sparsity.argtypes = [vp, vp, C.c_int64]
     L.tkv_timing_enable.argtypes = [vp, C.c_int]
     L.tkv_timing_read.argtypes = [vp, C.POINTER(Timing)]

@@ -71,7 +71,8 @@ __device__ __forceinline__ void kst(const TkvState& st, int i, unsigned long lon
   if (st.kstats && threadIdx.x == 0) atomicAdd(st.kstats + i, v);
 }
 __device__ __forceinline__ void kstm(const TkvState& st, int m, int i, unsigned long long v) {
-  if (st.kstats && threadIdx.x == 0) atomicAdd(st.kstats + i + (m <= 16 ? 16 : 0), v);
+  if (st.kstats && threadIdx.x == 0)
+    atomicAdd(st.kstats + 32 + 16 * (m <= 8 ? 0 : m <= 16 ? 1 : m <= 32 ? 2 : m <= 64 ? 3 : 4) + i, v);
 }
 
 // x / n for a cluster size n >= 1.  For n = 2^k the multiply by the exact
@@ -826,7 +827,8 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
         }
         for (int o = 16; o > 0; o >>= 1) abssum += __shfl_xor_sync(0xffffffffu, abssum, o);
         if (!__any_sync(0xffffffffu, neg) || abssum < 5e-13) continue;
-        if (st.kstats && lane == 0 && m > 16) atomicAdd(st.kstats + 31, 1ull);
+        if (st.kstats && lane == 0)
+          atomicAdd(st.kstats + 32 + 16 * (m <= 8 ? 0 : m <= 16 ? 1 : m <= 32 ? 2 : m <= 64 ? 3 : 4) + 1, 1ull);
         double delta = 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {

@@ -1142,7 +1142,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
     r->d_trace = dalloc<double>(r, (size_t)desc->max_gen_len * dm.U, 0);
   st.kstats = nullptr;
   st.max_live = st.dm.NS;
-  if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 32, 0);
+  if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 128, 0);
   st.err = dalloc<int32_t>(r, U);
   check_launch(tkv_launch_init(st, r->stream), "init kernel");
   // arenas
@@ -1515,6 +1515,48 @@ int tkv_bytes(tkv_run* run, tkv_bytes_t* out) {
   }
 }
 
+int tkv_export_cache(tkv_run* run, int64_t unit0, int64_t nunits, void* dst, size_t cap, int64_t* unit_offsets,
+                     size_t* needed) {
+  int64_t* d_buf = nullptr;
+  try {
+    check_device_errors(run);
+    const int64_t U = run->st.dm.U;
+    if (unit0 < 0 || nunits < 0 || unit0 + nunits > U) throw TkvError(TKV_ERR_CONFIG, "unit range out of bounds");
+    if (run->open_pos >= 0) throw TkvError(TKV_ERR_CONFIG, "export inside an open layer-by-layer step");
+    std::vector<int64_t> offs((size_t)nunits + 1, 0);
+    if (nunits > 0) {
+      CUDA_OK(cudaMalloc(&d_buf, (size_t)(2 * nunits + 1) * sizeof(int64_t)));
+      const int npos = (int)std::min<int64_t>(run->pos, run->st.dm.T);
+      launch(run, CAT_APPLY, "export size kernel", [&] {
+        return tkv_launch_export(run->st, (int)unit0, (int)nunits, npos, 0, d_buf, nullptr, nullptr, run->stream);
+      });
+      std::vector<int64_t> sizes((size_t)nunits);
+      CUDA_OK(cudaMemcpyAsync(sizes.data(), d_buf, (size_t)nunits * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                              run->stream));
+      CUDA_OK(cudaStreamSynchronize(run->stream));
+      for (int64_t i = 0; i < nunits; ++i) offs[(size_t)i + 1] = offs[(size_t)i] + sizes[(size_t)i];
+      if (dst && cap >= (size_t)offs.back()) {
+        CUDA_OK(cudaMemcpyAsync(d_buf + nunits, offs.data(), (size_t)(nunits + 1) * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, run->stream));
+        launch(run, CAT_APPLY, "export write kernel", [&] {
+          return tkv_launch_export(run->st, (int)unit0, (int)nunits, npos, 1, nullptr, d_buf + nunits,
+                                   static_cast<uint8_t*>(dst), run->stream);
+        });
+        CUDA_OK(cudaStreamSynchronize(run->stream));
+      }
+      CUDA_OK(cudaFree(d_buf));
+      d_buf = nullptr;
+    }
+    if (unit_offsets) std::memcpy(unit_offsets, offs.data(), offs.size() * sizeof(int64_t));
+    if (needed) *needed = (size_t)offs.back();
+    if (dst && cap < (size_t)offs.back()) throw TkvError(TKV_ERR_CONFIG, "export buffer too small");
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    if (d_buf) cudaFree(d_buf);
+    return fail(e);
+  }
+}
+
 int tkv_unit_sparsity(tkv_run* run, double* out, int64_t n) {
   try {
     const auto sp = download_sparsity(run);
@@ -1541,16 +1583,18 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
   try {
     drain_timing(run);
     if (run->st.kstats) {
-      unsigned long long k[32];
+      unsigned long long k[128];
       CUDA_OK(cudaMemcpy(k, run->st.kstats, sizeof(k), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[kstats] prep=%llu cyc_pd=%llu cyc_prep=%llu restarts=%llu lloyd_it=%llu cyc_lloyd=%llu cyc_hinit=%llu "
-              "passes=%llu moves=%llu swapscans=%llu exact_swaps=%llu cyc_moves=%llu cyc_swaps=%llu cyc_restart=%llu sum_m=%llu "
-              "cyc_swapfilter=%llu ordered_sums=%llu\n",
-              k[0], k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8], k[9], k[10], k[11], k[12], k[13], k[14], k[15],
-              k[31]);
-      fprintf(stderr, "[kstats-small] restarts=%llu lloyd_it=%llu cyc_lloyd=%llu cyc_hinit=%llu passes=%llu moves=%llu "
-              "swapscans=%llu exact_swaps=%llu cyc_moves=%llu cyc_swaps=%llu cyc_restart=%llu sum_m=%llu\n",
-              k[19], k[20], k[21], k[22], k[23], k[24], k[25], k[26], k[27], k[28], k[29], k[30]);
+      fprintf(stderr, "[kstats] prep=%llu cyc_pd=%llu cyc_prep=%llu\n", k[0], k[1], k[2]);
+      static const char* cls[5] = {"m<=8", "m<=16", "m<=32", "m<=64", "m<=128"};
+      for (int c = 0; c < 5; ++c) {
+        const unsigned long long* q = k + 32 + 16 * c;
+        if (!q[3]) continue;
+        fprintf(stderr, "[kstats %s] restarts=%llu sum_m=%llu lloyd_it=%llu cyc_lloyd=%llu cyc_hinit=%llu passes=%llu "
+                "moves=%llu swapscans=%llu cand=%llu ordered_sums=%llu cyc_moves=%llu cyc_swaps=%llu cyc_swapfilter=%llu "
+                "cyc_restart=%llu\n",
+                cls[c], q[3], q[14], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[1], q[11], q[12], q[15], q[13]);
+      }
       CUDA_OK(cudaMemset(run->st.kstats, 0, sizeof(k)));
     }
     out->attend_ms = run->acc_ms[CAT_ATTEND];

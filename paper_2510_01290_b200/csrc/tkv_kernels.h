@@ -63,3 +63,10 @@ cudaError_t tkv_launch_init(const TkvState& st, cudaStream_t stream);
 size_t tkv_gather_smem(const TkvGatherState& g, int exact);
 cudaError_t tkv_launch_gather_step(const TkvGatherState& g, int n, int64_t pos, const void* q, const void* k,
                                    const void* v, float* out, int exact, cudaStream_t stream);
+
+// Compressed-cache export in the reference wire layout (k_export.cu, SURVEY
+// §8f-3): pass 0 writes each unit's byte size into sizes[0..nunits), pass 1
+// writes the unit streams at offsets[] into dst.  Tokens with id < npos.
+size_t tkv_export_smem(const TkvState& st);
+cudaError_t tkv_launch_export(const TkvState& st, int unit0, int nunits, int npos, int pass, int64_t* sizes,
+                              const int64_t* offsets, uint8_t* dst, cudaStream_t stream);

@@ -75,8 +75,27 @@ def run_parity(cfg, seed=0x71534B56, steps=None, check_every=1, inputs=None):
     return res
 
 
+def compare_export(res, cfg):
+    """Compressed-cache export (k_export.cu) == the oracle's export built by
+    the reference's serialize_group, byte for byte, for every unit; the
+    stream parses with the package's wire reader."""
+    from paper_2510_01290_b200 import wire
+    run, orc = res["run"], res["oracle"]
+    buf, offs = run.export_cache()
+    host = buf.cpu().numpy().tobytes()
+    ups = cfg.units_per_seq
+    for u in range(cfg.units):
+        got = host[offs[u]:offs[u + 1]]
+        ref = orc.export(u // ups, u % ups)
+        assert got == ref, f"unit {u}: export differs ({len(got)} vs {len(ref)} bytes)"
+        recs, used = wire.parse_unit(got)
+        assert used == len(got)
+    return len(host)
+
+
 def compare_state(res, cfg, finish=True):
     run, orc = res["run"], res["oracle"]
+    compare_export(res, cfg)
     if finish:
         run.finish()
         orc.finish()
