@@ -16,7 +16,7 @@ EXPORTS = (
     "tkv_last_error", "tkv_abi_version", "tkv_init", "tkv_ctx_destroy", "tkv_run_create",
     "tkv_run_destroy", "tkv_step", "tkv_step_layer", "tkv_step_host", "tkv_finish", "tkv_synchronize",
     "tkv_position", "tkv_dump_json", "tkv_bytes", "tkv_unit_sparsity", "tkv_synth_inputs",
-    "tkv_timing_enable", "tkv_timing_read", "tkv_step_host_async",
+    "tkv_timing_enable", "tkv_timing_read", "tkv_step_host_async", "tkv_export_cache",
     "tkv_gather_create", "tkv_gather_destroy", "tkv_gather_step", "tkv_gather_stats", "tkv_gather_ids",
 )
 
