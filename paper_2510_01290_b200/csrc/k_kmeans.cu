@@ -95,7 +95,11 @@ struct RowSplit {
 };
 
 __device__ __forceinline__ double xget(const float* X, int64_t k) { return (double)X[k]; }
-__device__ __forceinline__ double xget(const __half* X, int64_t k) { return (double)__half2float(X[k]); }
+__device__ __forceinline__ double xget(const __half* X, int64_t k) {
+  double r;  // one F2F.F64.F16 (exact widening)
+  asm("cvt.f64.f16 %0, %1;" : "=d"(r) : "h"(__half_as_ushort(X[k])));
+  return r;
+}
 // Decoded key channel: f32 store, or f16 when every band is a quantised
 // format (code x E4M3 scale <= 8 significant bits in [2^-10, 2688], FP8 codes
 // in [2^-9, 448]: exact in f16).
@@ -197,6 +201,7 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
 #pragma unroll
       for (int q = 0; q < 4; ++q) ip[q] = min(pb * 4 + q, m - 1);
       double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      #pragma unroll 2
       for (int ch = 0; ch < D; ++ch) {
         const double a0 = xval(sX, sxs, jj0, ch, XS, scaled), a1 = xval(sX, sxs, jj1, ch, XS, scaled);
 #pragma unroll
@@ -231,6 +236,7 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
   __syncthreads();
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     double d = 0.0;
+    #pragma unroll 8
     for (int ch = 0; ch < D; ++ch) {
       const double t = __dsub_rn(xval(sX, sxs, i, ch, XS, scaled), mean[ch]);
       d = __dadd_rn(d, __dmul_rn(t, t));
@@ -356,6 +362,7 @@ __device__ void fill_sel(SM& s, const XT* X, int XS, const double* xs, bool scal
       const double* r0 = C + (int64_t)c0 * cstride;
       const double* r1 = C + (int64_t)c1 * cstride;
       double d0 = 0.0, d1 = 0.0;
+      #pragma unroll 8
       for (int ch = 0; ch < D; ++ch) {
         const double t0 = __dsub_rn(xval(X, xs, i0, ch, XS, scaled), r0[ch]);
         const double t1 = __dsub_rn(xval(X, xs, i1, ch, XS, scaled), r1[ch]);
@@ -381,6 +388,7 @@ __device__ void fill_sel(SM& s, const XT* X, int XS, const double* xs, bool scal
 #pragma unroll
     for (int q = 0; q < 4; ++q) ip[q] = min(pb * 4 + q, m - 1);
     double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    #pragma unroll 2
     for (int ch = 0; ch < D; ++ch) {
       const double a0 = r0[ch], a1 = r1[ch];
 #pragma unroll
@@ -409,6 +417,7 @@ __device__ void refresh_cols(const XT* X, int XS, const double* xs, bool scaled,
     const int i = t >> 1, c = (t & 1) ? b : a;
     const double* cr = C + (int64_t)c * cstride;
     double d = 0.0;
+    #pragma unroll 8
     for (int ch = 0; ch < D; ++ch) {
       const double tt = __dsub_rn(xval(X, xs, i, ch, XS, scaled), cr[ch]);
       d = __dadd_rn(d, __dmul_rn(tt, tt));
@@ -626,6 +635,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     __syncthreads();
     for (int c = threadIdx.x; c < K; c += NT) {
       double d = 0.0;
+      #pragma unroll 8
       for (int ch = 0; ch < D; ++ch) {
         const double t = __dsub_rn(S[(int64_t)c * D + ch], Mn[(int64_t)c * MS + ch]);
         d = __dadd_rn(d, __dmul_rn(t, t));
@@ -927,6 +937,7 @@ template <typename XT>
 __device__ __forceinline__ double tiny_dist(const XT* X, int XS, const double* xs, bool scaled, int i,
                                             const double* mu, int D) {
   double d = 0.0;
+  #pragma unroll 8
   for (int ch = 0; ch < D; ++ch) {
     const double t = __dsub_rn(xval(X, xs, i, ch, XS, scaled), mu[ch]);
     d = __dadd_rn(d, __dmul_rn(t, t));
@@ -972,6 +983,9 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
   __shared__ double pd[kTinyM][kTinyM];
   __shared__ double tabA[kTinyM + 1], tabR[kTinyM + 1];  // n / (n + 1.0), -n / (n - 1.0) (evictor.cpp:201, 205)
   __shared__ TinyState ws[kTinyWarps];
+  __shared__ uint32_t fin[512];  // final Lloyd assignment per restart (3 bits per point)
+  __shared__ int uniq[512];
+  __shared__ int nuniq;
   TinyState& w = ws[warp];
   double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)kTinyM * XS * sizeof(XT) + 15) / 16 * 16)) +
                (int64_t)warp * (2 * kmax * D + kTinyM * kTinyM);
@@ -1077,6 +1091,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
       double mv = 0.0;
       if (lane < K) {
         double d = 0.0;
+        #pragma unroll 8
         for (int ch = 0; ch < D; ++ch) {
           const double t = __dsub_rn(S[lane * D + ch], Mn[lane * D + ch]);
           d = __dadd_rn(d, __dmul_rn(t, t));
@@ -1093,6 +1108,43 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
       __syncwarp();
       if (movement < 1e-6) break;
     }
+    // Hartigan's input is the final Lloyd assignment alone (its sums, means and
+    // distances are recomputed from it, evictor.cpp:167-187), so restarts that
+    // end Lloyd with the same assignment produce identical results: record it
+    // and run the refinement once per distinct assignment (phase 2).
+    if (lane == 0) {
+      uint32_t code = 0;
+      for (int i = 0; i < m; ++i) code |= (uint32_t)w.assign[i] << (3 * i);
+      fin[r] = code;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // distinct final assignments, first occurrence (lowest restart) first; a
+  // later duplicate has the same cost and loses the tie to it (evictor.cpp:319-325)
+  if (threadIdx.x == 0) nuniq = 0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+    bool first = true;
+    for (int r2 = 0; r2 < r && first; ++r2) first = fin[r2] != fin[r];
+    if (first) uniq[atomicAdd(&nuniq, 1)] = r;
+    else reinterpret_cast<double*>(base + geo.cost_off())[r] = CUDART_INF;
+  }
+  __syncthreads();
+  for (int ui = warp; ui < nuniq; ui += kTinyWarps) {
+    const int r = uniq[ui];
+    if (lane == 0) {
+      for (int c = 0; c < K; ++c) { w.sizes[c] = 0; w.members[c] = 0u; }
+      for (int i = 0; i < m; ++i) {
+        const int a = (fin[r] >> (3 * i)) & 7;
+        w.assign[i] = a;
+        w.sizes[a] += 1;
+        w.members[a] |= 1u << i;
+      }
+      // D2 columns: a singleton's mean is its point (pd column), else evaluate
+      for (int c = 0; c < K; ++c) w.colsrc[c] = w.sizes[c] == 1 ? __ffs(w.members[c]) - 1 : kColCompute;
+    }
+    __syncwarp();
     // ---- Hartigan (evictor.cpp:167-243) ---------------------------------------------
     for (int idx = lane; idx < K * D; idx += 32) {
       const int c = idx / D, ch = idx - c * D;
@@ -1107,7 +1159,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
       Mn[idx] = div_n(acc, w.sizes[c]);
     }
     __syncwarp();
-    if (movement != 0.0) tiny_fill(w, X, XS, xs, scaled, pd, Mn, d2, m, K, D, lane);
+    tiny_fill(w, X, XS, xs, scaled, pd, Mn, d2, m, K, D, lane);
     for (int pass = 0; pass < 100; ++pass) {
       bool moved = false;  // warp-uniform
       for (int i = 0; i < m; ++i) {
