@@ -93,6 +93,32 @@ def test_parity_full_tau_kmeans():
     compare_state(res, cfg)
 
 
+KMEANS_STRESS = {
+    # many 128 -> 64 -> 32 -> 16 -> 8 -> 4 chains, FP8 band (scaled keys)
+    "tau128_fp8": ThinkvConfig(num_seqs=2, units_per_seq=6, num_q_heads=4, head_dim=128, tau=128, group_size=16,
+                               block_size=16, budget=300, levels=(64, 32, 16, 8, 4), psi_bits=(8, 4, 2),
+                               max_gen_len=1450, script=script(2, 13, seed=21, pT=250), record_events=True),
+    # f32 inputs with a raw 16-bit band: f32 key store (fp32 means in global memory), d = 64
+    "tau128_f32_raw": ThinkvConfig(num_seqs=1, units_per_seq=6, num_q_heads=8, gqa_maxpool=True, head_dim=64,
+                                   tau=128, group_size=16, block_size=8, budget=300, levels=(64, 32, 16, 8, 4),
+                                   psi_bits=(16, 4, 2), max_gen_len=1450, script=script(1, 13, seed=22, pT=250),
+                                   input_dtype="f32", record_events=True),
+}
+
+
+@pytest.mark.parametrize("name", sorted(KMEANS_STRESS))
+def test_parity_kmeans_stress(name):
+    """Many full-size K-means chains: the approximate-distance cache with
+    exact fallback must reproduce every medoid set of the reference."""
+    from harness import synth_inputs
+    cfg = KMEANS_STRESS[name]
+    inputs = None
+    if cfg.input_dtype != "bf16":
+        inputs = lambda t: tuple(O.bf16_to_f64(x) for x in synth_inputs(cfg, 0x71534B56, t))  # noqa: E731
+    res = run_parity(cfg, check_every=25, inputs=inputs)
+    compare_state(res, cfg)
+
+
 def test_pool_exhaustion_matches_reference_error():
     cfg = ThinkvConfig(num_seqs=1, units_per_seq=1, num_q_heads=2, head_dim=16, tau=16, group_size=8,
                        block_size=4, pool_blocks=3, budget=4096, levels=(8, 4), max_gen_len=64,
