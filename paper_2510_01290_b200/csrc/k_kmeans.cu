@@ -345,6 +345,7 @@ __device__ void fill_sel(SM& s, const XT* X, int XS, const double* xs, bool scal
     }
     if (threadIdx.x == 0) s.nccols = base;
   }
+#pragma unroll 4
   for (int t = threadIdx.x; t < m * K; t += NT) {
     const int i = t / K, c = t % K;
     const int src = s.colsrc[c];
@@ -1006,6 +1007,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     }
   }
   __syncthreads();
+  long long tk0 = clock64();
   for (int r = warp; r < nr; r += kTinyWarps) {
     // ---- seeds -------------------------------------------------------------------
     if (lane == 0) {
@@ -1120,6 +1122,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     __syncwarp();
   }
   __syncthreads();
+  if (st.kstats && lane == 0) { atomicAdd(st.kstats + 32 + 5, (unsigned long long)(clock64() - tk0)); atomicAdd(st.kstats + 32 + 3, (unsigned long long)((nr - warp + kTinyWarps - 1) / kTinyWarps)); }
   // distinct final assignments, first occurrence (lowest restart) first; a
   // later duplicate has the same cost and loses the tie to it (evictor.cpp:319-325)
   if (threadIdx.x == 0) nuniq = 0;
@@ -1131,6 +1134,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     else reinterpret_cast<double*>(base + geo.cost_off())[r] = CUDART_INF;
   }
   __syncthreads();
+  const long long tk1 = clock64();
   for (int ui = warp; ui < nuniq; ui += kTinyWarps) {
     const int r = uniq[ui];
     if (lane == 0) {
@@ -1161,6 +1165,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     __syncwarp();
     tiny_fill(w, X, XS, xs, scaled, pd, Mn, d2, m, K, D, lane);
     for (int pass = 0; pass < 100; ++pass) {
+      if (st.kstats && lane == 0) atomicAdd(st.kstats + 32 + 7, 1ull);
       bool moved = false;  // warp-uniform
       for (int i = 0; i < m; ++i) {
         const int from = w.assign[i];
@@ -1209,6 +1214,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
         __syncwarp();
       }
       if (moved) continue;
+      if (st.kstats && lane == 0) atomicAdd(st.kstats + 32 + 9, 1ull);
       // pairwise swaps (evictor.cpp:213-240): pair q = lane in lexicographic order
       int pi = 0, pj = 0;
       bool valid = false;
@@ -1292,7 +1298,9 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     if (lane < K) atomicOr(mask + (ids[med] >> 5), 1u << (ids[med] & 31));
     if (lane == 0) reinterpret_cast<double*>(base + geo.cost_off())[r] = cst;
     __syncwarp();
+    if (st.kstats && lane == 0) atomicAdd(st.kstats + 32 + 8, 1ull);  // distinct refinements
   }
+  if (st.kstats && lane == 0) atomicAdd(st.kstats + 32 + 11, (unsigned long long)(clock64() - tk1));
 }
 
 // ---------------------------------------------------------------------------

@@ -1587,7 +1587,10 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
       CUDA_OK(cudaMemcpy(k, run->st.kstats, sizeof(k), cudaMemcpyDeviceToHost));
       fprintf(stderr, "[kstats] prep=%llu cyc_pd=%llu cyc_prep=%llu\n", k[0], k[1], k[2]);
       static const char* cls[5] = {"m<=8", "m<=16", "m<=32", "m<=64", "m<=128"};
-      for (int c = 0; c < 5; ++c) {
+      if (k[32 + 3])
+        fprintf(stderr, "[kstats tiny] restarts/warp=%llu cyc_lloyd_phase=%llu refinements=%llu passes=%llu swapscans=%llu "
+                "cyc_refine_phase=%llu\n", k[32 + 3], k[32 + 5], k[32 + 8], k[32 + 7], k[32 + 9], k[32 + 11]);
+      for (int c = 1; c < 5; ++c) {
         const unsigned long long* q = k + 32 + 16 * c;
         if (!q[3]) continue;
         fprintf(stderr, "[kstats %s] restarts=%llu sum_m=%llu lloyd_it=%llu cyc_lloyd=%llu cyc_hinit=%llu passes=%llu "
