@@ -11,6 +11,8 @@ ThinkvMethod::process (proj/src/sim.cpp:748-843) for 8192 units.
 Usage:  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 Multi-GPU: launched under torchrun; each rank decodes its own 32 sequences
 (weak scaling, no data-path collective); NCCL all-gathers per-rank stats.
+--scaling strong keeps the global batch at --seqs and splits it over the ranks
+(e.g. 4 sequences per GPU at 8 GPUs).
 """
 from __future__ import annotations
 
@@ -29,16 +31,25 @@ METRIC = "decode tokens/s & TPOT, R1-Llama-8B shape bs32 32K ctx; achieved HBM G
 SEED = 0x71534B56
 
 
+def global_seqs(args, world=1):
+    """Global batch: args.seqs per rank (weak scaling, the default) or
+    args.seqs in total, cut into contiguous per-rank blocks (strong scaling)."""
+    return args.seqs if args.scaling == "strong" else args.seqs * world
+
+
 def workload(args, rank=0, world=1):
-    """This rank's share of the global batch: args.seqs sequences per rank
-    (weak scaling), global sequences [rank*seqs, (rank+1)*seqs)."""
+    """This rank's share of the global batch (shard.seq_range blocks)."""
     from paper_2510_01290_b200 import ThinkvConfig
-    from paper_2510_01290_b200.shard import shard_script
+    from paper_2510_01290_b200.shard import seq_range, shard_script
     from paper_2510_01290_b200.synth import band_script
     intervals = args.max_gen // args.tau + 2
+    gs = global_seqs(args, world)
+    b, e = seq_range(gs, rank, world)
+    if e <= b:
+        raise SystemExit(f"strong scaling: {gs} sequences cannot feed {world} ranks")
     # Scripted thought labels per global sequence: T with p=0.1, else R/E 50/50.
-    script = shard_script(band_script(SEED, args.seqs * world, intervals, 3, args.pT_permille), rank, world)
-    return ThinkvConfig(num_seqs=args.seqs, units_per_seq=args.layers * args.kv_heads, num_q_heads=args.q_per_kv,
+    script = shard_script(band_script(SEED, gs, intervals, 3, args.pT_permille), rank, world)
+    return ThinkvConfig(num_seqs=e - b, units_per_seq=args.layers * args.kv_heads, num_q_heads=args.q_per_kv,
                         head_dim=args.head_dim, tau=args.tau, group_size=16, block_size=args.block_size,
                         budget=args.budget, levels=(64, 32, 16, 8, 4), psi_bits=tuple(args.psi),
                         max_gen_len=args.max_gen, script=script)
@@ -126,7 +137,7 @@ def ncu_traffic():
         return None
 
 
-def cpu_reference(args, cfg, start, steps, unit0=0):
+def cpu_reference(args, cfg, start, steps, unit0=0, total_seqs=None):
     """The reference's own CPU implementation (compiled from /root/reference by
     oracle/Makefile into oracle/_ref/, driven by the ThinkvMethod restatement)
     on all host cores: one thread per core, each decoding one unit of this
@@ -171,13 +182,16 @@ def cpu_reference(args, cfg, start, steps, unit0=0):
     if errs:
         raise RuntimeError(errs[0])
     unit_step_s = sum(per_thread_time) / (threads * steps)
-    tpot_s = unit_step_s * cfg.units / threads
+    # the whole job's units (every rank's sequences) on this box's host cores
+    seqs = total_seqs if total_seqs is not None else cfg.num_seqs
+    units = seqs * cfg.units_per_seq
+    tpot_s = unit_step_s * units / threads
     return {
-        "value": cfg.num_seqs / tpot_s, "unit": "tokens/s", "cores": threads, "kind": "reference",
+        "value": seqs / tpot_s, "unit": "tokens/s", "cores": threads, "kind": "reference",
         "tpot_ms": tpot_s * 1e3, "unit_step_us": unit_step_s * 1e6,
         "sample": (f"{threads} threads x 1 unit each (units spread over the batch), decoded from step 0; "
                    f"positions {start}..{start + steps - 1} timed (only the reference step calls); TPOT "
-                   f"extrapolated as per-unit-step time x {cfg.units} units / {threads} threads "
+                   f"extrapolated as per-unit-step time x {units} units / {threads} threads "
                    f"({wall:.1f} s wall)"),
     }
 
@@ -214,6 +228,8 @@ def main():
     ap.add_argument("--cpu-start", type=int, default=None, help="first timed CPU position (default: the GPU's)")
     ap.add_argument("--cpu-steps", type=int, default=None, help="timed CPU steps (default: --steps)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --seqs per GPU (default); strong: --seqs in total, split over the GPUs")
     args = ap.parse_args()
     preset = PRESETS[args.config]
     for key, val in preset.items():
@@ -225,11 +241,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = workload(args, rank, world)
     from paper_2510_01290_b200.shard import unit_offset
-    unit0 = unit_offset(args.seqs * world, cfg.units_per_seq, rank, world)
+    unit0 = unit_offset(global_seqs(args, world), cfg.units_per_seq, rank, world)
     custom = any((list(getattr(args, k)) if k == "psi" else getattr(args, k)) != (list(v) if k == "psi" else v)
                  for k, v in preset.items() if k != "name")
     config = {"workload": f"ThinKV decode, BASELINE config {args.config}: " + preset["name"] + (" (overridden)" if custom else ""),
-              "global_batch": args.seqs * world, "units_per_gpu": cfg.units, "parallelism": f"seq-shard x{world}",
+              "global_batch": global_seqs(args, world), "units_per_gpu": cfg.units, "parallelism": f"seq-shard x{world}",
               "gqa": "per-head"}
 
     if args.impl == "reference":
@@ -237,9 +253,9 @@ def main():
             return
         ctx = positions(args, cfg)
         cb = cpu_reference(args, cfg, args.cpu_start if args.cpu_start is not None else ctx + args.warmup,
-                           args.cpu_steps or args.steps, unit0)
+                           args.cpu_steps or args.steps, unit0, total_seqs=global_seqs(args, world))
         line = {"metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": cb["tpot_ms"], "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": cb["tpot_ms"], "higher_is_better": True, "scaling": args.scaling,
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference", "config": config,
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -331,14 +347,14 @@ def main():
             torch.distributed.destroy_process_group()
         return
 
-    tok_s = cfg.num_seqs * world * K / (ms_max / 1e3)
+    tok_s = global_seqs(args, world) * K / (ms_max / 1e3)
     peak, peak_kind = measured_peak()
     k1_ms = tm["attend_ms"] / max(1, tm["attend_launches"])
     achieved = bytes_k1["algorithmic_bytes"] / (k1_ms / 1e3) / 1e9
     traffic = ncu_traffic()
     line = {
         "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "bf16 in / fp32 attention / fp64 eviction", "data": "synthetic (deterministic bf16 q/k/v, scripted labels)",
         "config": {**config, "context_steps": ctx, "timed_positions": [ctx + W, ctx + W + K - 1],
                    "l2": (f"K1 reads {bytes_k1['algorithmic_bytes'] / 1e9:.2f} GB per step (compressed KV), larger "
@@ -352,7 +368,7 @@ def main():
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algorithmic_bytes_per_launch": bytes_k1["algorithmic_bytes"],
                      "launch_ms": k1_ms, "live_tokens_per_unit": bytes_k1["live_slots"] / U},
-        "e2e": {"value": cfg.num_seqs * world * E / e2e_s, "unit": "tokens/s",
+        "e2e": {"value": global_seqs(args, world) * E / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in host_inputs[0])),
                 "d2h_bytes_per_step": int(pouts[0].numel() * 4), "steps": E,
                 "api": "tkv_step_host_async (pinned host buffers, copies overlapped with kernels)"},

@@ -92,3 +92,22 @@ def test_two_rank_gloo_sharding_matches_single_rank(tmp_path):
     assert sharded_dumps == full_dumps
     sharded_out = np.concatenate([np.array(r["out"]) for r in res], axis=1)
     assert np.array_equal(sharded_out, full_out)
+
+
+def test_bench_workload_weak_and_strong_split():
+    """bench.py's per-rank workload: weak scaling gives every rank --seqs
+    sequences of a world * seqs global batch; strong scaling splits --seqs
+    over the ranks; in both the ranks' scripts tile the global script."""
+    import argparse
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    for mode, world in (("weak", 2), ("strong", 2), ("strong", 8)):
+        a = argparse.Namespace(seqs=32, layers=2, kv_heads=2, q_per_kv=4, head_dim=64, tau=128, block_size=16,
+                               budget=1024, max_gen=1024, psi=(4, 4, 2), pT_permille=100, scaling=mode)
+        cfgs = [bench.workload(a, r, world) for r in range(world)]
+        gs = bench.global_seqs(a, world)
+        assert gs == (32 * world if mode == "weak" else 32)
+        assert sum(c.num_seqs for c in cfgs) == gs
+        full = band_script(bench.SEED, gs, 1024 // 128 + 2, 3, 100)
+        assert [s for c in cfgs for s in c.script] == [list(s) for s in full]
