@@ -316,6 +316,8 @@ struct RsSmem {
   double tabR[MAXM + 1];  // -n / (n - 1.0) (evictor.cpp:201)
   double mv[MAXM];
   double xs[MAXM];
+  double x2[MAXM];    // |x_i|^2 (swap-filter error bound)
+  double m2[MAXM];    // |mean_of(c)|^2 (swap-filter error bound)
   int flag, move_i, move_to, pair, ncand;
   int res[32];
   int cand[WIN];
@@ -425,6 +427,16 @@ __device__ void refresh_cols(const XT* X, int XS, const double* xs, bool scaled,
     }
     D2[(int64_t)i * K + c] = d;
   }
+}
+
+// |mean_of(c)|^2 of one cluster (one warp; any summation order: it only
+// scales the swap pre-filter's error bound).
+template <typename SM>
+__device__ __forceinline__ void mean_norm(SM& s, const double* Mn, int MS, int c, int D, int lane) {
+  double acc = 0.0;
+  for (int ch = lane; ch < D; ch += 32) acc += Mn[(int64_t)c * MS + ch] * Mn[(int64_t)c * MS + ch];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) s.m2[c] = acc;
 }
 
 // Member lists per cluster in ascending point order (offs/order).
@@ -589,6 +601,14 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     }
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < m; i += NT) {  // |x_i|^2 (bound only: any order)
+    double acc = 0.0;
+    for (int ch = 0; ch < D; ++ch) {
+      const double x = xval(X, xs, i, ch, XS, scaled);
+      acc += x * x;
+    }
+    s.x2[i] = acc;
+  }
   const long long t0 = clock64();
   kstm(st, m, 3, 1);
   // ---- Lloyd (evictor.cpp:102-159) ----------------------------------------
@@ -600,6 +620,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   __syncthreads();
   for (int iter = 0; iter < 50; ++iter) {
     kstm(st, m, 4, 1);
+    for (int c = threadIdx.x; c < K; c += NT) s.mv[c] = 0.0;
     fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D);
     __syncthreads();
     assign_nearest<NT>(s, D2, m, K);
@@ -627,6 +648,66 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       __syncthreads();
       members_par<NT>(s, m, K);
     }
+    if constexpr (MAXM > 32) {  // sums rows in global memory: no read-back chains
+    // next centroids (member sums in point order / size, evictor.cpp:143-152)
+    // written in place, and the movement terms (next - old)^2 (evictor.cpp:
+    // 153-156) summed per column in any order: only "d == 0" (exact for a sum
+    // of non-negative terms) and "sqrt(d) < 1e-6" (decided with a relative
+    // margin, else by the channel-order sum from the saved old centroid) are used.
+    for (int base = 0; base < K * D; base += NT) {
+      const int idx = base + threadIdx.x;
+      const bool valid = idx < K * D;
+      const int c = valid ? rs.row(idx) : -1, ch = valid ? rs.col(idx) : 0;
+      double t2 = 0.0;
+      if (valid) {
+        double acc = 0.0;
+        for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
+        const double nx = div_n(acc, s.sizes[c]);
+        const double old = Mn[(int64_t)c * MS + ch];
+        const double t = __dsub_rn(nx, old);
+        t2 = __dmul_rn(t, t);
+        S[idx] = old;
+        Mn[(int64_t)c * MS + ch] = nx;
+      }
+      const int c0 = __shfl_sync(0xffffffffu, c, 0);
+      if (__all_sync(0xffffffffu, c == c0)) {
+        for (int o = 16; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+        if ((threadIdx.x & 31) == 0 && c0 >= 0) atomicAdd(&s.mv[c0], t2);
+      } else if (valid) {
+        atomicAdd(&s.mv[c], t2);
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < K; c += NT) {
+      double d = s.mv[c];
+      int code;  // 0: unchanged, 1: moved below the tolerance, 2: moved at or above it
+      if (d == 0.0) {
+        code = 0;
+      } else if (__dsqrt_rn(d * (1.0 + 1e-12)) < 1e-6) {
+        code = 1;
+      } else if (!(__dsqrt_rn(d * (1.0 - 1e-12)) < 1e-6)) {
+        code = 2;
+      } else {  // within rounding of the tolerance: the reference's channel-order sum
+        d = 0.0;
+        for (int ch = 0; ch < D; ++ch) {
+          const double t = __dsub_rn(Mn[(int64_t)c * MS + ch], S[(int64_t)c * D + ch]);
+          d = __dadd_rn(d, __dmul_rn(t, t));
+        }
+        code = __dsqrt_rn(d) < 1e-6 ? 1 : 2;
+      }
+      s.cur[c] = code;
+      // next fill: unchanged centroid -> keep; singleton (0 + x) / 1 = x -> pd column
+      s.colsrc[c] = code == 0 ? kColKeep : (s.sizes[c] == 1 ? s.order[s.offs[c]] : kColCompute);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int mx = 0;
+      for (int c = 0; c < K; ++c) mx = mx < s.cur[c] ? s.cur[c] : mx;
+      s.flag = mx < 2;               // movement < 1e-6
+      s.cost = mx > 0 ? 1.0 : 0.0;   // movement != 0: the final means differ from the last fill's
+    }
+    __syncthreads();
+    } else {  // shared-memory sums: channel-order movement per centroid
     for (int idx = threadIdx.x; idx < K * D; idx += NT) {
       const int c = rs.row(idx), ch = rs.col(idx);
       double acc = 0.0;
@@ -654,6 +735,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     }
     for (int idx = threadIdx.x; idx < K * D; idx += NT) Mn[rs.row(idx) * MS + rs.col(idx)] = S[idx];
     __syncthreads();
+    }
     if (s.flag) break;
   }
   const long long t1 = clock64();
@@ -670,6 +752,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   __syncthreads();
   // Lloyd's last update left colsrc describing the final centroids (= these means)
   if (s.cost != 0.0) fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D);
+  for (int c = threadIdx.x >> 5; c < K; c += NT / 32) mean_norm(s, Mn, MS, c, D, threadIdx.x & 31);
   __syncthreads();
   kstm(st, m, 6, (unsigned long long)(clock64() - t1));
   long long tmove = 0, tswap = 0;
@@ -730,6 +813,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       const int nf = s.sizes[from] - 1, nt = s.sizes[to] + 1;
       kstm(st, m, 8, 1);
       moved = true;
+      const long long tu0 = clock64();
       __syncthreads();
       if (threadIdx.x == 0) {
         s.sizes[from] = nf;
@@ -747,8 +831,12 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
         Mn[(int64_t)to * MS + ch] = div_n(sto, nt);
       }
       __syncthreads();
+      const long long tu1 = clock64();
       refresh_cols<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D, from, to);
+      for (int q = threadIdx.x >> 5; q < 2; q += NT / 32) mean_norm(s, Mn, MS, q ? to : from, D, threadIdx.x & 31);
       __syncthreads();
+      kstm(st, m, 0, (unsigned long long)(tu1 - tu0));          // move update
+      kstm(st, m, 2, (unsigned long long)(clock64() - tu1));    // column refresh
     }
     tmove += clock64() - tp;
     if (moved) continue;
@@ -774,13 +862,22 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
         const int i = lo, j = i + 1 + (p - i * (2 * m - i - 1) / 2);
         const int a = s.assign[i], b = s.assign[j];
         if (a == b) continue;
+        // Two singletons with f16 keys: x_j - x_i is exact in fp64 (f16
+        // significands and exponent range), so ma == x_j, mb == x_i and every
+        // term of evictor.cpp:222-225 is exactly 0: not an improving swap.
+        if (sizeof(XT) == 2 && !scaled && s.sizes[a] == 1 && s.sizes[b] == 1) continue;
         const double na = (double)s.sizes[a], nb = (double)s.sizes[b];
         const double w = 1.0 / na + 1.0 / nb;
         const double dja = D2[(int64_t)j * K + a], dia = D2[(int64_t)i * K + a];
         const double dib = D2[(int64_t)i * K + b], djb = D2[(int64_t)j * K + b];
         const double pij = pd[(int64_t)i * geo.mmax + j];
         const double approx = dja - dia + dib - djb - w * pij;
-        const double margin = 1e-6 * (dja + dia + dib + djb + w * pij) + 1e-9;
+        // |approx - reference delta| is below (2D + 10) 2^-53 times the operand
+        // magnitudes: distances, and per channel x_i^2 + x_j^2 + n (m^2 + mu^2)
+        // (evictor.cpp:215-228), <= 14 (|x_i|^2 + |x_j|^2) + 3 (na |mu_a|^2 +
+        // nb |mu_b|^2); 1e-12 covers D <= 256 with a >= 17x safety factor.
+        const double margin = 1e-12 * (dja + dia + dib + djb + w * pij + 16.0 * (s.x2[i] + s.x2[j]) +
+                                       4.0 * (na * s.m2[a] + nb * s.m2[b])) + 1e-12;
         if (approx >= -1e-12 + margin) continue;
         s.cand[atomicAdd(&s.ncand, 1)] = p;
       }
@@ -876,6 +973,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       s.assign[j] = a;
     }
     refresh_cols<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D, a, b);
+    for (int q = threadIdx.x >> 5; q < 2; q += NT / 32) mean_norm(s, Mn, MS, q ? b : a, D, threadIdx.x & 31);
     __syncthreads();
   }
   kstm(st, m, 11, (unsigned long long)tmove);
@@ -932,7 +1030,20 @@ struct TinyState {  // per warp, warp-uniform
   unsigned members[kTinyM];
   int colsrc[kTinyM];
   int seeds[kTinyM];
+  double m2[kTinyM];  // |mean_of(c)|^2 (swap-filter error bound)
 };
+
+// |mean_of(c)|^2 of the listed clusters (lanes = channels, any order).
+__device__ __forceinline__ void tiny_norms(TinyState& w, const double* Mn, int D, int c0, int c1, int lane) {
+  for (int q = 0; q < 2; ++q) {
+    const int c = q ? c1 : c0;
+    double acc = 0.0;
+    for (int ch = lane; ch < D; ch += 32) acc += Mn[c * D + ch] * Mn[c * D + ch];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) w.m2[c] = acc;
+  }
+  __syncwarp();
+}
 
 template <typename XT>
 __device__ __forceinline__ double tiny_dist(const XT* X, int XS, const double* xs, bool scaled, int i,
@@ -983,6 +1094,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
   __shared__ double xs[kTinyM];
   __shared__ double pd[kTinyM][kTinyM];
   __shared__ double tabA[kTinyM + 1], tabR[kTinyM + 1];  // n / (n + 1.0), -n / (n - 1.0) (evictor.cpp:201, 205)
+  __shared__ double tx2[kTinyM];  // |x_i|^2 (swap-filter error bound)
   __shared__ TinyState ws[kTinyWarps];
   __shared__ uint32_t fin[512];  // final Lloyd assignment per restart (3 bits per point)
   __shared__ int uniq[512];
@@ -998,7 +1110,15 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     const double* gpd = reinterpret_cast<const double*>(base + geo.pd_off());
     const RowSplit rs(D);
     for (int i = threadIdx.x; i < m * D; i += blockDim.x) X[rs.row(i) * XS + rs.col(i)] = (XT)gX[i];
-    for (int i = threadIdx.x; i < m; i += blockDim.x) xs[i] = gxs[i];
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      xs[i] = gxs[i];
+      double acc = 0.0;
+      for (int ch = 0; ch < D; ++ch) {
+        const double x = scaled_any ? (double)gX[(int64_t)i * D + ch] * gxs[i] : (double)gX[(int64_t)i * D + ch];
+        acc += x * x;
+      }
+      tx2[i] = acc * 1.000001;
+    }
     for (int t = threadIdx.x; t < m * m; t += blockDim.x) pd[t / m][t % m] = gpd[(int64_t)(t / m) * geo.mmax + t % m];
     for (int n = threadIdx.x; n <= kTinyM; n += blockDim.x) {
       const double dn = (double)n;
@@ -1164,6 +1284,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     }
     __syncwarp();
     tiny_fill(w, X, XS, xs, scaled, pd, Mn, d2, m, K, D, lane);
+    for (int c = 0; c < K; c += 2) tiny_norms(w, Mn, D, c, c + 1 < K ? c + 1 : c, lane);
     for (int pass = 0; pass < 100; ++pass) {
       if (st.kstats && lane == 0) atomicAdd(st.kstats + 32 + 7, 1ull);
       bool moved = false;  // warp-uniform
@@ -1207,6 +1328,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
           Mn[to * D + ch] = div_n(sto, nt);
         }
         __syncwarp();
+        tiny_norms(w, Mn, D, from, to, lane);
         for (int p = lane; p < 2 * m; p += 32) {
           const int pi = p >> 1, c = (p & 1) ? to : from;
           d2[pi * K + c] = tiny_dist(X, XS, xs, scaled, pi, Mn + c * D, D);
@@ -1222,7 +1344,8 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
         for (int j = i + 1; j < m; ++j, ++q)
           if (q == lane) { pi = i; pj = j; valid = true; }
       bool improving = false;
-      if (valid && w.assign[pi] != w.assign[pj]) {
+      if (valid && w.assign[pi] != w.assign[pj] &&
+          !(sizeof(XT) == 2 && !scaled && w.sizes[w.assign[pi]] == 1 && w.sizes[w.assign[pj]] == 1)) {
         const int ai = w.assign[pi], aj = w.assign[pj];
         const int sa = w.sizes[ai], sb = w.sizes[aj];
         const double na = (double)sa, nb = (double)sb;
@@ -1232,7 +1355,9 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
         const double dja = d2[pj * K + ai], dia = d2[pi * K + ai], dib = d2[pi * K + aj], djb = d2[pj * K + aj];
         const double pij = pd[pi][pj];
         const double approx = dja - dia + dib - djb - wgt * pij;
-        const double margin = 1e-6 * (dja + dia + dib + djb + wgt * pij) + 1e-9;
+        // error bound of the identity vs the reference expression (as in km_restart_kernel)
+        const double margin = 1e-12 * (dja + dia + dib + djb + wgt * pij + 16.0 * (tx2[pi] + tx2[pj]) +
+                                       4.0 * (na * w.m2[ai] + nb * w.m2[aj])) + 1e-12;
         if (approx < -1e-12 + margin) {
           const double* mua = Mn + ai * D;
           const double* mub = Mn + aj * D;
@@ -1273,6 +1398,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
         Mn[b * D + ch] = div_n(sb, nb_);
       }
       __syncwarp();
+      tiny_norms(w, Mn, D, a, b, lane);
       for (int p = lane; p < 2 * m; p += 32) {
         const int ii = p >> 1, c = (p & 1) ? b : a;
         d2[ii * K + c] = tiny_dist(X, XS, xs, scaled, ii, Mn + c * D, D);

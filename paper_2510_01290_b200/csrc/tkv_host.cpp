@@ -1595,8 +1595,9 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
         if (!q[3]) continue;
         fprintf(stderr, "[kstats %s] restarts=%llu sum_m=%llu lloyd_it=%llu cyc_lloyd=%llu cyc_hinit=%llu passes=%llu "
                 "moves=%llu swapscans=%llu cand=%llu ordered_sums=%llu cyc_moves=%llu cyc_swaps=%llu cyc_swapfilter=%llu "
-                "cyc_restart=%llu\n",
-                cls[c], q[3], q[14], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[1], q[11], q[12], q[15], q[13]);
+                "cyc_restart=%llu cyc_move_update=%llu cyc_refresh=%llu\n",
+                cls[c], q[3], q[14], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[1], q[11], q[12], q[15], q[13], q[0],
+                q[2]);
       }
       CUDA_OK(cudaMemset(run->st.kstats, 0, sizeof(k)));
     }
