@@ -72,7 +72,7 @@ __device__ __forceinline__ void kst(const TkvState& st, int i, unsigned long lon
 }
 __device__ __forceinline__ void kstm(const TkvState& st, int m, int i, unsigned long long v) {
   if (st.kstats && threadIdx.x == 0)
-    atomicAdd(st.kstats + 32 + 16 * (m <= 8 ? 0 : m <= 16 ? 1 : m <= 32 ? 2 : m <= 64 ? 3 : 4) + i, v);
+    atomicAdd(st.kstats + 32 + 32 * (m <= 8 ? 0 : m <= 16 ? 1 : m <= 32 ? 2 : m <= 64 ? 3 : 4) + i, v);
 }
 
 // x / n for a cluster size n >= 1.  For n = 2^k the multiply by the exact
@@ -621,8 +621,11 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
   for (int iter = 0; iter < 50; ++iter) {
     kstm(st, m, 4, 1);
     for (int c = threadIdx.x; c < K; c += NT) s.mv[c] = 0.0;
+    const long long tl0 = clock64();
     fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D);
     __syncthreads();
+    const long long tl1 = clock64();
+    kstm(st, m, 16, (unsigned long long)(tl1 - tl0));
     assign_nearest<NT>(s, D2, m, K);
     __syncthreads();
     members_par<NT>(s, m, K);
@@ -648,6 +651,8 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       __syncthreads();
       members_par<NT>(s, m, K);
     }
+    const long long tl2 = clock64();
+    kstm(st, m, 17, (unsigned long long)(tl2 - tl1));
     if constexpr (MAXM > 32) {  // sums rows in global memory: no read-back chains
     // next centroids (member sums in point order / size, evictor.cpp:143-152)
     // written in place, and the movement terms (next - old)^2 (evictor.cpp:
@@ -736,6 +741,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
     for (int idx = threadIdx.x; idx < K * D; idx += NT) Mn[rs.row(idx) * MS + rs.col(idx)] = S[idx];
     __syncthreads();
     }
+    kstm(st, m, 18, (unsigned long long)(clock64() - tl2));
     if (s.flag) break;
   }
   const long long t1 = clock64();
@@ -936,7 +942,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
         for (int o = 16; o > 0; o >>= 1) abssum += __shfl_xor_sync(0xffffffffu, abssum, o);
         if (!__any_sync(0xffffffffu, neg) || abssum < 5e-13) continue;
         if (st.kstats && lane == 0)
-          atomicAdd(st.kstats + 32 + 16 * (m <= 8 ? 0 : m <= 16 ? 1 : m <= 32 ? 2 : m <= 64 ? 3 : 4) + 1, 1ull);
+          atomicAdd(st.kstats + 32 + 32 * (m <= 8 ? 0 : m <= 16 ? 1 : m <= 32 ? 2 : m <= 64 ? 3 : 4) + 1, 1ull);
         double delta = 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {

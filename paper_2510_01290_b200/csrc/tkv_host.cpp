@@ -1142,7 +1142,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
     r->d_trace = dalloc<double>(r, (size_t)desc->max_gen_len * dm.U, 0);
   st.kstats = nullptr;
   st.max_live = st.dm.NS;
-  if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 128, 0);
+  if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 256, 0);
   st.err = dalloc<int32_t>(r, U);
   check_launch(tkv_launch_init(st, r->stream), "init kernel");
   // arenas
@@ -1583,7 +1583,7 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
   try {
     drain_timing(run);
     if (run->st.kstats) {
-      unsigned long long k[128];
+      unsigned long long k[256];
       CUDA_OK(cudaMemcpy(k, run->st.kstats, sizeof(k), cudaMemcpyDeviceToHost));
       fprintf(stderr, "[kstats] prep=%llu cyc_pd=%llu cyc_prep=%llu\n", k[0], k[1], k[2]);
       static const char* cls[5] = {"m<=8", "m<=16", "m<=32", "m<=64", "m<=128"};
@@ -1591,13 +1591,14 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
         fprintf(stderr, "[kstats tiny] restarts/warp=%llu cyc_lloyd_phase=%llu refinements=%llu passes=%llu swapscans=%llu "
                 "cyc_refine_phase=%llu\n", k[32 + 3], k[32 + 5], k[32 + 8], k[32 + 7], k[32 + 9], k[32 + 11]);
       for (int c = 1; c < 5; ++c) {
-        const unsigned long long* q = k + 32 + 16 * c;
+        const unsigned long long* q = k + 32 + 32 * c;
         if (!q[3]) continue;
         fprintf(stderr, "[kstats %s] restarts=%llu sum_m=%llu lloyd_it=%llu cyc_lloyd=%llu cyc_hinit=%llu passes=%llu "
                 "moves=%llu swapscans=%llu cand=%llu ordered_sums=%llu cyc_moves=%llu cyc_swaps=%llu cyc_swapfilter=%llu "
-                "cyc_restart=%llu cyc_move_update=%llu cyc_refresh=%llu\n",
+                "cyc_restart=%llu cyc_move_update=%llu cyc_refresh=%llu cyc_lloyd_fill=%llu cyc_lloyd_assign=%llu "
+                "cyc_lloyd_update=%llu\n",
                 cls[c], q[3], q[14], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[1], q[11], q[12], q[15], q[13], q[0],
-                q[2]);
+                q[2], q[16], q[17], q[18]);
       }
       CUDA_OK(cudaMemset(run->st.kstats, 0, sizeof(k)));
     }
