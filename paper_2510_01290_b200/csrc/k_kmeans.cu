@@ -439,6 +439,18 @@ __device__ __forceinline__ void mean_norm(SM& s, const double* Mn, int MS, int c
   if (lane == 0) s.m2[c] = acc;
 }
 
+// Row i of pair rank p in the lexicographic order of pairs (i < j < m):
+// prow(i) = i (2m - i - 1) / 2 <= p < prow(i + 1).  Closed form from the
+// quadratic, then corrected with exact integer comparisons.
+__device__ __forceinline__ int pair_row(int p, int m) {
+  const float b = (float)(2 * m - 1);
+  int i = (int)((b - sqrtf(b * b - 8.0f * (float)p)) * 0.5f);
+  i = max(0, min(i, m - 2));
+  while (i > 0 && i * (2 * m - i - 1) / 2 > p) --i;
+  while (i < m - 2 && (i + 1) * (2 * m - i - 2) / 2 <= p) ++i;
+  return i;
+}
+
 // Member lists per cluster in ascending point order (offs/order).
 template <typename SM>
 __device__ void members(SM& s, int m, int K) {
@@ -534,7 +546,7 @@ __device__ void assign_nearest(SM& s, const double* D2, int m, int K) {
 }
 
 template <int NT, int MAXM, typename XT>
-__global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
                                                         const int32_t* __restrict__ rprefix, int nruns, int run0,
                                                         const int32_t* __restrict__ item_prefix, int item0,
                                                         uint8_t* __restrict__ scratch, KmGeo geo,
@@ -860,12 +872,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       __syncthreads();
       const long long tf0 = clock64();
       for (int p = p0 + threadIdx.x; p < min(npairs, p0 + RsSmem<MAXM>::WIN); p += NT) {
-        int lo = 0, hi = m - 2;  // row i: prow(i) <= p < prow(i + 1)
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (mid * (2 * m - mid - 1) / 2 <= p) lo = mid; else hi = mid - 1;
-        }
-        const int i = lo, j = i + 1 + (p - i * (2 * m - i - 1) / 2);
+        const int i = pair_row(p, m), j = i + 1 + (p - i * (2 * m - i - 1) / 2);
         const int a = s.assign[i], b = s.assign[j];
         if (a == b) continue;
         // Two singletons with f16 keys: x_j - x_i is exact in fp64 (f16
@@ -896,12 +903,7 @@ __global__ void __launch_bounds__(NT) km_restart_kernel(TkvState st, const TkvAn
       // accumulated in the reference's channel order through shuffles.
       for (int c = warp; c < s.ncand; c += NT / 32) {
         const int p = s.cand[c];
-        int lo = 0, hi = m - 2;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (mid * (2 * m - mid - 1) / 2 <= p) lo = mid; else hi = mid - 1;
-        }
-        const int i = lo, j = i + 1 + (p - i * (2 * m - i - 1) / 2);
+        const int i = pair_row(p, m), j = i + 1 + (p - i * (2 * m - i - 1) / 2);
         const int a = s.assign[i], b = s.assign[j];
         const double na = (double)s.sizes[a], nb = (double)s.sizes[b];
         // exact reference expression (evictor.cpp:215-228)

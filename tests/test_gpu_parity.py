@@ -262,3 +262,37 @@ def test_sparsity_trace_matches_reference_every_step():
             got = np.array(rec[str(u)])
             assert got.shape == (cfg.max_gen_len,)
             assert np.array_equal(got, ref[:, s * 3 + u]), f"seq {s} unit {u}"
+
+
+def test_export_edge_cases():
+    """Compressed-cache export: empty cache (before the first emission), a
+    unit sub-range, mid-run exports (partial windows, evicted and reused
+    slots) byte-equal to the oracle's, and the too-small-buffer error."""
+    import ctypes as C
+    from paper_2510_01290_b200 import _abi, wire
+    cfg = ThinkvConfig(num_seqs=2, units_per_seq=3, num_q_heads=4, head_dim=64, tau=32, group_size=16,
+                       block_size=8, budget=40, levels=(16, 8, 4), psi_bits=(8, 4, 2), max_gen_len=200,
+                       script=script(2, 8, seed=17, pT=300))
+    run = DecodeRun(cfg)
+    orc = O.OracleRun(harness_oracle_config(cfg))
+    dev = torch.device("cuda:0")
+    out = torch.empty((cfg.units, 4, 64), device=dev)
+    buf, offs = run.export_cache()
+    assert offs.tolist() == [12 * u for u in range(cfg.units + 1)]  # headers only
+    for u in range(cfg.units):
+        recs, used = wire.parse_unit(buf.cpu().numpy().tobytes()[offs[u]:offs[u + 1]])
+        assert recs == [] and used == 12
+    for t in range(cfg.max_gen_len):
+        q, k, v = O.synth_step(0x71534B56, cfg.units_per_seq, cfg.tau, cfg.units, 4, 64, t)
+        orc.step(O.bf16_to_f64(q), O.bf16_to_f64(k), O.bf16_to_f64(v))
+        tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev) for x in (q, k, v))
+        run.step(tq, tk, tv, out)
+        if t in (15, 16, 47, 120, 199):
+            buf, offs = run.export_cache(unit0=2, nunits=3)
+            host = buf.cpu().numpy().tobytes()
+            for j, u in enumerate(range(2, 5)):
+                assert host[offs[j]:offs[j + 1]] == orc.export(u // 3, u % 3), f"step {t} unit {u}"
+    need = C.c_size_t(0)
+    small = torch.empty(8, dtype=torch.uint8, device=dev)
+    rc = _abi.lib.tkv_export_cache(run._h, 0, cfg.units, small.data_ptr(), 8, None, C.byref(need))
+    assert rc == 2 and need.value > 8
