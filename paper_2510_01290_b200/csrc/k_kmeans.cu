@@ -546,7 +546,7 @@ __device__ void assign_nearest(SM& s, const double* D2, int m, int K) {
 }
 
 template <int NT, int MAXM, typename XT>
-__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 4 : NT == 64 ? 8 : 1) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
                                                         const int32_t* __restrict__ rprefix, int nruns, int run0,
                                                         const int32_t* __restrict__ item_prefix, int item0,
                                                         uint8_t* __restrict__ scratch, KmGeo geo,
@@ -1545,13 +1545,13 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
       return cudaSuccess;
     };
     if (x16) {
-      if (mmax <= 16) e = go(km_restart_kernel<32, 16, __half>, 32);
-      else if (mmax <= 32) e = go(km_restart_kernel<64, 32, __half>, 64);
+      if (mmax <= 16) e = go(km_restart_kernel<64, 16, __half>, 64);
+      else if (mmax <= 32) e = go(km_restart_kernel<128, 32, __half>, 128);
       else if (mmax <= 64) e = go(km_restart_kernel<256, 64, __half>, 256);
       else e = go(km_restart_kernel<512, kMaxM, __half>, 512);
     } else {
-      if (mmax <= 16) e = go(km_restart_kernel<32, 16, float>, 32);
-      else if (mmax <= 32) e = go(km_restart_kernel<64, 32, float>, 64);
+      if (mmax <= 16) e = go(km_restart_kernel<64, 16, float>, 64);
+      else if (mmax <= 32) e = go(km_restart_kernel<128, 32, float>, 128);
       else if (mmax <= 64) e = go(km_restart_kernel<256, 64, float>, 256);
       else e = go(km_restart_kernel<512, kMaxM, float>, 512);
     }
