@@ -112,7 +112,8 @@ __device__ __forceinline__ double xval(const XT* X, const double* xs, int i, int
 // ---------------------------------------------------------------------------
 // prep
 // ---------------------------------------------------------------------------
-__device__ void decode_point(const TkvState& st, int u, int slot, float* xrow, double* xs) {
+template <typename XT>
+__device__ void decode_point(const TkvState& st, int u, int slot, XT* xrow, double* xs) {
   const TkvDims& dm = st.dm;
   const int64_t gs = (int64_t)u * dm.NS + slot;
   const int fmt = dm.band_fmt[st.blk_thought[(int64_t)u * dm.P + slot / dm.bs]];
@@ -130,11 +131,12 @@ __device__ void decode_point(const TkvState& st, int u, int slot, float* xrow, d
       v = (float)tkv_decode_code(fmt, tkv_get_code(kr, fmt, ch),
                                  tkv_e4m3_decode(st.win_ks[((int64_t)u * dm.NW + win) * dm.D + ch]));
     }
-    xrow[ch] = v;
+    xrow[ch] = (XT)v;
   }
   *xs = fmt == TKV_FMT_FP8 ? (double)st.win_kf[(int64_t)u * dm.NW + win] : 1.0;
 }
 
+template <typename XT>
 __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
                                                       const int32_t* __restrict__ prefix, int nitems, int item0,
                                                       uint8_t* __restrict__ scratch, KmGeo geo, int scaled_any) {
@@ -175,15 +177,17 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
   if (sm_bad) return;
   const int m = sm_m, K = op.K;
   extern __shared__ __align__(16) uint8_t pdyn[];
-  float* sX = reinterpret_cast<float*>(pdyn);  // [m][D + 1] (padded: conflict-free column access)
-  const int XS = D + 1;
+  // decoded keys [m][XS] (padded: conflict-free column access); f16 when every
+  // band is quantised (exact, see xval), which doubles the CTAs per SM
+  XT* sX = reinterpret_cast<XT*>(pdyn);
+  const int XS = D + 4 / (int)sizeof(XT);
   __shared__ double sxs[kMaxM];
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     ids[i] = sids[i];
     decode_point(st, u, st.tok_slot[(int64_t)u * dm.T + op.seg_start + sids[i]], sX + (int64_t)i * XS, sxs + i);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < m * D; i += blockDim.x) X[i] = sX[(i / D) * XS + i % D];
+  for (int i = threadIdx.x; i < m * D; i += blockDim.x) X[i] = (float)sX[(i / D) * XS + i % D];
   for (int i = threadIdx.x; i < m; i += blockDim.x) xs[i] = sxs[i];
   const bool scaled = scaled_any != 0;
   // Exact pairwise distances, upper triangle mirrored ((a-b)^2 == (b-a)^2 in
@@ -1493,14 +1497,15 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
                               int run0, int run_count, int mmax, int kmax, int R, uint8_t* scratch, double* gsums,
                               int gsums_ctas, uint32_t* log, int scaled_any, int x16, cudaStream_t stream) {
   KmGeo geo{mmax, kmax, st.dm.D, st.dm.W, R};
-  const size_t psmem = (size_t)mmax * (st.dm.D + 1) * 4;
+  const size_t psmem = x16 ? (size_t)mmax * (st.dm.D + 2) * 2 : (size_t)mmax * (st.dm.D + 1) * 4;
   if (psmem > 160 * 1024) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaSuccess;
+  auto prep = x16 ? km_prep_kernel<__half> : km_prep_kernel<float>;
   if (psmem > 16 * 1024) {
-    e = cudaFuncSetAttribute(km_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    e = cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
     if (e != cudaSuccess) return e;
   }
-  km_prep_kernel<<<item_count, 256, psmem, stream>>>(st, ops, nops, item_prefix, nitems, item0, scratch, geo, scaled_any);
+  prep<<<item_count, 256, psmem, stream>>>(st, ops, nops, item_prefix, nitems, item0, scratch, geo, scaled_any);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "[kmeans] prep launch failed: items=%d: %s\n", item_count, cudaGetErrorString(e));
