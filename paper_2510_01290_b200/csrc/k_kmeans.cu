@@ -306,7 +306,8 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
 // ---------------------------------------------------------------------------
 template <int MAXM>
 struct RsSmem {
-  static constexpr int WIN = MAXM * (MAXM - 1) / 2 < kSwapWin ? MAXM * (MAXM - 1) / 2 : kSwapWin;
+  static constexpr int WIN = MAXM * (MAXM - 1) / 2 < (MAXM == 128 ? 512 : kSwapWin) ? MAXM * (MAXM - 1) / 2
+                                                                              : (MAXM == 128 ? 512 : kSwapWin);
   int assign[MAXM];
   int sizes[MAXM];
   int order[MAXM];
@@ -339,7 +340,8 @@ constexpr int kColCompute = -1;  // recompute the column from the centroid
 // their column; only the rest are evaluated.
 template <int NT, typename SM, typename XT>
 __device__ void fill_sel(SM& s, const XT* X, int XS, const double* xs, bool scaled, const double* C, int cstride,
-                         double* D2, const double* __restrict__ pd, int pstride, int m, int K, int D) {
+                         double* D2, const double* __restrict__ pd, int pstride, int m, int K, int D,
+                         double* stg = nullptr, int stg_rows = 0) {
   if (threadIdx.x < 32) {
     int base = 0;
     for (int c0 = 0; c0 < K; c0 += 32) {
@@ -360,6 +362,41 @@ __device__ void fill_sel(SM& s, const XT* X, int XS, const double* xs, bool scal
   __syncthreads();
   const int nc = s.nccols;
   if (nc == 0) return;
+  if (stg) {
+    // means in global memory: stage stg_rows mean rows at a time in shared
+    // memory, then (point, column) chains -- consecutive lanes take
+    // consecutive points of one column (conflict-free key rows, broadcast mean
+    // row), two independent chains per thread.
+    for (int c0 = 0; c0 < nc; c0 += stg_rows) {
+      const int cn = min(stg_rows, nc - c0);
+      for (int t = threadIdx.x; t < cn * D; t += NT) {
+        const int j = t / D, ch = t - j * D;
+        stg[(int64_t)j * cstride + ch] = C[(int64_t)s.ccols[c0 + j] * cstride + ch];
+      }
+      __syncthreads();
+      const int total = m * cn;
+      for (int t = threadIdx.x; t < total; t += 2 * NT) {
+        const int t2 = t + NT;
+        const bool v1 = t2 < total;
+        const int j0 = t / m, i0 = t - j0 * m;
+        const int j1 = v1 ? t2 / m : j0, i1 = v1 ? t2 - j1 * m : i0;
+        const double* r0 = stg + (int64_t)j0 * cstride;
+        const double* r1 = stg + (int64_t)j1 * cstride;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll 8
+        for (int ch = 0; ch < D; ++ch) {
+          const double a0 = __dsub_rn(xval(X, xs, i0, ch, XS, scaled), r0[ch]);
+          const double a1 = __dsub_rn(xval(X, xs, i1, ch, XS, scaled), r1[ch]);
+          d0 = __dadd_rn(d0, __dmul_rn(a0, a0));
+          d1 = __dadd_rn(d1, __dmul_rn(a1, a1));
+        }
+        D2[(int64_t)i0 * K + s.ccols[c0 + j0]] = d0;
+        if (v1) D2[(int64_t)i1 * K + s.ccols[c0 + j1]] = d1;
+      }
+      __syncthreads();
+    }
+    return;
+  }
   if (nc <= 16) {
     for (int t = threadIdx.x; t < m * nc; t += 2 * NT) {
       const int t2 = t + NT;
@@ -418,11 +455,11 @@ __device__ void fill_sel(SM& s, const XT* X, int XS, const double* xs, bool scal
 
 // Recompute D2 columns a and b (after a move or swap changed those means).
 template <int NT, typename XT>
-__device__ void refresh_cols(const XT* X, int XS, const double* xs, bool scaled, const double* C, int cstride,
+__device__ void refresh_cols(const XT* X, int XS, const double* xs, bool scaled, const double* ra, const double* rb,
                              double* D2, int m, int K, int D, int a, int b) {
   for (int t = threadIdx.x; t < 2 * m; t += NT) {
     const int i = t >> 1, c = (t & 1) ? b : a;
-    const double* cr = C + (int64_t)c * cstride;
+    const double* cr = (t & 1) ? rb : ra;
     double d = 0.0;
     #pragma unroll 8
     for (int ch = 0; ch < D; ++ch) {
@@ -436,9 +473,9 @@ __device__ void refresh_cols(const XT* X, int XS, const double* xs, bool scaled,
 // |mean_of(c)|^2 of one cluster (one warp; any summation order: it only
 // scales the swap pre-filter's error bound).
 template <typename SM>
-__device__ __forceinline__ void mean_norm(SM& s, const double* Mn, int MS, int c, int D, int lane) {
+__device__ __forceinline__ void mean_norm(SM& s, const double* row, int c, int D, int lane) {
   double acc = 0.0;
-  for (int ch = lane; ch < D; ch += 32) acc += Mn[(int64_t)c * MS + ch] * Mn[(int64_t)c * MS + ch];
+  for (int ch = lane; ch < D; ch += 32) acc += row[ch] * row[ch];
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) s.m2[c] = acc;
 }
@@ -550,7 +587,7 @@ __device__ void assign_nearest(SM& s, const double* D2, int m, int K) {
 }
 
 template <int NT, int MAXM, typename XT>
-__global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 4 : NT == 64 ? 8 : 1) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
+__global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 128 ? 4 : NT == 64 ? 8 : 1) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
                                                         const int32_t* __restrict__ rprefix, int nruns, int run0,
                                                         const int32_t* __restrict__ item_prefix, int item0,
                                                         uint8_t* __restrict__ scratch, KmGeo geo,
@@ -571,17 +608,25 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 4 : NT == 64 ?
   if (misc[1]) return;
   const int m = misc[0], K = op.K, D = dm.D;
   const bool scaled = scaled_any != 0;
+  // kMG (the 128-point class at two 256-thread CTAs per SM): the means live in
+  // the CTA's global row block; the rows a fill or a refresh needs are staged
+  // in shared memory (kStg rows).
+  constexpr bool kMG = NT == 256 && MAXM == 128;
+  constexpr int kStg = 4;
   extern __shared__ __align__(16) uint8_t dyn[];
   __shared__ RsSmem<MAXM> s;
   double* xs = s.xs;
-  // smem: X f32/f16 [m][XS] | means f64 [K][D+1] | D2 f64 [m][K]  (rows
-  // padded by one word so column-wise accesses across lanes are conflict-free)
+  // smem: X f32/f16 [m][XS] | means f64 [K][D+1] (not kMG) | D2 f64 [m][K] | staged rows [kStg][D+1] (kMG)
+  // (rows padded by one word so column-wise accesses across lanes are conflict-free)
   const int XS = D + 4 / (int)sizeof(XT), MS = D + 1;
   XT* X = reinterpret_cast<XT*>(dyn);
-  double* Mn = reinterpret_cast<double*>(dyn + (((int64_t)geo.mmax * XS * sizeof(XT) + 15) / 16 * 16));
-  double* D2 = Mn + (int64_t)geo.kmax * MS;
+  double* after_x = reinterpret_cast<double*>(dyn + (((int64_t)geo.mmax * XS * sizeof(XT) + 15) / 16 * 16));
+  double* gblk = gsums + (int64_t)blockIdx.x * geo.kmax * (kMG ? 2 * D + 1 : D);
+  double* Mn = kMG ? gblk + (int64_t)geo.kmax * D : after_x;
+  double* D2 = kMG ? after_x : Mn + (int64_t)geo.kmax * MS;
+  double* Stg = D2 + (int64_t)geo.mmax * geo.kmax;
   // sums / next: shared memory for small instances, else a global row block per CTA
-  double* S = MAXM <= 32 ? D2 + (int64_t)geo.mmax * geo.kmax : gsums + (int64_t)blockIdx.x * geo.kmax * D;
+  double* S = MAXM <= 32 ? D2 + (int64_t)geo.mmax * geo.kmax : gblk;
   const float* gX = reinterpret_cast<const float*>(base + geo.x_off());
   const double* gxs = reinterpret_cast<const double*>(base + geo.xs_off());
   const double* pd = reinterpret_cast<const double*>(base + geo.pd_off());
@@ -638,7 +683,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 4 : NT == 64 ?
     kstm(st, m, 4, 1);
     for (int c = threadIdx.x; c < K; c += NT) s.mv[c] = 0.0;
     const long long tl0 = clock64();
-    fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D);
+    fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D, kMG ? Stg : nullptr, kStg);
     __syncthreads();
     const long long tl1 = clock64();
     kstm(st, m, 16, (unsigned long long)(tl1 - tl0));
@@ -773,8 +818,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 4 : NT == 64 ?
   }
   __syncthreads();
   // Lloyd's last update left colsrc describing the final centroids (= these means)
-  if (s.cost != 0.0) fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D);
-  for (int c = threadIdx.x >> 5; c < K; c += NT / 32) mean_norm(s, Mn, MS, c, D, threadIdx.x & 31);
+  if (s.cost != 0.0) fill_sel<NT>(s, X, XS, xs, scaled, Mn, MS, D2, pd, geo.mmax, m, K, D, kMG ? Stg : nullptr, kStg);
+  for (int c = threadIdx.x >> 5; c < K; c += NT / 32) mean_norm(s, Mn + (int64_t)c * MS, c, D, threadIdx.x & 31);
   __syncthreads();
   kstm(st, m, 6, (unsigned long long)(clock64() - t1));
   long long tmove = 0, tswap = 0;
@@ -849,13 +894,22 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 4 : NT == 64 ?
         const double sto = __dadd_rn(S[(int64_t)to * D + ch], x);
         S[(int64_t)from * D + ch] = sf;
         S[(int64_t)to * D + ch] = sto;
-        Mn[(int64_t)from * MS + ch] = div_n(sf, nf);
-        Mn[(int64_t)to * MS + ch] = div_n(sto, nt);
+        const double mf = div_n(sf, nf), mt = div_n(sto, nt);
+        Mn[(int64_t)from * MS + ch] = mf;
+        Mn[(int64_t)to * MS + ch] = mt;
+        if constexpr (kMG) {
+          Stg[ch] = mf;
+          Stg[MS + ch] = mt;
+        }
       }
       __syncthreads();
       const long long tu1 = clock64();
-      refresh_cols<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D, from, to);
-      for (int q = threadIdx.x >> 5; q < 2; q += NT / 32) mean_norm(s, Mn, MS, q ? to : from, D, threadIdx.x & 31);
+      {
+        const double* ra = kMG ? Stg : Mn + (int64_t)from * MS;
+        const double* rb = kMG ? Stg + MS : Mn + (int64_t)to * MS;
+        refresh_cols<NT>(X, XS, xs, scaled, ra, rb, D2, m, K, D, from, to);
+        for (int q = threadIdx.x >> 5; q < 2; q += NT / 32) mean_norm(s, q ? rb : ra, q ? to : from, D, threadIdx.x & 31);
+      }
       __syncthreads();
       kstm(st, m, 0, (unsigned long long)(tu1 - tu0));          // move update
       kstm(st, m, 2, (unsigned long long)(clock64() - tu1));    // column refresh
@@ -974,18 +1028,29 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 4 : NT == 64 ?
     const int a = s.assign[i], b = s.assign[j];
     for (int ch = threadIdx.x; ch < D; ch += NT) {
       const double xi = xval(X, xs, i, ch, XS, scaled), xj = xval(X, xs, j, ch, XS, scaled);
-      S[(int64_t)a * D + ch] = __dadd_rn(__dsub_rn(S[(int64_t)a * D + ch], xi), xj);
-      S[(int64_t)b * D + ch] = __dsub_rn(__dadd_rn(S[(int64_t)b * D + ch], xi), xj);
-      Mn[(int64_t)a * MS + ch] = div_n(S[(int64_t)a * D + ch], s.sizes[a]);
-      Mn[(int64_t)b * MS + ch] = div_n(S[(int64_t)b * D + ch], s.sizes[b]);
+      const double sa = __dadd_rn(__dsub_rn(S[(int64_t)a * D + ch], xi), xj);
+      const double sb = __dsub_rn(__dadd_rn(S[(int64_t)b * D + ch], xi), xj);
+      S[(int64_t)a * D + ch] = sa;
+      S[(int64_t)b * D + ch] = sb;
+      const double ma = div_n(sa, s.sizes[a]), mb = div_n(sb, s.sizes[b]);
+      Mn[(int64_t)a * MS + ch] = ma;
+      Mn[(int64_t)b * MS + ch] = mb;
+      if constexpr (kMG) {
+        Stg[ch] = ma;
+        Stg[MS + ch] = mb;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       s.assign[i] = b;
       s.assign[j] = a;
     }
-    refresh_cols<NT>(X, XS, xs, scaled, Mn, MS, D2, m, K, D, a, b);
-    for (int q = threadIdx.x >> 5; q < 2; q += NT / 32) mean_norm(s, Mn, MS, q ? b : a, D, threadIdx.x & 31);
+    {
+      const double* ra = kMG ? Stg : Mn + (int64_t)a * MS;
+      const double* rb = kMG ? Stg + MS : Mn + (int64_t)b * MS;
+      refresh_cols<NT>(X, XS, xs, scaled, ra, rb, D2, m, K, D, a, b);
+      for (int q = threadIdx.x >> 5; q < 2; q += NT / 32) mean_norm(s, q ? rb : ra, q ? b : a, D, threadIdx.x & 31);
+    }
     __syncthreads();
   }
   kstm(st, m, 11, (unsigned long long)tmove);
@@ -1487,9 +1552,10 @@ int64_t tkv_km_instance_bytes(int mmax, int kmax, int D, int W, int R) {
   return g.bytes();
 }
 
-size_t tkv_km_restart_smem(int mmax, int kmax, int D, int xbytes) {
-  return (size_t)(((int64_t)mmax * (D + 4 / xbytes) * xbytes + 15) / 16 * 16) + (size_t)kmax * (D + 1) * 8 +
-         (size_t)mmax * kmax * 8;
+size_t tkv_km_restart_smem(int mmax, int kmax, int D, int xbytes, bool means_global) {
+  const size_t x = (size_t)(((int64_t)mmax * (D + 4 / xbytes) * xbytes + 15) / 16 * 16);
+  if (means_global) return x + (size_t)mmax * kmax * 8 + (size_t)4 * (D + 1) * 8;  // + staged rows
+  return x + (size_t)kmax * (D + 1) * 8 + (size_t)mmax * kmax * 8;
 }
 
 cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int nops, const int32_t* item_prefix,
@@ -1529,7 +1595,19 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
                                                                    item0, scratch, geo, log);
     return cudaGetLastError();
   }
-  const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D, x16 ? 2 : 4);
+  // 64 < m <= 128 with f16 keys: two 256-thread CTAs per SM, means in global memory
+  bool mg = x16 && mmax > 64 && mmax <= 128 && getenv("TKV_KM_ONE_CTA") == nullptr;
+  if (mg) {  // only worth it at two CTAs per SM
+    const size_t dyn = tkv_km_restart_smem(mmax, kmax, st.dm.D, 2, true);
+    int nb = 0;
+    if (cudaFuncSetAttribute(km_restart_kernel<256, 128, __half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dyn) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km_restart_kernel<256, 128, __half>, 256, dyn) !=
+            cudaSuccess)
+      cudaGetLastError(), nb = 0;
+    mg = nb >= 2;
+  }
+  const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D, x16 ? 2 : 4, mg);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // tau x d beyond the smem design point
   // runs are processed in chunks of gsums_ctas CTAs (one global sums buffer each)
   // Small classes keep their sums in shared memory: one launch for all runs.
@@ -1549,7 +1627,9 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
                                     scratch, geo, gsums, scaled_any);
       return cudaSuccess;
     };
-    if (x16) {
+    if (mg) {
+      e = go(km_restart_kernel<256, 128, __half>, 256);
+    } else if (x16) {
       if (mmax <= 16) e = go(km_restart_kernel<64, 16, __half>, 64);
       else if (mmax <= 32) e = go(km_restart_kernel<128, 32, __half>, 128);
       else if (mmax <= 64) e = go(km_restart_kernel<256, 64, __half>, 256);

@@ -1166,7 +1166,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   r->scratch_ctas = f64_raw ? (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, U)) : 1;
   r->d_scratch = dalloc<double>(r, (size_t)r->scratch_ctas * r->scratch_per_cta);
   r->km_sums_ctas = 1024;
-  r->km_sums = dalloc<double>(r, (size_t)r->km_sums_ctas * std::max(1, r->max_m - 1) * dm.D);
+  r->km_sums = dalloc<double>(r, (size_t)r->km_sums_ctas * std::max(1, r->max_m - 1) * (2 * dm.D + 1));  // sums | means (128-point class)
   // groups = sequences
   for (int s = 0; s < d.num_seqs; ++s) {
     Group g;

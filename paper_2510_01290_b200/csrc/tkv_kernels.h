@@ -36,7 +36,7 @@ cudaError_t tkv_launch_anneal(const TkvState& st, const TkvAnnealOp* ops, int no
 // K3d v2 (k_kmeans.cu): prep / restart / final kernels over instances
 // [item0, item0 + item_count) whose restarts are [run0, run0 + run_count).
 int64_t tkv_km_instance_bytes(int mmax, int kmax, int D, int W, int R);
-size_t tkv_km_restart_smem(int mmax, int kmax, int D, int xbytes);
+size_t tkv_km_restart_smem(int mmax, int kmax, int D, int xbytes, bool means_global);
 cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int nops, const int32_t* item_prefix,
                               int nitems, const int32_t* run_prefix, int nruns, int item0, int item_count,
                               int run0, int run_count, int mmax, int kmax, int R, uint8_t* scratch, double* gsums,
