@@ -512,7 +512,10 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
       const int run1 = i0 + cnt < items ? run_of_item(i0 + cnt) : runs;
       launch(r, CAT_ANNEAL, "kmeans kernels", [&] {
         return tkv_launch_kmeans(r->st, d_ops, (int)wv.size(), d_pre, items, d_rpre, runs, i0, cnt, run0,
-                                 run1 - run0, mmax, kmax, R, r->km_scratch, r->km_sums, r->km_sums_ctas, r->d_log,
+                                 run1 - run0, mmax, kmax, R, r->km_scratch, r->km_sums,
+                                 (int)std::min<int64_t>(1 << 20, (int64_t)r->km_sums_ctas * std::max(1, r->max_m - 1) /
+                                                                    std::max(1, kmax)),
+                                 r->d_log,
                                  fp8 ? 1 : 0, raw ? 0 : 1, r->stream);
       });
     }
@@ -1165,7 +1168,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   r->scratch_per_cta = f64_raw ? (int64_t)6 * r->max_m * dm.D : 1;
   r->scratch_ctas = f64_raw ? (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, U)) : 1;
   r->d_scratch = dalloc<double>(r, (size_t)r->scratch_ctas * r->scratch_per_cta);
-  r->km_sums_ctas = 1024;
+  r->km_sums_ctas = 2048;  // row blocks at the widest class; narrower classes fit proportionally more
   r->km_sums = dalloc<double>(r, (size_t)r->km_sums_ctas * std::max(1, r->max_m - 1) * (2 * dm.D + 1));  // sums | means (128-point class)
   // groups = sequences
   for (int s = 0; s < d.num_seqs; ++s) {
