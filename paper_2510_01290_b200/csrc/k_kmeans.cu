@@ -306,8 +306,8 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
 // ---------------------------------------------------------------------------
 template <int MAXM>
 struct RsSmem {
-  static constexpr int WIN = MAXM * (MAXM - 1) / 2 < (MAXM == 128 ? 512 : kSwapWin) ? MAXM * (MAXM - 1) / 2
-                                                                              : (MAXM == 128 ? 512 : kSwapWin);
+  static constexpr int CAP = (MAXM == 128 || MAXM == 64) ? 512 : kSwapWin;  // smaller for the multi-CTA classes
+  static constexpr int WIN = MAXM * (MAXM - 1) / 2 < CAP ? MAXM * (MAXM - 1) / 2 : CAP;
   int assign[MAXM];
   int sizes[MAXM];
   int order[MAXM];
@@ -587,7 +587,8 @@ __device__ void assign_nearest(SM& s, const double* D2, int m, int K) {
 }
 
 template <int NT, int MAXM, typename XT>
-__global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 128 ? 4 : NT == 64 ? 8 : 1) km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
+__global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 128 ? (MAXM == 64 ? 6 : 4) : NT == 64 ? 8 : 1)
+    km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
                                                         const int32_t* __restrict__ rprefix, int nruns, int run0,
                                                         const int32_t* __restrict__ item_prefix, int item0,
                                                         uint8_t* __restrict__ scratch, KmGeo geo,
@@ -611,7 +612,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 
   // kMG (the 128-point class at two 256-thread CTAs per SM): the means live in
   // the CTA's global row block; the rows a fill or a refresh needs are staged
   // in shared memory (kStg rows).
-  constexpr bool kMG = NT == 256 && MAXM == 128;
+  constexpr bool kMG = (NT == 256 && MAXM == 128) || (NT == 128 && MAXM == 64);
   constexpr int kStg = 4;
   extern __shared__ __align__(16) uint8_t dyn[];
   __shared__ RsSmem<MAXM> s;
@@ -1607,7 +1608,19 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
       cudaGetLastError(), nb = 0;
     mg = nb >= 2;
   }
-  const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D, x16 ? 2 : 4, mg);
+  // 32 < m <= 64 with f16 keys: six 128-thread CTAs per SM, means in global memory
+  bool mg64 = x16 && mmax > 32 && mmax <= 64 && getenv("TKV_KM_ONE_CTA") == nullptr;
+  if (mg64) {
+    const size_t dyn = tkv_km_restart_smem(mmax, kmax, st.dm.D, 2, true);
+    int nb = 0;
+    if (cudaFuncSetAttribute(km_restart_kernel<128, 64, __half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dyn) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km_restart_kernel<128, 64, __half>, 128, dyn) !=
+            cudaSuccess)
+      cudaGetLastError(), nb = 0;
+    mg64 = nb >= 6;
+  }
+  const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D, x16 ? 2 : 4, mg || mg64);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // tau x d beyond the smem design point
   // runs are processed in chunks of gsums_ctas CTAs (one global sums buffer each)
   // Small classes keep their sums in shared memory: one launch for all runs.
@@ -1629,6 +1642,8 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
     };
     if (mg) {
       e = go(km_restart_kernel<256, 128, __half>, 256);
+    } else if (mg64) {
+      e = go(km_restart_kernel<128, 64, __half>, 128);
     } else if (x16) {
       if (mmax <= 16) e = go(km_restart_kernel<64, 16, __half>, 64);
       else if (mmax <= 32) e = go(km_restart_kernel<128, 32, __half>, 128);
