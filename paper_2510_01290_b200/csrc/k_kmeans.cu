@@ -82,6 +82,10 @@ __device__ __forceinline__ double div_n(double x, int n) {
   if ((n & (n - 1)) == 0) return __dmul_rn(x, __longlong_as_double((long long)(1024 - __ffs(n)) << 52));
   return __ddiv_rn(x, (double)n);
 }
+// Out-of-line form for the warp-per-restart kernel: one copy of the division
+// sequence keeps its many concurrent warps inside the instruction cache
+// (inlined copies made "no instruction" the dominant stall).
+__device__ __noinline__ double div_n_ool(double x, int n) { return div_n(x, n); }
 
 // idx -> (row, channel) for row length D (shift/mask when D is a power of two).
 struct RowSplit {
@@ -649,10 +653,10 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 
       for (int c = 0; c < K; ++c) {
         while (true) {
           // number of subsets starting with x at position c
-          double cnt = 1.0;
+          int cnt = 1;  // C(n, k) <= 512 in exact integers (each step divides exactly)
           const int n = m - x - 1, k = K - c - 1;
-          for (int t = 0; t < k; ++t) cnt = cnt * (double)(n - t) / (double)(t + 1);
-          const int ci = (int)(cnt + 0.5);
+          for (int t = 0; t < k; ++t) cnt = cnt * (n - t) / (t + 1);
+          const int ci = (int)cnt;
           if (rank < ci) break;
           rank -= ci;
           ++x;
@@ -1124,10 +1128,10 @@ __device__ __forceinline__ void tiny_norms(TinyState& w, const double* Mn, int D
 }
 
 template <typename XT>
-__device__ __forceinline__ double tiny_dist(const XT* X, int XS, const double* xs, bool scaled, int i,
+__device__ __noinline__ double tiny_dist(const XT* X, int XS, const double* xs, bool scaled, int i,
                                             const double* mu, int D) {
   double d = 0.0;
-  #pragma unroll 8
+  #pragma unroll 2
   for (int ch = 0; ch < D; ++ch) {
     const double t = __dsub_rn(xval(X, xs, i, ch, XS, scaled), mu[ch]);
     d = __dadd_rn(d, __dmul_rn(t, t));
@@ -1217,10 +1221,10 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
         int rank = r, x = 0;
         for (int c = 0; c < K; ++c) {
           while (true) {
-            double cnt = 1.0;
+            int cnt = 1;  // C(n, k) <= 512 in exact integers (each step divides exactly)
             const int n = m - x - 1, k = K - c - 1;
-            for (int t = 0; t < k; ++t) cnt = cnt * (double)(n - t) / (double)(t + 1);
-            const int ci = (int)(cnt + 0.5);
+            for (int t = 0; t < k; ++t) cnt = cnt * (n - t) / (t + 1);
+            const int ci = (int)cnt;
             if (rank < ci) break;
             rank -= ci;
             ++x;
@@ -1284,7 +1288,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
           mm &= mm - 1;
           acc = __dadd_rn(acc, xval(X, xs, i, ch, XS, scaled));
         }
-        S[idx] = div_n(acc, w.sizes[c]);
+        S[idx] = div_n_ool(acc, w.sizes[c]);
       }
       __syncwarp();
       // movement per centroid (lane c, channel order); next fill's column sources
@@ -1358,7 +1362,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
         acc = __dadd_rn(acc, xval(X, xs, i, ch, XS, scaled));
       }
       S[idx] = acc;
-      Mn[idx] = div_n(acc, w.sizes[c]);
+      Mn[idx] = div_n_ool(acc, w.sizes[c]);
     }
     __syncwarp();
     tiny_fill(w, X, XS, xs, scaled, pd, Mn, d2, m, K, D, lane);
@@ -1402,8 +1406,8 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
           const double sto = __dadd_rn(S[to * D + ch], x);
           S[from * D + ch] = sf;
           S[to * D + ch] = sto;
-          Mn[from * D + ch] = div_n(sf, nf);
-          Mn[to * D + ch] = div_n(sto, nt);
+          Mn[from * D + ch] = div_n_ool(sf, nf);
+          Mn[to * D + ch] = div_n_ool(sto, nt);
         }
         __syncwarp();
         tiny_norms(w, Mn, D, from, to, lane);
@@ -1442,8 +1446,8 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
           double delta = 0.0;
           for (int ch = 0; ch < D; ++ch) {
             const double xi = xval(X, xs, pi, ch, XS, scaled), xj = xval(X, xs, pj, ch, XS, scaled);
-            const double ma = __dadd_rn(mua[ch], div_n(__dsub_rn(xj, xi), sa));
-            const double mb = __dadd_rn(mub[ch], div_n(__dsub_rn(xi, xj), sb));
+            const double ma = __dadd_rn(mua[ch], div_n_ool(__dsub_rn(xj, xi), sa));
+            const double mb = __dadd_rn(mub[ch], div_n_ool(__dsub_rn(xi, xj), sb));
             delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi)),
                                                __dmul_rn(na, __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua[ch], mua[ch])))));
             delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj)),
@@ -1472,8 +1476,8 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
         const double sb = __dsub_rn(__dadd_rn(S[b * D + ch], xi), xj);
         S[a * D + ch] = sa;
         S[b * D + ch] = sb;
-        Mn[a * D + ch] = div_n(sa, na_);
-        Mn[b * D + ch] = div_n(sb, nb_);
+        Mn[a * D + ch] = div_n_ool(sa, na_);
+        Mn[b * D + ch] = div_n_ool(sb, nb_);
       }
       __syncwarp();
       tiny_norms(w, Mn, D, a, b, lane);
