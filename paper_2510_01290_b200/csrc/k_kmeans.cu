@@ -460,7 +460,22 @@ __device__ void fill_sel(SM& s, const XT* X, int XS, const double* xs, bool scal
 // Recompute D2 columns a and b (after a move or swap changed those means).
 template <int NT, typename XT>
 __device__ void refresh_cols(const XT* X, int XS, const double* xs, bool scaled, const double* ra, const double* rb,
-                             double* D2, int m, int K, int D, int a, int b) {
+                             double* D2, int m, int K, int D, int a, int b, bool shared_x = false) {
+  if (shared_x) {  // one thread per point: the key channel is widened once for both chains
+    for (int i = threadIdx.x; i < m; i += NT) {
+      double da = 0.0, db = 0.0;
+#pragma unroll 8
+      for (int ch = 0; ch < D; ++ch) {
+        const double x = xval(X, xs, i, ch, XS, scaled);
+        const double ta = __dsub_rn(x, ra[ch]), tb = __dsub_rn(x, rb[ch]);
+        da = __dadd_rn(da, __dmul_rn(ta, ta));
+        db = __dadd_rn(db, __dmul_rn(tb, tb));
+      }
+      D2[(int64_t)i * K + a] = da;
+      D2[(int64_t)i * K + b] = db;
+    }
+    return;
+  }
   for (int t = threadIdx.x; t < 2 * m; t += NT) {
     const int i = t >> 1, c = (t & 1) ? b : a;
     const double* cr = (t & 1) ? rb : ra;
@@ -912,7 +927,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 
       {
         const double* ra = kMG ? Stg : Mn + (int64_t)from * MS;
         const double* rb = kMG ? Stg + MS : Mn + (int64_t)to * MS;
-        refresh_cols<NT>(X, XS, xs, scaled, ra, rb, D2, m, K, D, from, to);
+        refresh_cols<NT>(X, XS, xs, scaled, ra, rb, D2, m, K, D, from, to, kMG);
         for (int q = threadIdx.x >> 5; q < 2; q += NT / 32) mean_norm(s, q ? rb : ra, q ? to : from, D, threadIdx.x & 31);
       }
       __syncthreads();
@@ -1053,7 +1068,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 
     {
       const double* ra = kMG ? Stg : Mn + (int64_t)a * MS;
       const double* rb = kMG ? Stg + MS : Mn + (int64_t)b * MS;
-      refresh_cols<NT>(X, XS, xs, scaled, ra, rb, D2, m, K, D, a, b);
+      refresh_cols<NT>(X, XS, xs, scaled, ra, rb, D2, m, K, D, a, b, kMG);
       for (int q = threadIdx.x >> 5; q < 2; q += NT / 32) mean_norm(s, q ? rb : ra, q ? b : a, D, threadIdx.x & 31);
     }
     __syncthreads();
