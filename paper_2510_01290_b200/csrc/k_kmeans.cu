@@ -387,12 +387,22 @@ __device__ void fill_sel(SM& s, const XT* X, int XS, const double* xs, bool scal
         const double* r0 = stg + (int64_t)j0 * cstride;
         const double* r1 = stg + (int64_t)j1 * cstride;
         double d0 = 0.0, d1 = 0.0;
+        if (i0 == i1) {  // both chains on one point (m divides NT): widen each key channel once
 #pragma unroll 8
-        for (int ch = 0; ch < D; ++ch) {
-          const double a0 = __dsub_rn(xval(X, xs, i0, ch, XS, scaled), r0[ch]);
-          const double a1 = __dsub_rn(xval(X, xs, i1, ch, XS, scaled), r1[ch]);
-          d0 = __dadd_rn(d0, __dmul_rn(a0, a0));
-          d1 = __dadd_rn(d1, __dmul_rn(a1, a1));
+          for (int ch = 0; ch < D; ++ch) {
+            const double x = xval(X, xs, i0, ch, XS, scaled);
+            const double a0 = __dsub_rn(x, r0[ch]), a1 = __dsub_rn(x, r1[ch]);
+            d0 = __dadd_rn(d0, __dmul_rn(a0, a0));
+            d1 = __dadd_rn(d1, __dmul_rn(a1, a1));
+          }
+        } else {
+#pragma unroll 8
+          for (int ch = 0; ch < D; ++ch) {
+            const double a0 = __dsub_rn(xval(X, xs, i0, ch, XS, scaled), r0[ch]);
+            const double a1 = __dsub_rn(xval(X, xs, i1, ch, XS, scaled), r1[ch]);
+            d0 = __dadd_rn(d0, __dmul_rn(a0, a0));
+            d1 = __dadd_rn(d1, __dmul_rn(a1, a1));
+          }
         }
         D2[(int64_t)i0 * K + s.ccols[c0 + j0]] = d0;
         if (v1) D2[(int64_t)i1 * K + s.ccols[c0 + j1]] = d1;
