@@ -1266,7 +1266,6 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
       Mn[idx] = xval(X, xs, w.seeds[c], ch, XS, scaled);
     }
     __syncwarp();
-    double movement = 0.0;
     // ---- Lloyd (evictor.cpp:102-159) ------------------------------------------------
     for (int iter = 0; iter < 50; ++iter) {
       tiny_fill(w, X, XS, xs, scaled, pd, Mn, d2, m, K, D, lane);
@@ -1316,26 +1315,41 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
         S[idx] = div_n_ool(acc, w.sizes[c]);
       }
       __syncwarp();
-      // movement per centroid (lane c, channel order); next fill's column sources
-      double mv = 0.0;
-      if (lane < K) {
-        double d = 0.0;
-        #pragma unroll 8
-        for (int ch = 0; ch < D; ++ch) {
-          const double t = __dsub_rn(S[lane * D + ch], Mn[lane * D + ch]);
-          d = __dadd_rn(d, __dmul_rn(t, t));
-        }
-        mv = __dsqrt_rn(d);
-        w.colsrc[lane] = d == 0.0 ? kColKeep : (w.sizes[lane] == 1 ? __ffs(w.members[lane]) - 1 : kColCompute);
-      }
-      movement = 0.0;
+      // movement per centroid (evictor.cpp:153-156): the terms (next - old)^2
+      // summed across lanes in any order decide "== 0" exactly (non-negative
+      // terms) and "sqrt < 1e-6" with a relative margin; a sum within the
+      // margin is redone in channel order by one lane.  Next fill's columns.
+      int code_max = 0;
       for (int c = 0; c < K; ++c) {
-        const double x = __shfl_sync(0xffffffffu, mv, c);
-        movement = movement < x ? x : movement;
+        double part = 0.0;
+        for (int ch = lane; ch < D; ch += 32) {
+          const double t = __dsub_rn(S[c * D + ch], Mn[c * D + ch]);
+          part += __dmul_rn(t, t);
+        }
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        int code;
+        if (part == 0.0) {
+          code = 0;
+        } else if (__dsqrt_rn(part * (1.0 + 1e-12)) < 1e-6) {
+          code = 1;
+        } else if (!(__dsqrt_rn(part * (1.0 - 1e-12)) < 1e-6)) {
+          code = 2;
+        } else {
+          double d = 0.0;
+          if (lane == 0)
+            for (int ch = 0; ch < D; ++ch) {
+              const double t = __dsub_rn(S[c * D + ch], Mn[c * D + ch]);
+              d = __dadd_rn(d, __dmul_rn(t, t));
+            }
+          code = __shfl_sync(0xffffffffu, __dsqrt_rn(d) < 1e-6 ? 1 : 2, 0);
+        }
+        if (lane == 0)
+          w.colsrc[c] = code == 0 ? kColKeep : (w.sizes[c] == 1 ? __ffs(w.members[c]) - 1 : kColCompute);
+        code_max = code_max > code ? code_max : code;
       }
       for (int idx = lane; idx < K * D; idx += 32) Mn[idx] = S[idx];
       __syncwarp();
-      if (movement < 1e-6) break;
+      if (code_max < 2) break;  // movement < 1e-6
     }
     // Hartigan's input is the final Lloyd assignment alone (its sums, means and
     // distances are recomputed from it, evictor.cpp:167-187), so restarts that
