@@ -98,7 +98,7 @@ class ClockSampler:
                 self.samples.append(f)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.02)
 
     def __enter__(self):
         self._t.start()

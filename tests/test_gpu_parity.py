@@ -98,6 +98,10 @@ KMEANS_STRESS = {
     "tau128_fp8": ThinkvConfig(num_seqs=2, units_per_seq=6, num_q_heads=4, head_dim=128, tau=128, group_size=16,
                                block_size=16, budget=300, levels=(64, 32, 16, 8, 4), psi_bits=(8, 4, 2),
                                max_gen_len=1450, script=script(2, 13, seed=21, pT=250), record_events=True),
+    # tau = 96: 96 -> 64 -> 32 ... anneals (m not a power of two in the two-CTA class), block 8
+    "tau96_m96": ThinkvConfig(num_seqs=2, units_per_seq=3, num_q_heads=4, head_dim=128, tau=96, group_size=16,
+                              block_size=8, budget=260, levels=(64, 32, 16, 8, 4), psi_bits=(4, 8, 2),
+                              max_gen_len=1100, script=script(2, 13, seed=29, pT=300), record_events=True),
     # d = 64, all bands quantised: the multi-CTA restart classes (means in global memory)
     "tau128_d64": ThinkvConfig(num_seqs=2, units_per_seq=4, num_q_heads=8, head_dim=64, tau=128, group_size=16,
                                block_size=16, budget=300, levels=(64, 32, 16, 8, 4), psi_bits=(4, 4, 2),
