@@ -1615,7 +1615,9 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
     e = cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
     if (e != cudaSuccess) return e;
   }
-  prep<<<item_count, 256, psmem, stream>>>(st, ops, nops, item_prefix, nitems, item0, scratch, geo, scaled_any);
+  // (>= 4 warps: the farthest-first seeds use one warp per anchor)
+  prep<<<item_count, mmax > 32 ? 256 : 128, psmem, stream>>>(st, ops, nops, item_prefix, nitems, item0, scratch, geo,
+                                                            scaled_any);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "[kmeans] prep launch failed: items=%d: %s\n", item_count, cudaGetErrorString(e));
@@ -1667,7 +1669,12 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // tau x d beyond the smem design point
   // runs are processed in chunks of gsums_ctas CTAs (one global sums buffer each)
   // Small classes keep their sums in shared memory: one launch for all runs.
-  const int chunk = mmax <= 32 ? (run_count > 0 ? run_count : 1) : gsums_ctas;
+  // Launches of equal size (no short tail launch): ceil(runs / capacity) of them.
+  int chunk = mmax <= 32 ? (run_count > 0 ? run_count : 1) : gsums_ctas;
+  if (run_count > chunk) {
+    const int nl = (run_count + chunk - 1) / chunk;
+    chunk = (run_count + nl - 1) / nl;
+  }
   for (int r = 0; r < run_count; r += chunk) {
     const int n = run_count - r < chunk ? run_count - r : chunk;
     // Instance-size variants: static shared arrays and CTA width scale with
