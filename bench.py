@@ -262,6 +262,11 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    if args.steps % args.tau and rank == 0:
+        print(f"[bench] note: --steps {args.steps} is not a multiple of tau={args.tau}; the timed window "
+              "(the steps just before a refresh boundary) then holds no eviction wave, so TPOT is the "
+              "between-boundary TPOT, not the tau-period average the default --steps 128 measures",
+              file=sys.stderr)
     import torch
     torch.cuda.set_device(local)
     if world > 1:
@@ -357,6 +362,7 @@ def main():
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "bf16 in / fp32 attention / fp64 eviction", "data": "synthetic (deterministic bf16 q/k/v, scripted labels)",
         "config": {**config, "context_steps": ctx, "timed_positions": [ctx + W, ctx + W + K - 1],
+                   "refresh_boundaries_in_window": sum(1 for p in range(ctx + W, ctx + W + K) if p > 0 and p % args.tau == 0),
                    "l2": (f"K1 reads {bytes_k1['algorithmic_bytes'] / 1e9:.2f} GB per step (compressed KV), larger "
                           "than the 126 MB L2: no flush needed")
                          if bytes_k1["algorithmic_bytes"] > 126e6 else
