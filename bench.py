@@ -263,9 +263,9 @@ def main():
         return
 
     if args.steps % args.tau and rank == 0:
-        print(f"[bench] note: --steps {args.steps} is not a multiple of tau={args.tau}; the timed window "
-              "(the steps just before a refresh boundary) then holds no eviction wave, so TPOT is the "
-              "between-boundary TPOT, not the tau-period average the default --steps 128 measures",
+        print(f"[bench] note: --steps {args.steps} is not a multiple of tau={args.tau}: the timed window does "
+              "not cover whole tau periods, so its TPOT is not the tau-period average the default --steps 128 "
+              "measures (config.refresh_boundaries_in_window says how many eviction waves it holds)",
               file=sys.stderr)
     import torch
     torch.cuda.set_device(local)
