@@ -39,6 +39,37 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return r;
 }
 
+// Division-free encoders for inputs with <= 24 significant bits (bf16/f32).
+// The reference rounds q = x / s in double and then picks the nearest grid
+// point (NVFP4, ties to the even index, quant.cpp:114-130) or clamps
+// rint(q) (ternary, quant.cpp:141-158).  Every decision boundary is a grid
+// midpoint M, and s * M (E4M3 scale x midpoint, <= 7 significant bits) is
+// exact in fp64.  If x / s != M exactly, x - s*M is a multiple of the
+// coarser of the two quanta, >= 2^-26 relative to M, so RN(x / s) lies
+// strictly on the same side of M as x / s: comparing |x| with s*M takes the
+// same branch, and |x| == s*M is exactly the reference's tie.  fp64 inputs
+// keep the division.
+__device__ __forceinline__ uint8_t nvfp4_encode_cmp(double x, double s) {
+  const double a = fabs(x);
+  // midpoints between grid indices k, k+1 of {0, .5, 1, 1.5, 2, 3, 4, 6}; a tie
+  // goes to the even index: counted when k + 1 is even
+  int i = 0;
+  i += a > s * 0.25;
+  i += a >= s * 0.75;
+  i += a > s * 1.25;
+  i += a >= s * 1.75;
+  i += a > s * 2.5;
+  i += a >= s * 3.5;
+  i += a > s * 5.0;
+  if (i == 0) return 0;
+  return (signbit(x) ? 0x8 : 0x0) | (uint8_t)i;
+}
+__device__ __forceinline__ uint8_t ternary_encode_cmp(double x, double delta) {
+  // clamp(rint(x / delta), -1, 1): |x / delta| <= 0.5 rounds to (signed) 0
+  if (!(fabs(x) > delta * 0.5)) return tkv_ternary_bits(0);
+  return tkv_ternary_bits(x > 0.0 ? 1 : -1);
+}
+
 struct FlushSmem {
   int32_t claim[64];
   int8_t reuse[64];
@@ -97,6 +128,7 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
       if (threadIdx.x == 0) { sm.kf = kf; sm.vf = vf; }
     } else {
       bool b2 = false;
+      const bool narrow = dm.in_dtype != TKV_IN_F64;  // <= 24 significant bits: division-free encoders
       // keys: one group per channel over the window's tokens (zero padding
       // never changes the absmax).
       for (int ch = threadIdx.x; ch < D; ch += blockDim.x) {
@@ -109,16 +141,23 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
           for (int t = 0; t < n; ++t) {
             uint8_t code = 0;
             if (delta > 0.0) {
-              const double r = rint(load_in(bufk, dm.in_dtype, (int64_t)t * D + ch) / delta);
-              code = tkv_ternary_bits((int)fmin(fmax(r, -1.0), 1.0));
+              const double x = load_in(bufk, dm.in_dtype, (int64_t)t * D + ch);
+              if (narrow) {
+                code = ternary_encode_cmp(x, delta);
+              } else {
+                const double r = rint(x / delta);
+                code = tkv_ternary_bits((int)fmin(fmax(r, -1.0), 1.0));
+              }
             }
             kc[t * D + ch] = code;
           }
         } else {
           sc = tkv_e4m3_encode(am / 6.0, &b2);                 // quant.cpp:160-174
           const double s = tkv_e4m3_decode(sc);
-          for (int t = 0; t < n; ++t)
-            kc[t * D + ch] = s > 0.0 ? tkv_nvfp4_encode(load_in(bufk, dm.in_dtype, (int64_t)t * D + ch) / s) : 0;
+          for (int t = 0; t < n; ++t) {
+            const double x = load_in(bufk, dm.in_dtype, (int64_t)t * D + ch);
+            kc[t * D + ch] = s > 0.0 ? (narrow ? nvfp4_encode_cmp(x, s) : tkv_nvfp4_encode(x / s)) : 0;
+          }
         }
         ksc[ch] = sc;
       }
@@ -136,17 +175,23 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
           for (int q = 0; q < len; ++q) {
             uint8_t code = 0;
             if (delta > 0.0) {
-              const double r = rint(load_in(bufv, dm.in_dtype, (int64_t)t * D + base + q) / delta);
-              code = tkv_ternary_bits((int)fmin(fmax(r, -1.0), 1.0));
+              const double x = load_in(bufv, dm.in_dtype, (int64_t)t * D + base + q);
+              if (narrow) {
+                code = ternary_encode_cmp(x, delta);
+              } else {
+                const double r = rint(x / delta);
+                code = tkv_ternary_bits((int)fmin(fmax(r, -1.0), 1.0));
+              }
             }
             vc[t * D + base + q] = code;
           }
         } else {
           sc = tkv_e4m3_encode(am / 6.0, &b2);
           const double s = tkv_e4m3_decode(sc);
-          for (int q = 0; q < len; ++q)
-            vc[t * D + base + q] =
-                s > 0.0 ? tkv_nvfp4_encode(load_in(bufv, dm.in_dtype, (int64_t)t * D + base + q) / s) : 0;
+          for (int q = 0; q < len; ++q) {
+            const double x = load_in(bufv, dm.in_dtype, (int64_t)t * D + base + q);
+            vc[t * D + base + q] = s > 0.0 ? (narrow ? nvfp4_encode_cmp(x, s) : tkv_nvfp4_encode(x / s)) : 0;
+          }
         }
         vsc[t * vch + j] = sc;
       }
