@@ -96,6 +96,10 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
   uint8_t* vc = kc + 64 * D;                 // [n][D] value codes
   uint8_t* ksc = vc + 64 * D;                // [D] key scale codes
   uint8_t* vsc = ksc + D;                    // [n][vchunks] value scale codes
+  // block-table columns staged for the serial claim (thought, filled, evict mask)
+  uint32_t* ev_s = reinterpret_cast<uint32_t*>(dyn + (((int64_t)64 * D * 2 + D + 64 * dm.vchunks + 15) / 16 * 16));
+  int8_t* th_s = reinterpret_cast<int8_t*>(ev_s + P);
+  uint8_t* fl_s = reinterpret_cast<uint8_t*>(th_s + P);
   const int64_t buf_elems = (int64_t)g * D;
   const uint8_t* bufk = st.buf + ((int64_t)u * 4 + half * 2 + 0) * buf_elems * dm.in_bytes;
   const uint8_t* bufv = st.buf + ((int64_t)u * 4 + half * 2 + 1) * buf_elems * dm.in_bytes;
@@ -198,6 +202,11 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
       if (b2) atomicExch(&sm.bad, 1);
     }
   }
+  for (int b = threadIdx.x; b < P; b += blockDim.x) {
+    th_s[b] = st.blk_thought[(int64_t)u * P + b];
+    fl_s[b] = st.blk_filled[(int64_t)u * P + b];
+    ev_s[b] = st.blk_evict[(int64_t)u * P + b];
+  }
   __syncthreads();
 
   // ---- phase B: ordered claim + block-table bookkeeping (one thread) -----
@@ -218,8 +227,8 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
     if (sm.abort_code == 0) {
       // (1) soft-evicted slots of same-thought blocks, physical order.
       for (int b = 0; b < P && claims < n; ++b) {
-        if (th[b] != c.band) continue;
-        uint32_t m = ev[b] & (fl[b] >= 32 ? 0xffffffffu : ((1u << fl[b]) - 1u));
+        if (th_s[b] != c.band) continue;
+        uint32_t m = ev_s[b] & (fl_s[b] >= 32 ? 0xffffffffu : ((1u << fl_s[b]) - 1u));
         while (m && claims < n) {
           const int s = __ffs(m) - 1;
           m &= m - 1;
@@ -230,8 +239,8 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
       }
       // (2) unfilled tail slots of same-thought blocks.
       for (int b = 0; b < P && claims < n; ++b) {
-        if (th[b] != c.band) continue;
-        for (int s = fl[b]; s < bs && claims < n; ++s) {
+        if (th_s[b] != c.band) continue;
+        for (int s = fl_s[b]; s < bs && claims < n; ++s) {
           sm.claim[claims] = b * bs + s;
           sm.reuse[claims] = 0;
           ++claims;
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
         sm.abort_code = TKV_E_OOM;
       } else {
         for (int b = 0, got = 0; b < P && got < fresh; ++b) {
-          if (th[b] != -1) continue;
+          if (th_s[b] != -1) continue;
           th[b] = (int8_t)c.band;  // allocate_block (pager.cpp:28-47)
           fl[b] = 0;
           ev[b] = 0;
@@ -368,7 +377,12 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
 cudaError_t tkv_launch_flush(const TkvState& st, int half, int n, int pos0, const TkvFlushCtl* ctl,
                              int units_per_group, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  const size_t smem = (size_t)64 * st.dm.D * 2 + st.dm.D + (size_t)64 * st.dm.vchunks;
+  const size_t smem = ((size_t)64 * st.dm.D * 2 + st.dm.D + (size_t)64 * st.dm.vchunks + 15) / 16 * 16 +
+                      (size_t)st.dm.P * 6;  // + staged block-table columns
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   flush_kernel<<<st.dm.U, 128, smem, stream>>>(st, half, n, pos0, ctl, units_per_group);
   return cudaGetLastError();
 }
