@@ -1234,6 +1234,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     }
   }
   __syncthreads();
+  const RowSplit rsd(D);  // idx -> (centroid, channel) without integer division
   long long tk0 = clock64();
   for (int r = warp; r < nr; r += kTinyWarps) {
     // ---- seeds -------------------------------------------------------------------
@@ -1262,7 +1263,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     }
     __syncwarp();
     for (int idx = lane; idx < K * D; idx += 32) {
-      const int c = idx / D, ch = idx - c * D;
+      const int c = rsd.row(idx), ch = rsd.col(idx);
       Mn[idx] = xval(X, xs, w.seeds[c], ch, XS, scaled);
     }
     __syncwarp();
@@ -1304,7 +1305,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
       __syncwarp();
       // next centroids: member sums in point order / size (lanes = channels)
       for (int idx = lane; idx < K * D; idx += 32) {
-        const int c = idx / D, ch = idx - c * D;
+        const int c = rsd.row(idx), ch = rsd.col(idx);
         double acc = 0.0;
         unsigned mm = w.members[c];
         while (mm) {
@@ -1392,7 +1393,7 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
     __syncwarp();
     // ---- Hartigan (evictor.cpp:167-243) ---------------------------------------------
     for (int idx = lane; idx < K * D; idx += 32) {
-      const int c = idx / D, ch = idx - c * D;
+      const int c = rsd.row(idx), ch = rsd.col(idx);
       double acc = 0.0;
       unsigned mm = w.members[c];
       while (mm) {
