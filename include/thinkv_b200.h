@@ -154,6 +154,14 @@ int tkv_dump_json(tkv_run* run, int seq, const char* what, char* buf, size_t cap
  * pager.cpp:299-325, extended with buffer/q/out/metadata bytes). */
 int tkv_bytes(tkv_run* run, tkv_bytes_t* out);
 
+/* Per-launch byte accounting on the device (k_bytes.cu): while enabled,
+ * every attention launch is followed by a kernel that computes, from the
+ * state that launch read, the same algorithmic bytes as tkv_bytes; the
+ * counts are summed over launches.  Enabling resets the sums.  Reading
+ * synchronises; *launches = attention launches accounted. */
+int tkv_bytes_accounting(tkv_run* run, int enable);
+int tkv_bytes_accumulated(tkv_run* run, tkv_bytes_t* sum, int64_t* launches);
+
 /* Compressed-cache export: the live pager tokens of units
  * [unit0, unit0 + nunits) as QuantizedGroups in the reference wire layout of
  * serialize_group (proj/src/quant.cpp:274-324, quant.hpp:104-110), one byte
@@ -164,7 +172,8 @@ int tkv_bytes(tkv_run* run, tkv_bytes_t* out);
 int tkv_export_cache(tkv_run* run, int64_t unit0, int64_t nunits, void* dst, size_t cap, int64_t* unit_offsets,
                      size_t* needed);
 
-/* Last fp64 per-unit sparsity (layer_sparsity_average) computed on a refresh step. */
+/* Last fp64 per-unit sparsity (layer_sparsity_average) computed on a refresh step.  It is computed only
+ * where something consumes it: calibrated labels, an event log (record_events) or a sparsity trace. */
 int tkv_unit_sparsity(tkv_run* run, double* out, int64_t n);
 
 /* Per-kernel device time of the run's launches (CUDA events on the run's

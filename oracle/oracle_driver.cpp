@@ -322,6 +322,21 @@ class SeqOracle {
     return out;
   }
 
+  json frag() const {  // BlockPager::fragmentation_stats (pager.cpp:299-325), one object per unit
+    json arr = json::array();
+    for (const auto& pg : pagers_) {
+      const FragmentationStats st = pg.fragmentation_stats();
+      arr.push_back(json{{"live_slots", st.live_slots},
+                         {"masked_slots", st.masked_slots},
+                         {"unfilled_slots", st.unfilled_slots},
+                         {"blocks_in_use", st.blocks_in_use},
+                         {"free_blocks", st.free_blocks},
+                         {"live_code_bits", st.total_live_code_bits()},
+                         {"live_code_bits_by_format", st.live_code_bits_by_format},
+                         {"live_scale_bytes", st.live_scale_bytes}});
+    }
+    return arr;
+  }
   json tables() const {  // sim.cpp:939-943
     json arr = json::array();
     for (const auto& pg : pagers_) arr.push_back(pg.dump());
@@ -710,6 +725,8 @@ const char* orc_dump(orc_run* run, int seq, const char* what) {
     run->scratch = run->seqs.at(seq)->tables().dump();
   } else if (w == "segments") {
     run->scratch = run->seqs.at(seq)->segments().dump();
+  } else if (w == "frag") {
+    run->scratch = run->seqs.at(seq)->frag().dump();
   } else if (w == "events") {
     run->scratch = run->seqs.at(seq)->events();
   } else if (w == "step_dumps") {

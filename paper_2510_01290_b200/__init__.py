@@ -222,6 +222,16 @@ class DecodeRun:
         check(lib.tkv_bytes(self._h, C.byref(b)))
         return {n: getattr(b, n) for n, _ in _abi.Bytes._fields_}
 
+    def bytes_accounting(self, enable: bool = True):
+        """Exact per-launch algorithmic bytes on the device (k_bytes.cu); resets the sums."""
+        check(lib.tkv_bytes_accounting(self._h, int(enable)))
+
+    def bytes_accumulated(self):
+        """(sums over the accounted attention launches as in bytes(), launches)."""
+        b, n = _abi.Bytes(), C.c_int64()
+        check(lib.tkv_bytes_accumulated(self._h, C.byref(b), C.byref(n)))
+        return {f: getattr(b, f) for f, _ in _abi.Bytes._fields_}, n.value
+
     def export_cache(self, unit0: int = 0, nunits: int = None):
         """Live pager tokens of units [unit0, unit0 + nunits) in the reference
         wire layout (serialize_group, proj/src/quant.cpp:274-324; stream layout

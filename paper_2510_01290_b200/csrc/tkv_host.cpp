@@ -193,6 +193,10 @@ struct tkv_run {
   double acc_ms[5] = {0, 0, 0, 0, 0};
   int64_t acc_n[5] = {0, 0, 0, 0, 0};
   int64_t launches = 0;
+  // device byte accounting (tkv_bytes_accounting)
+  bool bytes_on = false;
+  unsigned long long* d_bytes_acc = nullptr;  // [5]
+  int64_t bytes_launches = 0, bytes_host = 0;  // accounted launches, host-known bytes (buffer, q, out)
   // host-pointer step staging: two slots, copies on their own stream so the
   // transfers of one step overlap the kernels of its neighbours
   void* d_q[2] = {nullptr, nullptr};
@@ -276,11 +280,14 @@ void validate(const tkv_run_desc& d) {
   } else {
     if (d.num_thresholds != d.num_thoughts - 1) errs.push_back("calibration must carry num_thoughts - 1 thresholds");
     if (d.num_calib_units < 1) errs.push_back("calibration layer subset is empty");
-    for (int i = 0; i < d.num_calib_units; ++i)
+    if (d.num_calib_units > 64) errs.push_back("calibration layer subset holds more than 64 layers");
+    for (int i = 0; i < std::min(d.num_calib_units, 64); ++i)
       if (d.calib_units[i] < 0 || d.calib_units[i] >= d.units_per_seq)
         errs.push_back("calibration layer index out of range");
   }
   if (d.input_dtype < 0 || d.input_dtype > 2) errs.push_back("input_dtype must be bf16, f32 or f64");
+  if (d.num_dump_positions < 0 || (d.num_dump_positions > 0 && !d.dump_positions))
+    errs.push_back("dump positions: negative count or null array");
   if (!errs.empty()) {
     std::string what = "invalid run config:";
     for (const auto& e : errs) what += "\n  - " + e;
@@ -654,7 +661,7 @@ void boundary(tkv_run* r, int64_t pos, bool decode) {
           mean /= (double)U;
         }
       } else {
-        for (int i = 0; i < d.num_calib_units; ++i) mean += sp[(size_t)g.unit0 + d.calib_units[i]];
+        for (int i = 0; i < std::min(d.num_calib_units, 64); ++i) mean += sp[(size_t)g.unit0 + d.calib_units[i]];
         mean /= (double)d.num_calib_units;
         band = 0;
         for (int i = 0; i < d.num_thresholds; ++i)
@@ -990,13 +997,26 @@ void step_attend(tkv_run* r, const StepCtx& c, const void* q, const void* k, con
   r->st.lmap_count = r->desc.num_seqs * lmap_h;
   // 1. attention (+ exact sparsity on refresh steps, where it is consumed, or
   //    on every decode step when a sparsity trace is recorded)
+  //    scripted labels without an event log read no sparsity (boundary(), the
+  //    refresh event's mean), so the score kernel is skipped there.
   const bool trace = c.decode && r->desc.record_sparsity_trace;
-  if ((c.refresh && c.decode) || trace)
+  const bool consumed = c.refresh && c.decode && (!r->desc.scripted || r->desc.record_events);
+  if (consumed || trace)
     launch(r, CAT_SCORE, "score kernel",
            [&] { return tkv_launch_score(r->st, q, k, r->cur_half, r->buf_len, r->stream); });
   launch(r, CAT_ATTEND, "attend kernel", [&] {
     return tkv_launch_attend(r->st, q, k, v, out, r->cur_half, r->buf_len, c.put_half, c.put_slot, r->stream);
   });
+  if (r->bytes_on) {
+    r->launches += 1;
+    check_launch(tkv_launch_bytes(r->st, r->d_bytes_acc, r->stream), "bytes kernel");
+    const TkvDims& dm = r->st.dm;
+    const int64_t n = tkv_launch_units(r->st);
+    const int rows = dm.maxpool ? 1 : dm.G;
+    r->bytes_host += n * ((int64_t)(r->buf_len + 1) * 2 * dm.D * dm.in_bytes +
+                          (int64_t)dm.G * dm.D * dm.in_bytes + (int64_t)rows * dm.D * 4);
+    if (lmap_h == 0 || layer == 0) r->bytes_launches += 1;
+  }
   r->st.lmap_h = 0;
 }
 
@@ -1147,6 +1167,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   st.max_live = st.dm.NS;
   if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 256, 0);
   st.err = dalloc<int32_t>(r, U);
+  r->d_bytes_acc = dalloc<unsigned long long>(r, 5, 0);
   check_launch(tkv_launch_init(st, r->stream), "init kernel");
   // arenas
   r->arena_cap = 8 << 20;
@@ -1231,7 +1252,7 @@ int64_t live_bytes_stats(tkv_run* r, tkv_bytes_t* out) {
         if ((ev[u * dm.P + b] >> s) & 1u) continue;
         out->live_slots += 1;
         out->live_code_bytes += 2 * (int64_t)dm.band_bytes[t];
-        out->meta_bytes += 8;  // slot -> window index + live-list entry
+        out->meta_bytes += 4;  // slot -> window index (the live list K1 builds is in shared memory)
         if (fmt == TKV_FMT_RAW) continue;
         const int w = swin[u * dm.NS + (size_t)b * dm.bs + s];
         if (fmt == TKV_FMT_FP8) {
@@ -1515,6 +1536,51 @@ int tkv_bytes(tkv_run* run, tkv_bytes_t* out) {
     return TKV_OK;
   } catch (const TkvError& e) {
     return fail(e);
+  }
+}
+
+int tkv_bytes_accounting(tkv_run* run, int enable) {
+  try {
+    if (!run) throw TkvError(TKV_ERR_CONFIG, "null run");
+    CUDA_OK(cudaMemsetAsync(run->d_bytes_acc, 0, 5 * sizeof(unsigned long long), run->stream));
+    run->bytes_launches = 0;
+    run->bytes_host = 0;
+    run->bytes_on = enable != 0;
+    return 0;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_bytes_accumulated(tkv_run* run, tkv_bytes_t* sum, int64_t* launches) {
+  try {
+    if (!run || !sum) throw TkvError(TKV_ERR_CONFIG, "null argument");
+    unsigned long long acc[5];
+    CUDA_OK(cudaMemcpyAsync(acc, run->d_bytes_acc, sizeof(acc), cudaMemcpyDeviceToHost, run->stream));
+    CUDA_OK(cudaStreamSynchronize(run->stream));
+    std::memset(sum, 0, sizeof(*sum));
+    sum->live_slots = (int64_t)acc[0];
+    sum->resident_slots = (int64_t)acc[1];
+    sum->live_code_bytes = (int64_t)acc[2];
+    sum->live_scale_bytes = (int64_t)acc[3];
+    sum->meta_bytes = (int64_t)acc[4];
+    const TkvDims& dm = run->st.dm;
+    const int rows = dm.maxpool ? 1 : dm.G;
+    const int64_t qo = (int64_t)dm.G * dm.D * dm.in_bytes + (int64_t)rows * dm.D * 4;
+    // host-known bytes: split back into buffer and q/out parts
+    const int64_t unit_launches = run->bytes_launches * (int64_t)dm.U;
+    sum->qo_bytes = unit_launches * qo;
+    sum->buffer_bytes = run->bytes_host - sum->qo_bytes;
+    sum->algorithmic_bytes = sum->live_code_bytes + sum->live_scale_bytes + sum->buffer_bytes + sum->qo_bytes +
+                             sum->meta_bytes;
+    if (launches) *launches = run->bytes_launches;
+    return 0;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
   }
 }
 

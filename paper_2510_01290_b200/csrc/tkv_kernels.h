@@ -17,6 +17,11 @@ bool tkv_attend_mma_supported(const TkvDims& dm);
 cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void* k, const void* v, float* out,
                                   int buf_half, int nbuf, int put_half, int put_slot, cudaStream_t stream);
 
+// Algorithmic-byte accounting of the state an attention launch reads
+// (k_bytes.cu): adds live slots, resident slots, live code bytes, live scale
+// bytes and metadata bytes of every launched unit to acc[0..5).
+cudaError_t tkv_launch_bytes(const TkvState& st, unsigned long long* acc, cudaStream_t stream);
+
 // K3a: fp64 sparsity statistics (layer_sparsity_average) over the same view.
 cudaError_t tkv_launch_score(const TkvState& st, const void* q, const void* k, int buf_half,
                              int nbuf, cudaStream_t stream);

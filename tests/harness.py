@@ -96,6 +96,7 @@ def compare_export(res, cfg):
 def compare_state(res, cfg, finish=True):
     run, orc = res["run"], res["oracle"]
     compare_export(res, cfg)
+    compare_bytes(run, [orc])
     if finish:
         run.finish()
         orc.finish()
@@ -111,3 +112,107 @@ def compare_state(res, cfg, finish=True):
             assert run.step_dumps(s) == orc.dump(s, "step_dumps"), f"seq {s}: step dumps differ"
         if finish:
             assert run.metrics(s) == orc.dump(s, "metrics"), f"seq {s}: metrics differ"
+
+
+def unit_subset_config(cfg, units):
+    """A run of len(units) one-unit sequences that is, unit for unit, the same
+    decode as units `units` of `cfg` (scripted labels are per sequence and
+    units are independent): unit u keeps its sequence's script."""
+    ups = cfg.units_per_seq
+    return dataclasses.replace(cfg, num_seqs=len(units), units_per_seq=1,
+                               script=[list(cfg.script[u // ups]) for u in units])
+
+
+def run_parity_units(cfg, units, seed=0x71534B56, steps=None, check=()):
+    """GPU vs oracle over global units `units` of `cfg` (inputs of those
+    global units, generated as cfg generates them) for `steps` steps.  The
+    oracle decodes each unit on its own thread, concurrently with the GPU.
+    Outputs are compared at the positions in `check`; returns the same dict
+    as run_parity with one OracleRun per unit under "oracles"."""
+    import threading
+
+    import torch
+    from paper_2510_01290_b200 import DecodeRun
+
+    steps = steps if steps is not None else cfg.prompt_len + cfg.max_gen_len
+    sub = unit_subset_config(cfg, units)
+    check = set(check)
+    G, D, ups = cfg.num_q_heads, cfg.head_dim, cfg.units_per_seq
+    orcs = [O.OracleRun(oracle_config(unit_subset_config(cfg, [u]))) for u in units]
+    ref_outs = [dict() for _ in units]
+    errs = []
+
+    def worker(i):
+        try:
+            for t in range(steps):
+                q, k, v = O.synth_step(seed, ups, cfg.tau, 1, G, D, t, unit0=units[i])
+                out, _ = orcs[i].step(O.bf16_to_f64(q), O.bf16_to_f64(k), O.bf16_to_f64(v))
+                if t in check:
+                    ref_outs[i][t] = out[0].copy()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(len(units))]
+    for th in threads:
+        th.start()
+    run = DecodeRun(sub)
+    dev = torch.device("cuda:0")
+    out = torch.empty((len(units), sub.out_rows, D), dtype=torch.float32, device=dev)
+    got = {}
+    for t in range(steps):
+        parts = [O.synth_step(seed, ups, cfg.tau, 1, G, D, t, unit0=u) for u in units]
+        q, k, v = (np.concatenate([p[j] for p in parts]) for j in range(3))
+        tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev) for x in (q, k, v))
+        run.step(tq, tk, tv, out)
+        if t in check:
+            got[t] = out.double().cpu().numpy()
+    run.synchronize()
+    for th in threads:
+        th.join()
+    if errs:
+        raise errs[0]
+    max_err = 0.0
+    for t, g in got.items():
+        for i in range(len(units)):
+            ref = ref_outs[i][t]
+            err = float(np.max(np.abs(g[i] - ref)))
+            scale = float(np.max(np.abs(ref)))
+            assert err <= ATOL + RTOL * scale, f"step {t} unit {units[i]}: attention error {err} (scale {scale})"
+            max_err = max(max_err, err)
+    return {"max_err": max_err, "run": run, "oracles": orcs, "steps": steps, "config": sub}
+
+
+def compare_units_state(res, finish=True):
+    """compare_state for run_parity_units: unit i of the GPU run against its
+    own OracleRun (tables, segments, events, export bytes, fragmentation
+    byte accounting, metrics)."""
+    run, orcs, sub = res["run"], res["oracles"], res["config"]
+    buf, offs = run.export_cache()
+    host = buf.cpu().numpy().tobytes()
+    for i, orc in enumerate(orcs):
+        assert host[offs[i]:offs[i + 1]] == orc.export(0, 0), f"unit {i}: export differs"
+    compare_bytes(run, orcs)
+    if finish:
+        run.finish()
+        for orc in orcs:
+            orc.finish()
+    for i, orc in enumerate(orcs):
+        assert run.tables(i) == orc.dump(0, "tables"), f"unit {i}: block tables differ"
+        assert run.segments(i) == orc.dump(0, "segments"), f"unit {i}: segments differ"
+        if sub.record_events:
+            assert run.events(i).splitlines() == orc.dump(0, "events").splitlines(), f"unit {i}: events differ"
+        if finish:
+            assert run.metrics(i) == orc.dump(0, "metrics"), f"unit {i}: metrics differ"
+
+
+def compare_bytes(run, orcs):
+    """Byte accounting (tkv_bytes, the roofline numerator) against the
+    reference's BlockPager::fragmentation_stats (pager.cpp:299-325) summed
+    over units: live slots, live code bits, live scale bytes."""
+    frag = [f for orc in orcs for seq in range(orc.cfg.num_seqs) for f in orc.dump(seq, "frag")]
+    b = run.bytes()
+    assert b["live_slots"] == sum(f["live_slots"] for f in frag)
+    assert b["resident_slots"] == sum(f["live_slots"] + f["masked_slots"] for f in frag)
+    assert b["live_code_bytes"] * 8 == sum(f["live_code_bits"] for f in frag)
+    assert b["live_scale_bytes"] == sum(f["live_scale_bytes"] for f in frag)
+    return b

@@ -21,3 +21,31 @@ def test_reference_arm_line():
     assert line["e2e"] == {"value": line["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert line["config"]["global_batch"] == 1 and line["scaling"] == "weak"
+
+
+def test_reference_arm_does_not_map_the_cuda_library():
+    """The reference arm imports the package only for its configuration types;
+    the CUDA library loads lazily, so that process never maps it."""
+    code = ("import sys; sys.argv = ['bench.py', '--impl', 'reference', '--config', '1', '--max-gen', '300', "
+            "'--steps', '2', '--warmup', '1', '--e2e-steps', '1']; import bench; bench.main(); "
+            "maps = open('/proc/self/maps').read(); assert 'libthinkv_b200' not in maps, 'mapped'; "
+            "assert 'liboracle' in maps")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+
+
+def test_amortised_tpot():
+    sys.path.insert(0, ROOT)
+    import bench
+    # window of whole tau periods: plain mean
+    steps = [10.0] + [1.0] * 3 + [10.0] + [1.0] * 3
+    assert bench.amortize(steps, 8, 4)[0] == sum(steps) / len(steps)
+    # short window opening on a boundary: the boundary is weighted 1/tau
+    tpot, bnd, oth = bench.amortize([130.0, 1.0, 1.0], 256, 128)
+    assert bnd == [130.0] and oth == [1.0, 1.0] and abs(tpot - (130.0 + 127.0) / 128) < 1e-12
+    # first timed position: a boundary leaving room for K + E steps
+    class A:
+        ctx, warmup, steps, e2e_steps = None, 5, 20, 128
+    class Cfg:
+        max_gen_len, tau = 32768, 128
+    assert bench.positions(A, Cfg) == 32512
