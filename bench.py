@@ -284,6 +284,8 @@ def main():
     ap.add_argument("--psi", type=int, nargs=3, default=None, help="bits per band E R T")
     ap.add_argument("--pT-permille", type=int, default=100)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline and its parity check")
+    ap.add_argument("--no-bytes-accounting", action="store_true",
+                    help="diagnostic: skip the per-launch device byte accounting (roofline numerator)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: --seqs per GPU (default); strong: --seqs in total, split over the GPUs")
     args = ap.parse_args()
@@ -352,7 +354,7 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     run.timing_enable(True)
-    run.bytes_accounting(True)
+    run.bytes_accounting(not args.no_bytes_accounting)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)

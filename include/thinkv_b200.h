@@ -162,6 +162,11 @@ int tkv_bytes(tkv_run* run, tkv_bytes_t* out);
 int tkv_bytes_accounting(tkv_run* run, int enable);
 int tkv_bytes_accumulated(tkv_run* run, tkv_bytes_t* sum, int64_t* launches);
 
+/* y[i] = exp(x[i]) for HOST arrays, evaluated on the device with the exp the
+ * fp64 kernels use (K3a sparsity, exact gather scores): glibc's exp
+ * (attention.cpp:62 calls it through std::exp) restated bit for bit. */
+int tkv_exp_f64(tkv_ctx* ctx, const double* x, double* y, int64_t n);
+
 /* Compressed-cache export: the live pager tokens of units
  * [unit0, unit0 + nunits) as QuantizedGroups in the reference wire layout of
  * serialize_group (proj/src/quant.cpp:274-324, quant.hpp:104-110), one byte

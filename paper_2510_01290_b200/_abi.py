@@ -19,7 +19,7 @@ EXPORTS = (
     "tkv_last_error", "tkv_abi_version", "tkv_init", "tkv_ctx_destroy", "tkv_run_create",
     "tkv_run_destroy", "tkv_step", "tkv_step_layer", "tkv_step_host", "tkv_finish", "tkv_synchronize",
     "tkv_position", "tkv_dump_json", "tkv_bytes", "tkv_unit_sparsity", "tkv_synth_inputs",
-    "tkv_timing_enable", "tkv_timing_read", "tkv_bytes_accounting", "tkv_bytes_accumulated", "tkv_step_host_async", "tkv_export_cache",
+    "tkv_timing_enable", "tkv_timing_read", "tkv_bytes_accounting", "tkv_bytes_accumulated", "tkv_exp_f64", "tkv_step_host_async", "tkv_export_cache",
     "tkv_gather_create", "tkv_gather_destroy", "tkv_gather_step", "tkv_gather_stats", "tkv_gather_ids",
 )
 
@@ -95,6 +95,7 @@ def _load():
     L.tkv_dump_json.argtypes = [vp, C.c_int, C.c_char_p, C.c_char_p, C.c_size_t,
                                 C.POINTER(C.c_size_t)]
     L.tkv_bytes.argtypes = [vp, C.POINTER(Bytes)]
+    L.tkv_exp_f64.argtypes = [vp, vp, vp, C.c_int64]
     L.tkv_bytes_accounting.argtypes = [vp, C.c_int]
     L.tkv_bytes_accumulated.argtypes = [vp, C.POINTER(Bytes), C.POINTER(C.c_int64)]
     L.tkv_export_cache.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_size_t, vp, C.POINTER(C.c_size_t)]
@@ -113,12 +114,14 @@ def _load():
 class _LazyLib:
     """Proxy for the CDLL: resolves it on the first attribute access."""
 
-    _cdll = None
+    def __init__(self):
+        self.__dict__["_cdll"] = None
 
     def __getattr__(self, name):
-        if _LazyLib._cdll is None:
-            _LazyLib._cdll = _load()
-        return getattr(_LazyLib._cdll, name)
+        cdll = self.__dict__["_cdll"]
+        if cdll is None:
+            cdll = self.__dict__["_cdll"] = _load()
+        return getattr(cdll, name)
 
 
 lib = _LazyLib()

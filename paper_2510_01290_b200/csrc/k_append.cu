@@ -221,8 +221,8 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
     uint8_t* fl = st.blk_filled + (int64_t)u * P;
     uint32_t* ev = st.blk_evict + (int64_t)u * P;
     uint8_t* ns = st.blk_nstart + (int64_t)u * P;
-    int32_t* sstart = st.blk_start + (int64_t)u * P * (bs + 1);
-    uint32_t* smask = st.blk_segmask + (int64_t)u * P * bs;
+    int32_t* sstart = st.blk_start + (int64_t)u * P * TKV_STARTS_PER_BLOCK(bs);
+    uint32_t* smask = st.blk_segmask + (int64_t)u * P * TKV_MASKS_PER_BLOCK(bs);
     int claims = 0;
     if (sm.abort_code == 0) {
       // (1) soft-evicted slots of same-thought blocks, physical order.
@@ -286,8 +286,8 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
       for (int i = 0; i < n && sm.abort_code == 0; ++i) {
         const int b = sm.claim[i] / bs, s = sm.claim[i] % bs;
         const uint32_t bit = 1u << s;
-        int32_t* starts = sstart + (int64_t)b * (bs + 1);
-        uint32_t* masks = smask + (int64_t)b * bs;
+        int32_t* starts = sstart + (int64_t)b * TKV_STARTS_PER_BLOCK(bs);
+        uint32_t* masks = smask + (int64_t)b * TKV_MASKS_PER_BLOCK(bs);
         if (sm.reuse[i]) {
           ev[b] &= ~bit;
           for (int k = 0; k + 1 < ns[b]; ++k) masks[k] &= ~bit;

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include "tkv_exp.cuh"
 #include "tkv_kernels.h"
 
 namespace {
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(kThreads) gather_step_kernel(TkvGatherState g,
       __syncthreads();
       mx = redd[0];
       for (int w = 1; w < kWarps; ++w) mx = fmax(mx, redd[w]);
-      for (int i = threadIdx.x; i < rows; i += kThreads) sc[i] = exp(__dsub_rn(sc[i], mx));
+      for (int i = threadIdx.x; i < rows; i += kThreads) sc[i] = tkv_exp(__dsub_rn(sc[i], mx));
       __syncthreads();
       if (threadIdx.x == 0) {  // softmax denominator in index order (attention.cpp:59-63)
         double s = 0.0;

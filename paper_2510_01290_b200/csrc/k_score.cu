@@ -17,8 +17,8 @@
 //     logit gives exp(0) = 1 and division by sum is monotone), threshold =
 //     frac * that, count s_i < threshold strictly;
 //   * layer average: sum of per-row sparsities in row order / rows.
-// exp is CUDA's double exp (<= 1 ulp, like glibc's); a differing last bit can
-// only change a count when e_i / sum lands within an ulp of the threshold.
+// exp is tkv_exp (tkv_exp.cuh): glibc's exp restated bit for bit, so every e_i,
+// the sum and every s_i carry the reference's exact bits.
 //
 // Layout: one CTA (256 threads) per unit.  The unit's live slots are listed in
 // physical (block, slot) order (BlockPager::read_active, pager.cpp:261-271),
@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include "tkv_exp.cuh"
 #include "tkv_kernels.h"
 #include "tkv_state.h"
 
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(TkvState st, const void
       double m = red[0][r];
       for (int w = 1; w < kWarps; ++w) m = fmax(m, red[w][r]);
       double* L = lg + (int64_t)r * nmax;
-      for (int i = threadIdx.x; i < n; i += kThreads) L[i] = exp(__dsub_rn(L[i], m));
+      for (int i = threadIdx.x; i < n; i += kThreads) L[i] = tkv_exp(__dsub_rn(L[i], m));
     }
     __syncthreads();
     // ---- denominators: one lane per row, index order, loads batched ahead -----------

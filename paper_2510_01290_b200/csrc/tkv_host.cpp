@@ -734,8 +734,8 @@ std::vector<UnitSnap> snapshot(tkv_run* r, int u0, int n) {
     d2h(r, s.fl, r->st.blk_filled + u * dm.P, dm.P);
     d2h(r, s.ns, r->st.blk_nstart + u * dm.P, dm.P);
     d2h(r, s.ev, r->st.blk_evict + u * dm.P, dm.P);
-    d2h(r, s.smask, r->st.blk_segmask + u * dm.P * dm.bs, (size_t)dm.P * dm.bs);
-    d2h(r, s.start, r->st.blk_start + u * dm.P * (dm.bs + 1), (size_t)dm.P * (dm.bs + 1));
+    d2h(r, s.smask, r->st.blk_segmask + u * dm.P * TKV_MASKS_PER_BLOCK(dm.bs), (size_t)dm.P * TKV_MASKS_PER_BLOCK(dm.bs));
+    d2h(r, s.start, r->st.blk_start + u * dm.P * TKV_STARTS_PER_BLOCK(dm.bs), (size_t)dm.P * TKV_STARTS_PER_BLOCK(dm.bs));
     d2h(r, s.sid, r->st.slot_id + u * dm.NS, dm.NS);
     d2h(r, s.swin, r->st.slot_win + u * dm.NS, dm.NS);
     d2h(r, s.wrefs, r->st.win_refs + u * dm.NW, dm.NW);
@@ -769,10 +769,10 @@ json table_json(const tkv_run* r, const UnitSnap& s) {  // BlockPager::dump (pag
     e["filled"] = (int)s.fl[b];
     e["thought"] = (int)s.th[b];
     std::vector<int64_t> starts;
-    for (int k = 0; k < s.ns[b]; ++k) starts.push_back(s.start[(size_t)b * (dm.bs + 1) + k]);
+    for (int k = 0; k < s.ns[b]; ++k) starts.push_back(s.start[(size_t)b * TKV_STARTS_PER_BLOCK(dm.bs) + k]);
     e["start_indices"] = starts;
     json masks = json::array();
-    for (int k = 0; k + 1 < s.ns[b]; ++k) masks.push_back(mask_string(s.smask[(size_t)b * dm.bs + k], dm.bs));
+    for (int k = 0; k + 1 < s.ns[b]; ++k) masks.push_back(mask_string(s.smask[(size_t)b * TKV_MASKS_PER_BLOCK(dm.bs) + k], dm.bs));
     e["segment_masks"] = masks;
     e["eviction_mask"] = mask_string(s.ev[b], dm.bs);
     json toks = json::array();
@@ -1143,8 +1143,8 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   st.blk_filled = dalloc<uint8_t>(r, U * dm.P, 0);
   st.blk_evict = dalloc<uint32_t>(r, U * dm.P, 0);
   st.blk_nstart = dalloc<uint8_t>(r, U * dm.P, 0);
-  st.blk_start = dalloc<int32_t>(r, U * dm.P * (dm.bs + 1), 0);
-  st.blk_segmask = dalloc<uint32_t>(r, U * dm.P * dm.bs, 0);
+  st.blk_start = dalloc<int32_t>(r, U * dm.P * TKV_STARTS_PER_BLOCK(dm.bs), 0);
+  st.blk_segmask = dalloc<uint32_t>(r, U * dm.P * TKV_MASKS_PER_BLOCK(dm.bs), 0);
   st.unit_nfree = dalloc<int32_t>(r, U);
   st.slot_k = dalloc<uint8_t>(r, U * dm.NS * dm.kstride, 0);
   st.slot_v = dalloc<uint8_t>(r, U * dm.NS * dm.kstride, 0);
@@ -1536,6 +1536,26 @@ int tkv_bytes(tkv_run* run, tkv_bytes_t* out) {
     return TKV_OK;
   } catch (const TkvError& e) {
     return fail(e);
+  }
+}
+
+int tkv_exp_f64(tkv_ctx* ctx, const double* x, double* y, int64_t n) {
+  try {
+    if (!ctx || (n > 0 && (!x || !y))) throw TkvError(TKV_ERR_CONFIG, "null argument");
+    if (n <= 0) return TKV_OK;
+    CUDA_OK(cudaSetDevice(ctx->device));
+    double* d = nullptr;
+    CUDA_OK(cudaMalloc(&d, 2 * n * sizeof(double)));
+    cudaError_t e = cudaMemcpy(d, x, n * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = tkv_launch_exp(d, d + n, n, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(y, d + n, n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CUDA_OK(e);
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
   }
 }
 

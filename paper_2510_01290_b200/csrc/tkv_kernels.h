@@ -22,6 +22,9 @@ cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void*
 // bytes and metadata bytes of every launched unit to acc[0..5).
 cudaError_t tkv_launch_bytes(const TkvState& st, unsigned long long* acc, cudaStream_t stream);
 
+// y[i] = tkv_exp(x[i]) (k_math.cu): glibc's exp, bit for bit.
+cudaError_t tkv_launch_exp(const double* x, double* y, int64_t n, cudaStream_t stream);
+
 // K3a: fp64 sparsity statistics (layer_sparsity_average) over the same view.
 cudaError_t tkv_launch_score(const TkvState& st, const void* q, const void* k, int buf_half,
                              int nbuf, cudaStream_t stream);

@@ -8,9 +8,14 @@
 //
 // HBM layout (SoA; P = pool blocks per unit, bs = block size, NS = P*bs):
 //   block table   thought[P] i8, filled[P] u8, evict[P] u32 (slot bitmask),
-//                 nstart[P] u8, start[P][bs+1] i32, segmask[P][bs] u32
+//                 nstart[P] u8, start[P][bs+2] i32, segmask[P][bs+1] u32
 //                 -- BlockTableEntry (pager.hpp:55-62) with the segment masks
 //                 stored as bitmasks, one per start index beyond the first.
+//                 Masks are disjoint and non-empty after pruning, so a block
+//                 holds at most bs masks + the implicit first segment; while a
+//                 placement runs (pager.cpp:190-216: append the new segment's
+//                 mask, then prune the ones its reuse emptied) there can be one
+//                 more of each, hence bs + 2 starts and bs + 1 masks.
 //   slots         kcode[NS][kstride] u8, vcode[NS][vstride] u8 (packed 2/4/8-bit
 //                 codes, or raw input-dtype values for 16-bit passthrough),
 //                 vscale[NS][vchunks] u8 (E4M3 per-token value-chunk scales),
@@ -27,6 +32,8 @@
 
 #define TKV_MAX_BANDS 8
 #define TKV_MAX_G 16
+#define TKV_STARTS_PER_BLOCK(bs) ((bs) + 2)
+#define TKV_MASKS_PER_BLOCK(bs) ((bs) + 1)
 
 enum { TKV_FMT_TERNARY = 0, TKV_FMT_NVFP4 = 1, TKV_FMT_FP8 = 2, TKV_FMT_RAW = 3 };
 enum { TKV_IN_BF16 = 0, TKV_IN_F32 = 1, TKV_IN_F64 = 2 };

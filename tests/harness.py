@@ -213,6 +213,11 @@ def compare_bytes(run, orcs):
     b = run.bytes()
     assert b["live_slots"] == sum(f["live_slots"] for f in frag)
     assert b["resident_slots"] == sum(f["live_slots"] + f["masked_slots"] for f in frag)
-    assert b["live_code_bytes"] * 8 == sum(f["live_code_bits"] for f in frag)
+    # RAW16 passthrough: the reference counts 16 bits per element; the device
+    # stores (and K1 reads) the input dtype, so those bits scale by its width.
+    in_bytes = {"bf16": 2, "f32": 4, "f64": 8}[run.cfg.input_dtype]
+    want_bits = sum(bits * (in_bytes // 2 if fmt == "RAW16" else 1)
+                    for f in frag for fmt, bits in f["live_code_bits_by_format"].items())
+    assert b["live_code_bytes"] * 8 == want_bits
     assert b["live_scale_bytes"] == sum(f["live_scale_bytes"] for f in frag)
     return b

@@ -127,6 +127,26 @@ def test_parity_kmeans_stress(name):
     compare_state(res, cfg)
 
 
+def test_block_start_list_at_capacity():
+    """A block whose slots all belong to later segments keeps its implicit
+    first segment too: bs + 1 start indices (pager.cpp:190-216).  When one
+    more segment reuses a slot there, the reference appends its start and
+    mask before pruning the emptied one, so the device arrays hold one extra
+    start and mask transiently (TKV_STARTS_PER_BLOCK).  This configuration
+    (block size 4, found by an oracle search) reaches bs + 1 starts by step
+    275 and keeps churning; the step dumps prove it got there."""
+    from paper_2510_01290_b200.synth import band_script
+    cfg = ThinkvConfig(num_seqs=2, units_per_seq=2, num_q_heads=2, head_dim=32, tau=32, group_size=16,
+                       block_size=4, budget=96, levels=(16, 8, 4), max_gen_len=900,
+                       script=band_script(5, 2, 30, 3, 100), record_events=True,
+                       dump_positions=tuple(range(250, 900, 5)))
+    res = run_parity(cfg, check_every=4)
+    dumps = res["run"].step_dumps(0)
+    most = max(len(b["start_indices"]) for d in dumps.values() for t in d["block_tables"] for b in t["blocks"])
+    assert most >= cfg.block_size + 1
+    compare_state(res, cfg)
+
+
 def test_pool_exhaustion_matches_reference_error():
     cfg = ThinkvConfig(num_seqs=1, units_per_seq=1, num_q_heads=2, head_dim=16, tau=16, group_size=8,
                        block_size=4, pool_blocks=3, budget=4096, levels=(8, 4), max_gen_len=64,
