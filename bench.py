@@ -284,6 +284,7 @@ def main():
     ap.add_argument("--psi", type=int, nargs=3, default=None, help="bits per band E R T")
     ap.add_argument("--pT-permille", type=int, default=100)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline and its parity check")
+    ap.add_argument("--dump-step-ms", action="store_true", help="diagnostic: print the per-step times to stderr")
     ap.add_argument("--no-bytes-accounting", action="store_true",
                     help="diagnostic: skip the per-launch device byte accounting (roofline numerator)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
@@ -369,6 +370,8 @@ def main():
     acc, acc_launches = run.bytes_accumulated()
     run.bytes_accounting(False)
     step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(K)]
+    if args.dump_step_ms:
+        print("[bench] step ms: " + " ".join(f"{x:.3f}" for x in step_ms), file=sys.stderr)
     window_ms = evs[0].elapsed_time(evs[K])
     tpot, bnd, oth = amortize(step_ms, start, cfg.tau)
     ms_t = torch.tensor([tpot, window_ms / K], device=dev, dtype=torch.float64)

@@ -198,6 +198,52 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out);
 int tkv_synth_inputs(tkv_run* run, uint64_t seed, int64_t unit0, int64_t step, void* q, void* k, void* v,
                      void* stream);
 
+/* ---- drop-in batch-1 calls ------------------------------------------------
+ * The kernels behind the reference's own C++ API (the unchanged headers in
+ * proj/include/thinkv/, implemented as adapters in paper_2510_01290_b200/
+ * dropin/ -- SURVEY §8b).  One call = one kernel launch over HOST arrays
+ * (copied in and out; synchronous; reentrant: per-thread staging and
+ * stream).  Formats: 0 ternary, 1 NVFP4, 2 FP8 (E4M3). */
+
+/* quantize_window (quant.hpp:170-172, quant.cpp:486-580) for bits 2/4/8:
+ * keys/values [n][d] (n <= group_size); key_codes/value_codes [n][d];
+ * key_scales [d] and value_scales [n][ceil(d/group_size)] (E4M3 codes) or
+ * fp8_scales [2] (key, value f32 window scales) for 8 bits.  Non-finite
+ * input: TKV_ERR_CONFIG (the reference's kStructural). */
+int tkv_dropin_quantize_window(tkv_ctx* ctx, int32_t n, int32_t d, int32_t bits, int32_t group_size,
+                               const double* keys, const double* values, uint8_t* key_codes, uint8_t* value_codes,
+                               uint8_t* key_scales, uint8_t* value_scales, float* fp8_scales);
+/* decode_code (quant.cpp:195-205) elementwise: out[i] = value(codes[i]) * scales[i]
+ * (BlockPager::decode_payload, pager.cpp:89-112). */
+int tkv_dropin_decode(tkv_ctx* ctx, int32_t fmt, int64_t n, const uint8_t* codes, const double* scales, double* out);
+/* gqa_attend (attention.hpp:62-66, attention.cpp:124-146): q [G][d], keys/values
+ * [n][d]; out [d], row [n] (softmax scores).  fp64 in the reference's operation
+ * order, glibc's exp: the reference's bits. */
+int tkv_dropin_gqa_attend(tkv_ctx* ctx, int32_t G, int64_t n, int32_t d, double scale, const double* q,
+                          const double* keys, const double* values, double* out, double* row);
+/* sparsity (attention.cpp:148-158) of rows [offsets[r], offsets[r+1]) of scores. */
+int tkv_dropin_sparsity(tkv_ctx* ctx, const double* scores, const int64_t* offsets, int32_t nrows, double frac,
+                        double* out);
+/* kmeans_select (evictor.hpp:98-108, evictor.cpp:255-338) for ninst
+ * independent instances in one launch: instance i has m[i] <= 256 points of
+ * d channels (keys concatenated, [sum m][d]) and 1 <= k[i] < m[i] clusters;
+ * medoids (concatenated, [sum k]) = each cluster's medoid point index. */
+int tkv_dropin_kmeans_select(tkv_ctx* ctx, int32_t ninst, int32_t d, const int32_t* m, const int32_t* k,
+                             const double* keys, int32_t* medoids);
+/* BlockPager::append_tokens' placement (pager.cpp:114-219) over one pager's
+ * table -- thought/filled/evict (slot bitmask)/nstart [P], starts [P][bs+2],
+ * masks [P][bs+1], nfree: updated in place -- for n tokens of band `band`
+ * in segment seg_start: claims [n] = block * bs + slot, reused [n].
+ * TKV_ERR_OOM with the table unchanged when the pool is short.  bs <= 32. */
+int tkv_dropin_pager_place(tkv_ctx* ctx, int32_t P, int32_t bs, int8_t* thought, uint8_t* filled, uint32_t* evict,
+                           uint8_t* nstart, int32_t* starts, uint32_t* masks, int32_t* nfree, int32_t band,
+                           int32_t seg_start, int32_t n, int32_t* claims, int8_t* reused);
+/* BlockPager::apply_eviction_plan (pager.cpp:238-259) on the table: mask
+ * slots [n] (block * bs + slot), free touched blocks left without live
+ * slots; freed [<= P] lists them in ascending id, *nfreed their count. */
+int tkv_dropin_pager_evict(tkv_ctx* ctx, int32_t P, int32_t bs, int8_t* thought, uint8_t* filled, uint32_t* evict,
+                           uint8_t* nstart, int32_t n, const int32_t* slots, int32_t* freed, int32_t* nfreed);
+
 /* ---- gather-compaction comparator ---------------------------------------
  * Replaces the reference's GatherMethod (proj/src/sim.cpp:1117-1206), the
  * R-KV-style baseline of BASELINE config 5: every unit keeps a dense

@@ -20,6 +20,8 @@ EXPORTS = (
     "tkv_run_destroy", "tkv_step", "tkv_step_layer", "tkv_step_host", "tkv_finish", "tkv_synchronize",
     "tkv_position", "tkv_dump_json", "tkv_bytes", "tkv_unit_sparsity", "tkv_synth_inputs",
     "tkv_timing_enable", "tkv_timing_read", "tkv_bytes_accounting", "tkv_bytes_accumulated", "tkv_exp_f64", "tkv_step_host_async", "tkv_export_cache",
+    "tkv_dropin_quantize_window", "tkv_dropin_decode", "tkv_dropin_gqa_attend", "tkv_dropin_sparsity",
+    "tkv_dropin_kmeans_select", "tkv_dropin_pager_place", "tkv_dropin_pager_evict",
     "tkv_gather_create", "tkv_gather_destroy", "tkv_gather_step", "tkv_gather_stats", "tkv_gather_ids",
 )
 

@@ -70,6 +70,95 @@ __device__ __forceinline__ uint8_t ternary_encode_cmp(double x, double delta) {
   return tkv_ternary_bits(x > 0.0 ? 1 : -1);
 }
 
+// BlockPager::append_tokens (pager.cpp:132-164), the claim: n slots for
+// thought `band`, in the reference's order -- (1) soft-evicted slots of
+// same-thought blocks in physical order, (2) unfilled tail slots of
+// same-thought blocks, (3) fresh blocks, lowest free id first
+// (allocate_block, pager.cpp:28-47).  The capacity check comes before any
+// mutation: TKV_E_OOM with nothing changed.  th_r/fl_r/ev_r are the columns
+// the scan reads (a staged copy or the table itself); fresh-block
+// allocation writes th/fl/ev/ns and *nfree.  claim[i] = block * bs + slot.
+// Shared by K2 (flush_kernel) and the drop-in pager (pager_place_kernel).
+__device__ int tkv_claim_slots(const int8_t* th_r, const uint8_t* fl_r, const uint32_t* ev_r, int8_t* th,
+                               uint8_t* fl, uint32_t* ev, uint8_t* ns, int32_t* nfree, int P, int bs, int band,
+                               int n, int32_t* claim, int8_t* reuse) {
+  int claims = 0;
+  for (int b = 0; b < P && claims < n; ++b) {
+    if (th_r[b] != band) continue;
+    uint32_t m = ev_r[b] & (fl_r[b] >= 32 ? 0xffffffffu : ((1u << fl_r[b]) - 1u));
+    while (m && claims < n) {
+      const int s = __ffs(m) - 1;
+      m &= m - 1;
+      claim[claims] = b * bs + s;
+      reuse[claims] = 1;
+      ++claims;
+    }
+  }
+  for (int b = 0; b < P && claims < n; ++b) {
+    if (th_r[b] != band) continue;
+    for (int s = fl_r[b]; s < bs && claims < n; ++s) {
+      claim[claims] = b * bs + s;
+      reuse[claims] = 0;
+      ++claims;
+    }
+  }
+  const int remaining = n - claims;
+  const int fresh = (remaining + bs - 1) / bs;
+  if (fresh > *nfree) return TKV_E_OOM;
+  for (int b = 0, got = 0; b < P && got < fresh; ++b) {
+    if (th_r[b] != -1) continue;
+    th[b] = (int8_t)band;
+    fl[b] = 0;
+    ev[b] = 0;
+    ns[b] = 0;
+    ++got;
+    for (int s = 0; s < bs && claims < n; ++s) {
+      claim[claims] = b * bs + s;
+      reuse[claims] = 0;
+      ++claims;
+    }
+  }
+  *nfree -= fresh;
+  return 0;
+}
+
+// BlockPager::append_tokens (pager.cpp:166-216), the per-token bookkeeping of
+// the claimed slots in placement order: clear the eviction bit and drop the
+// slot from older segment masks on reuse (else filled++), append the
+// segment's start index and mask when it is new to the block (the first
+// segment is implicit), then prune later masks that reuse emptied.
+__device__ void tkv_record_placements(uint8_t* fl, uint32_t* ev, uint8_t* ns, int32_t* sstart, uint32_t* smask,
+                                      int bs, int32_t seg_start, int n, const int32_t* claim, const int8_t* reuse) {
+  for (int i = 0; i < n; ++i) {
+    const int b = claim[i] / bs, s = claim[i] % bs;
+    const uint32_t bit = 1u << s;
+    int32_t* starts = sstart + (int64_t)b * TKV_STARTS_PER_BLOCK(bs);
+    uint32_t* masks = smask + (int64_t)b * TKV_MASKS_PER_BLOCK(bs);
+    if (reuse[i]) {
+      ev[b] &= ~bit;
+      for (int k = 0; k + 1 < ns[b]; ++k) masks[k] &= ~bit;
+    } else {
+      fl[b] += 1;
+    }
+    int found = -1;
+    for (int k = 0; k < ns[b]; ++k)
+      if (starts[k] == seg_start) { found = k; break; }
+    if (found < 0) {
+      starts[ns[b]] = seg_start;
+      if (ns[b] > 0) masks[ns[b] - 1] = bit;
+      ns[b] += 1;
+    } else if (found > 0) {
+      masks[found - 1] |= bit;
+    }
+    for (int k = ns[b] - 2; k >= 0; --k) {
+      if (masks[k] != 0) continue;
+      for (int j = k; j + 1 < ns[b] - 1; ++j) masks[j] = masks[j + 1];
+      for (int j = k + 1; j + 1 < ns[b]; ++j) starts[j] = starts[j + 1];
+      ns[b] -= 1;
+    }
+  }
+}
+
 struct FlushSmem {
   int32_t claim[64];
   int8_t reuse[64];
@@ -223,51 +312,9 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
     uint8_t* ns = st.blk_nstart + (int64_t)u * P;
     int32_t* sstart = st.blk_start + (int64_t)u * P * TKV_STARTS_PER_BLOCK(bs);
     uint32_t* smask = st.blk_segmask + (int64_t)u * P * TKV_MASKS_PER_BLOCK(bs);
-    int claims = 0;
-    if (sm.abort_code == 0) {
-      // (1) soft-evicted slots of same-thought blocks, physical order.
-      for (int b = 0; b < P && claims < n; ++b) {
-        if (th_s[b] != c.band) continue;
-        uint32_t m = ev_s[b] & (fl_s[b] >= 32 ? 0xffffffffu : ((1u << fl_s[b]) - 1u));
-        while (m && claims < n) {
-          const int s = __ffs(m) - 1;
-          m &= m - 1;
-          sm.claim[claims] = b * bs + s;
-          sm.reuse[claims] = 1;
-          ++claims;
-        }
-      }
-      // (2) unfilled tail slots of same-thought blocks.
-      for (int b = 0; b < P && claims < n; ++b) {
-        if (th_s[b] != c.band) continue;
-        for (int s = fl_s[b]; s < bs && claims < n; ++s) {
-          sm.claim[claims] = b * bs + s;
-          sm.reuse[claims] = 0;
-          ++claims;
-        }
-      }
-      // (3) fresh blocks, lowest free id first; capacity checked up front.
-      const int remaining = n - claims;
-      const int fresh = (remaining + bs - 1) / bs;
-      if (fresh > st.unit_nfree[u]) {
-        sm.abort_code = TKV_E_OOM;
-      } else {
-        for (int b = 0, got = 0; b < P && got < fresh; ++b) {
-          if (th_s[b] != -1) continue;
-          th[b] = (int8_t)c.band;  // allocate_block (pager.cpp:28-47)
-          fl[b] = 0;
-          ev[b] = 0;
-          ns[b] = 0;
-          ++got;
-          for (int s = 0; s < bs && claims < n; ++s) {
-            sm.claim[claims] = b * bs + s;
-            sm.reuse[claims] = 0;
-            ++claims;
-          }
-        }
-        st.unit_nfree[u] -= fresh;
-      }
-    }
+    if (sm.abort_code == 0)
+      sm.abort_code = tkv_claim_slots(th_s, fl_s, ev_s, th, fl, ev, ns, st.unit_nfree + u, P, bs, c.band, n,
+                                      sm.claim, sm.reuse);
     if (sm.abort_code != 0) {
       *err = sm.abort_code;
     } else {
@@ -283,36 +330,7 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
         }
       }
       sm.win = w;
-      for (int i = 0; i < n && sm.abort_code == 0; ++i) {
-        const int b = sm.claim[i] / bs, s = sm.claim[i] % bs;
-        const uint32_t bit = 1u << s;
-        int32_t* starts = sstart + (int64_t)b * TKV_STARTS_PER_BLOCK(bs);
-        uint32_t* masks = smask + (int64_t)b * TKV_MASKS_PER_BLOCK(bs);
-        if (sm.reuse[i]) {
-          ev[b] &= ~bit;
-          for (int k = 0; k + 1 < ns[b]; ++k) masks[k] &= ~bit;
-        } else {
-          fl[b] += 1;
-        }
-        // Segment bookkeeping: first segment implicit, later ones carry masks.
-        int found = -1;
-        for (int k = 0; k < ns[b]; ++k)
-          if (starts[k] == c.seg_start) { found = k; break; }
-        if (found < 0) {
-          starts[ns[b]] = c.seg_start;
-          if (ns[b] > 0) masks[ns[b] - 1] = bit;
-          ns[b] += 1;
-        } else if (found > 0) {
-          masks[found - 1] |= bit;
-        }
-        // Prune later segments whose masks emptied after reuse.
-        for (int k = ns[b] - 2; k >= 0; --k) {
-          if (masks[k] != 0) continue;
-          for (int j = k; j + 1 < ns[b] - 1; ++j) masks[j] = masks[j + 1];
-          for (int j = k + 1; j + 1 < ns[b]; ++j) starts[j] = starts[j + 1];
-          ns[b] -= 1;
-        }
-      }
+      if (sm.abort_code == 0) tkv_record_placements(fl, ev, ns, sstart, smask, bs, c.seg_start, n, sm.claim, sm.reuse);
     }
   }
   __syncthreads();
@@ -372,7 +390,64 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
   }
 }
 
+
+// ---- drop-in pager: one BlockPager's table per launch --------
+// BlockPager::append_tokens' placement over a caller-supplied table (the
+// drop-in adapter's host mirror, uploaded for the call): the same claim and
+// bookkeeping K2 runs on the paged state.
+__global__ void pager_place_kernel(int P, int bs, int8_t* th, uint8_t* fl, uint32_t* ev, uint8_t* ns, int32_t* sstart,
+                                   uint32_t* smask, int32_t* nfree, int band, int32_t seg_start, int n, int32_t* claim,
+                                   int8_t* reuse, int32_t* rc) {
+  if (threadIdx.x != 0) return;
+  const int r = tkv_claim_slots(th, fl, ev, th, fl, ev, ns, nfree, P, bs, band, n, claim, reuse);
+  *rc = r;
+  if (r == 0) tkv_record_placements(fl, ev, ns, sstart, smask, bs, seg_start, n, claim, reuse);
+}
+
+// BlockPager::apply_eviction_plan (pager.cpp:238-259) on the table: mask the
+// listed slots, then free every touched block whose live count reached zero,
+// in ascending block id (free_block :228-236).  freed[] lists them.
+__global__ void pager_evict_kernel(int P, int bs, int8_t* th, uint8_t* fl, uint32_t* ev, uint8_t* ns, int n,
+                                   const int32_t* slots, int32_t* freed, int32_t* nfreed) {
+  extern __shared__ uint8_t touched[];
+  for (int b = threadIdx.x; b < P; b += blockDim.x) touched[b] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n; ++i) {
+      const int b = slots[i] / bs, s = slots[i] % bs;
+      ev[b] |= 1u << s;
+      touched[b] = 1;
+    }
+    int k = 0;
+    for (int b = 0; b < P; ++b) {
+      if (!touched[b]) continue;
+      const uint32_t filled = fl[b] >= 32 ? 0xffffffffu : ((1u << fl[b]) - 1u);
+      if ((~ev[b] & filled) != 0) continue;  // live_in_block > 0
+      th[b] = -1;
+      fl[b] = 0;
+      ev[b] = 0;
+      ns[b] = 0;
+      freed[k++] = b;
+    }
+    *nfreed = k;
+  }
+}
+
 }  // namespace
+
+cudaError_t tkv_launch_pager_place(int P, int bs, int8_t* th, uint8_t* fl, uint32_t* ev, uint8_t* ns, int32_t* sstart,
+                                   uint32_t* smask, int32_t* nfree, int band, int32_t seg_start, int n, int32_t* claim,
+                                   int8_t* reuse, int32_t* rc, cudaStream_t stream) {
+  pager_place_kernel<<<1, 32, 0, stream>>>(P, bs, th, fl, ev, ns, sstart, smask, nfree, band, seg_start, n, claim,
+                                           reuse, rc);
+  return cudaGetLastError();
+}
+
+cudaError_t tkv_launch_pager_evict(int P, int bs, int8_t* th, uint8_t* fl, uint32_t* ev, uint8_t* ns, int n,
+                                   const int32_t* slots, int32_t* freed, int32_t* nfreed, cudaStream_t stream) {
+  pager_evict_kernel<<<1, 128, P, stream>>>(P, bs, th, fl, ev, ns, n, slots, freed, nfreed);
+  return cudaGetLastError();
+}
 
 cudaError_t tkv_launch_flush(const TkvState& st, int half, int n, int pos0, const TkvFlushCtl* ctl,
                              int units_per_group, cudaStream_t stream) {

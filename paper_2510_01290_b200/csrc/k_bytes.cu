@@ -13,8 +13,10 @@
 //                     4 B per live slot (slot -> window index)
 // The host adds the buffer, current-token, q and out bytes (known per launch).
 //
-// One CTA per unit.  Distinct live windows are counted with a bitmap in
-// shared memory (one bit per window id).  Runs when byte accounting is
+// One CTA per unit: pass 1 walks the block table (a thread per block: live
+// slot mask, counts, code and value-scale bytes), pass 2 reads the window
+// index of live slots only (coalesced) and marks distinct live windows in a
+// shared-memory bitmap (one bit per window id).  Runs when byte accounting is
 // enabled (tkv_bytes_accounting), right after the attention launch of a step,
 // so every timed K1 launch is matched with its own exact byte count.
 #include <cuda_runtime.h>
@@ -27,39 +29,47 @@ namespace {
 constexpr int kThreads = 128;
 
 __global__ void __launch_bounds__(kThreads) bytes_kernel(TkvState st, unsigned long long* acc) {
-  extern __shared__ uint32_t win_bits[];  // [2][nwords]: E4M3-scaled windows | FP8 windows
+  extern __shared__ uint32_t win_bits[];  // [2][nwords] E4M3-scaled | FP8 windows, then live slot masks [P]
   const TkvDims& dm = st.dm;
   const int u = tkv_unit_of(st, blockIdx.x);
   const int nwords = (dm.NW + 31) / 32;
+  uint32_t* live_m = win_bits + 2 * nwords;
   for (int i = threadIdx.x; i < 2 * nwords; i += kThreads) win_bits[i] = 0u;
-  __syncthreads();
   unsigned long long live = 0, resident = 0, code = 0, scale = 0, meta = 0;
-  const int8_t* th = st.blk_thought + (int64_t)u * dm.P;
-  const uint8_t* fl = st.blk_filled + (int64_t)u * dm.P;
-  const uint32_t* ev = st.blk_evict + (int64_t)u * dm.P;
-  const int32_t* sw = st.slot_win + (int64_t)u * dm.NS;
-  // slot-granular walk: thread i takes slots i, i + 128, ...
+  // pass 1: one block per thread -- live slot mask, counts, code bytes
+  for (int b = threadIdx.x; b < dm.P; b += kThreads) {
+    meta += 6;
+    const int t = st.blk_thought[(int64_t)u * dm.P + b];
+    uint32_t lm = 0;
+    if (t >= 0) {
+      const int f = st.blk_filled[(int64_t)u * dm.P + b];
+      const uint32_t fm = f >= 32 ? 0xffffffffu : ((1u << f) - 1u);
+      lm = fm & ~st.blk_evict[(int64_t)u * dm.P + b];
+      const int nl = __popc(lm);
+      resident += (unsigned)f;
+      live += (unsigned)nl;
+      meta += 4ull * nl;
+      code += 2ull * (unsigned)dm.band_bytes[t] * nl;
+      const int fmt = dm.band_fmt[t];
+      if (fmt == TKV_FMT_RAW) lm = 0;  // no scales
+      else if (fmt != TKV_FMT_FP8) scale += (unsigned long long)dm.vchunks * nl;
+    }
+    live_m[b] = lm;
+  }
+  __syncthreads();
+  // pass 2: slot-parallel, coalesced slot -> window reads of live slots only
+  const int bs = dm.bs;
   for (int s = threadIdx.x; s < dm.NS; s += kThreads) {
-    const int b = s / dm.bs, sl = s - b * dm.bs;
-    if (sl == 0) meta += 6;
-    const int t = th[b];
-    if (t < 0 || sl >= fl[b]) continue;
-    resident += 1;
-    if ((ev[b] >> sl) & 1u) continue;
-    live += 1;
-    meta += 4;
-    code += 2ull * (unsigned)dm.band_bytes[t];
-    const int fmt = dm.band_fmt[t];
-    if (fmt == TKV_FMT_RAW) continue;
-    const int w = sw[s];
+    const int b = s / bs, sl = s - b * bs;
+    if (!((live_m[b] >> sl) & 1u)) continue;
+    const int w = st.slot_win[(int64_t)u * dm.NS + s];
     if (w < 0) continue;
-    if (fmt != TKV_FMT_FP8) scale += (unsigned)dm.vchunks;
-    atomicOr(&win_bits[(fmt == TKV_FMT_FP8 ? nwords : 0) + (w >> 5)], 1u << (w & 31));
+    const bool fp8 = dm.band_fmt[st.blk_thought[(int64_t)u * dm.P + b]] == TKV_FMT_FP8;
+    atomicOr(&win_bits[(fp8 ? nwords : 0) + (w >> 5)], 1u << (w & 31));
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 2 * nwords; i += kThreads)
     scale += (unsigned long long)__popc(win_bits[i]) * (i < nwords ? (unsigned)dm.D : 8u);
-  // warp reduce, then one atomic per warp per counter
   unsigned long long v[5] = {live, resident, code, scale, meta};
 #pragma unroll
   for (int j = 0; j < 5; ++j) {
@@ -78,7 +88,7 @@ __global__ void __launch_bounds__(kThreads) bytes_kernel(TkvState st, unsigned l
 cudaError_t tkv_launch_bytes(const TkvState& st, unsigned long long* acc, cudaStream_t stream) {
   const int n = tkv_launch_units(st);
   if (n <= 0) return cudaSuccess;
-  const size_t smem = 2 * (size_t)((st.dm.NW + 31) / 32) * sizeof(uint32_t);
+  const size_t smem = (2 * (size_t)((st.dm.NW + 31) / 32) + st.dm.P) * sizeof(uint32_t);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(bytes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -339,6 +339,83 @@ __device__ void farthest_first(const Km& km, KmSmem& s, int anchor) {
   }
 }
 
+// kmeans_select's medoid choice (kmeans_cluster, evictor.cpp:255-338) over
+// the keys in km.X: seed sets, the restarts (lowest cost wins, ties to the
+// earlier), then the member nearest each centroid (ties to the lowest
+// index).  Leaves the medoid point index of cluster c in s.medoid[c].
+__device__ void select_medoids(const Km& km, KmSmem& s) {
+  const int m = km.m, K = km.K, D = km.D;
+  // Seed sets (kmeans_cluster, evictor.cpp:255-317).
+  double subsets = 1.0;
+  for (int i = 0; i < K; ++i) subsets = __dmul_rn(subsets, __ddiv_rn((double)(m - i), (double)(i + 1)));
+  kstat(km, 10, 1);
+  if (subsets <= 512.0) {
+    kstat(km, 11, 1);
+    if (threadIdx.x == 0)
+      for (int i = 0; i < K; ++i) s.seeds[i] = i;
+    __syncthreads();
+    while (true) {
+      run_seeds(km, s);
+      if (threadIdx.x == 0) {
+        int j = K;
+        while (j > 0 && s.seeds[j - 1] == m - K + j - 1) --j;
+        if (j == 0) {
+          s.flag = 1;
+        } else {
+          ++s.seeds[j - 1];
+          for (int l = j; l < K; ++l) s.seeds[l] = s.seeds[l - 1] + 1;
+          s.flag = 0;
+        }
+      }
+      __syncthreads();
+      if (s.flag) break;
+    }
+  } else {
+    // Anchors: index 0, farthest from and nearest to the mean, m/2.
+    double* mean = km.best;  // scratch until the first run
+    for (int ch = threadIdx.x; ch < D; ch += kThreads) {
+      double acc = 0.0;
+      for (int i = 0; i < m; ++i) acc = __dadd_rn(acc, km.X[i * D + ch]);
+      mean[ch] = __ddiv_rn(acc, (double)m);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += kThreads) s.tmp[i] = dist2(km.X + i * D, mean, D);
+    __syncthreads();
+    __shared__ int anchors[4];
+    if (threadIdx.x == 0) {
+      int far_idx = 0, near_idx = 0;
+      double far_d = -1.0, near_d = CUDART_INF;
+      for (int i = 0; i < m; ++i) {
+        const double d = s.tmp[i];
+        if (d > far_d) { far_d = d; far_idx = i; }
+        if (d < near_d) { near_d = d; near_idx = i; }
+      }
+      anchors[0] = 0;
+      anchors[1] = far_idx;
+      anchors[2] = near_idx;
+      anchors[3] = m / 2;
+    }
+    __syncthreads();
+    for (int a = 0; a < 4; ++a) {
+      const long long f0 = clock64();
+      farthest_first(km, s, anchors[a]);
+      kstat(km, 12, (unsigned long long)(clock64() - f0));
+      run_seeds(km, s);
+    }
+  }
+  // Medoids: member nearest each centroid, ties to the lowest id.
+  for (int c = threadIdx.x; c < K; c += kThreads) {
+    int best_i = m;
+    double best_d = CUDART_INF;
+    for (int i = 0; i < m; ++i) {
+      if (s.best_assign[i] != c) continue;
+      const double d = dist2(km.X + i * D, km.best + c * D, D);
+      if (d < best_d) { best_d = d; best_i = i; }
+    }
+    s.medoid[c] = best_i;
+  }
+  __syncthreads();}
+
 __device__ double decode_key(const TkvState& st, int u, int slot, int ch) {
   const TkvDims& dm = st.dm;
   const int64_t gs = (int64_t)u * dm.NS + slot;
@@ -426,82 +503,12 @@ __global__ void __launch_bounds__(kThreads) anneal_kernel(TkvState st, const Tkv
       __syncthreads();
       continue;
     }
-    const int K = op.K;
-    // Seed sets (kmeans_cluster, evictor.cpp:255-317).
-    double subsets = 1.0;
-    for (int i = 0; i < K; ++i) subsets = __dmul_rn(subsets, __ddiv_rn((double)(m - i), (double)(i + 1)));
-    kstat(km, 10, 1);
-    if (subsets <= 512.0) {
-      kstat(km, 11, 1);
-      if (threadIdx.x == 0)
-        for (int i = 0; i < K; ++i) s.seeds[i] = i;
-      __syncthreads();
-      while (true) {
-        run_seeds(km, s);
-        if (threadIdx.x == 0) {
-          int j = K;
-          while (j > 0 && s.seeds[j - 1] == m - K + j - 1) --j;
-          if (j == 0) {
-            s.flag = 1;
-          } else {
-            ++s.seeds[j - 1];
-            for (int l = j; l < K; ++l) s.seeds[l] = s.seeds[l - 1] + 1;
-            s.flag = 0;
-          }
-        }
-        __syncthreads();
-        if (s.flag) break;
-      }
-    } else {
-      // Anchors: index 0, farthest from and nearest to the mean, m/2.
-      double* mean = km.best;  // scratch until the first run
-      for (int ch = threadIdx.x; ch < D; ch += kThreads) {
-        double acc = 0.0;
-        for (int i = 0; i < m; ++i) acc = __dadd_rn(acc, km.X[i * D + ch]);
-        mean[ch] = __ddiv_rn(acc, (double)m);
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < m; i += kThreads) s.tmp[i] = dist2(km.X + i * D, mean, D);
-      __syncthreads();
-      __shared__ int anchors[4];
-      if (threadIdx.x == 0) {
-        int far_idx = 0, near_idx = 0;
-        double far_d = -1.0, near_d = CUDART_INF;
-        for (int i = 0; i < m; ++i) {
-          const double d = s.tmp[i];
-          if (d > far_d) { far_d = d; far_idx = i; }
-          if (d < near_d) { near_d = d; near_idx = i; }
-        }
-        anchors[0] = 0;
-        anchors[1] = far_idx;
-        anchors[2] = near_idx;
-        anchors[3] = m / 2;
-      }
-      __syncthreads();
-      for (int a = 0; a < 4; ++a) {
-        const long long f0 = clock64();
-        farthest_first(km, s, anchors[a]);
-        kstat(km, 12, (unsigned long long)(clock64() - f0));
-        run_seeds(km, s);
-      }
-    }
+    select_medoids(km, s);
     kstat(km, 13, (unsigned long long)(clock64() - i0));
     kstat(km, 14, (unsigned long long)m);
-    // Medoids: member nearest each centroid, ties to the lowest id.
-    for (int c = threadIdx.x; c < K; c += kThreads) {
-      int best_i = m;
-      double best_d = CUDART_INF;
-      for (int i = 0; i < m; ++i) {
-        if (s.best_assign[i] != c) continue;
-        const double d = dist2(km.X + i * D, km.best + c * D, D);
-        if (d < best_d) { best_d = d; best_i = i; }
-      }
-      s.medoid[c] = best_i;
-    }
-    __syncthreads();
     if (threadIdx.x == 0) {
       uint32_t keep[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int c = 0; c < K; ++c) {
+      for (int c = 0; c < op.K; ++c) {
         const int b = s.ids[s.medoid[c]];
         keep[b >> 5] |= 1u << (b & 31);
       }
@@ -513,6 +520,36 @@ __global__ void __launch_bounds__(kThreads) anneal_kernel(TkvState st, const Tkv
     }
     __syncthreads();
   }
+}
+
+// Drop-in kmeans_select: one CTA per instance over caller-
+// supplied fp64 keys (instance i: m[i] <= 256 points of D channels at
+// X + xoff[i], K[i] clusters); medoid point indices, one per cluster, to
+// out + ooff[i].  Scratch: 5 * m[i] * D doubles at scratch + 5 * xoff[i].
+__global__ void __launch_bounds__(kThreads) kmeans_select_f64_kernel(const double* __restrict__ X,
+                                                                     const int32_t* __restrict__ ms,
+                                                                     const int32_t* __restrict__ ks,
+                                                                     const int64_t* __restrict__ xoff,
+                                                                     const int64_t* __restrict__ ooff, int D,
+                                                                     double* __restrict__ scratch, int32_t* out) {
+  __shared__ KmSmem s;
+  const int i = blockIdx.x;
+  const int m = ms[i], K = ks[i];
+  Km km;
+  km.m = m;
+  km.K = K;
+  km.D = D;
+  km.X = const_cast<double*>(X) + xoff[i];
+  km.cb[0] = scratch + 5 * xoff[i];
+  km.cb[1] = km.cb[0] + (int64_t)m * D;
+  km.sums = km.cb[1] + (int64_t)m * D;
+  km.means = km.sums + (int64_t)m * D;
+  km.best = km.means + (int64_t)m * D;
+  km.ks = nullptr;
+  if (threadIdx.x == 0) s.have_best = 0;
+  __syncthreads();
+  select_medoids(km, s);
+  for (int c = threadIdx.x; c < K; c += kThreads) out[ooff[i] + c] = s.medoid[c];
 }
 
 __global__ void __launch_bounds__(32) apply_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops,
@@ -600,6 +637,14 @@ cudaError_t tkv_launch_anneal(const TkvState& st, const TkvAnnealOp* ops, int no
   const int grid = nitems < scratch_ctas ? nitems : scratch_ctas;
   anneal_kernel<<<grid, kThreads, 0, stream>>>(st, ops, nops, item_prefix, nitems, log, scratch,
                                                scratch_doubles_per_cta, max_m);
+  return cudaGetLastError();
+}
+
+cudaError_t tkv_launch_kmeans_select_f64(int ninst, const double* X, const int32_t* m, const int32_t* K,
+                                         const int64_t* xoff, const int64_t* ooff, int D, double* scratch,
+                                         int32_t* out, cudaStream_t stream) {
+  if (ninst <= 0) return cudaSuccess;
+  kmeans_select_f64_kernel<<<ninst, kThreads, 0, stream>>>(X, m, K, xoff, ooff, D, scratch, out);
   return cudaGetLastError();
 }
 

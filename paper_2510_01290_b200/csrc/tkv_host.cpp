@@ -30,6 +30,7 @@
 #include "json.hpp"
 #include "../../include/thinkv_b200.h"
 #include "synth.h"
+#include "tkv_internal.h"
 #include "tkv_kernels.h"
 #include "tkv_state.h"
 
@@ -141,9 +142,6 @@ struct GroupPlan {
 
 }  // namespace
 
-struct tkv_ctx {
-  int device = 0;
-};
 
 struct tkv_run {
   tkv_ctx* ctx = nullptr;
@@ -1273,6 +1271,8 @@ int64_t live_bytes_stats(tkv_run* r, tkv_bytes_t* out) {
 }
 
 }  // namespace
+
+void tkv_internal_set_error(const std::string& msg) { g_last_error = msg; }
 
 extern "C" {
 

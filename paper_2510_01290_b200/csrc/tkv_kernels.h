@@ -57,6 +57,35 @@ cudaError_t tkv_launch_apply(const TkvState& st, const TkvAnnealOp* ops,
                              const int32_t* unit_prefix, int nitems, const uint32_t* log,
                              cudaStream_t stream);
 
+// ---- drop-in batch-1 kernels (k_dropin.cu, k_append.cu, k_evict.cu) ----
+// quantize_window over n <= group_size fp64 tokens (fmt = TKV_FMT_TERNARY/NVFP4/FP8):
+// kc/vc [n][d], ksc [d], vsc [n][ceil(d/group_size)], f8 [2] (FP8 key/value scales);
+// *bad = 1 on a non-finite input (the reference throws kStructural).
+cudaError_t tkv_launch_window_quant(int n, int d, int fmt, int group_size, const double* keys, const double* values,
+                                    uint8_t* kc, uint8_t* vc, uint8_t* ksc, uint8_t* vsc, float* f8, int* bad,
+                                    cudaStream_t stream);
+// gqa_attend in fp64 (reference order): out [d], row [n] (the softmax scores).
+cudaError_t tkv_launch_gqa_attend_f64(int G, int n, int d, double scale, const double* q, const double* k,
+                                      const double* v, double* out, double* row, cudaStream_t stream);
+// sparsity of rows [offs[r], offs[r+1]) of scores.
+cudaError_t tkv_launch_sparsity_rows(const double* scores, const int64_t* offs, int nrows, double frac, double* out,
+                                     cudaStream_t stream);
+// decode_code elementwise.
+cudaError_t tkv_launch_decode_codes(int fmt, int64_t n, const uint8_t* codes, const double* scales, double* out,
+                                    cudaStream_t stream);
+// BlockPager placement / eviction over one pager's table (layout as TkvState's
+// block table for one unit: th/fl/ev/ns [P], starts [P][bs+2], masks [P][bs+1]).
+cudaError_t tkv_launch_pager_place(int P, int bs, int8_t* th, uint8_t* fl, uint32_t* ev, uint8_t* ns, int32_t* sstart,
+                                   uint32_t* smask, int32_t* nfree, int band, int32_t seg_start, int n, int32_t* claim,
+                                   int8_t* reuse, int32_t* rc, cudaStream_t stream);
+cudaError_t tkv_launch_pager_evict(int P, int bs, int8_t* th, uint8_t* fl, uint32_t* ev, uint8_t* ns, int n,
+                                   const int32_t* slots, int32_t* freed, int32_t* nfreed, cudaStream_t stream);
+// kmeans_select medoid indices of ninst instances (instance i: m[i] <= 256 points
+// of D channels at X + xoff[i], 1 <= K[i] < m[i]; out + ooff[i]); scratch >= 5 * total points * D.
+cudaError_t tkv_launch_kmeans_select_f64(int ninst, const double* X, const int32_t* m, const int32_t* K,
+                                         const int64_t* xoff, const int64_t* ooff, int D, double* scratch,
+                                         int32_t* out, cudaStream_t stream);
+
 // Synthetic decode inputs (bf16) generated on device with the same integer
 // generator as the host oracle (synth.h).
 cudaError_t tkv_launch_synth(uint64_t seed, int units_per_seq, int tau, int sink_tokens, int64_t unit0,
