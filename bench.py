@@ -140,16 +140,27 @@ def ncu_traffic():
 
 
 def amortize(step_ms, first_pos, tau):
-    """tau-amortised TPOT from per-step times of a window starting at decode
-    position first_pos: a refresh boundary (eviction wave, K-means) happens on
-    one step in tau, so TPOT = (mean boundary step + (tau - 1) * mean other
-    step) / tau ("TPOT = ... amortized K2/K3").  Windows of whole
-    tau periods give exactly their plain mean."""
+    """tau-amortised TPOT from the per-step times of a window that opens on
+    a refresh boundary (first_pos % tau == 0).  In steady state the eviction
+    work is tau-periodic: the boundary step (flush, Case-1/Case-2 anneals of
+    the closing segment) and a Case-2 anneal a few steps later when the open
+    segment pushes the total over budget; the other steps are plain decode
+    steps.  So
+      K >= tau: TPOT = mean of the window's first floor(K / tau) whole periods;
+      K <  tau: TPOT = (sum of the K steps + (tau - K) * median plain step) / tau,
+    the unseen tail of the period estimated by the window's median plain
+    step ("TPOT = ... amortized K2/K3").  Returns (TPOT, boundary
+    step times, other step times)."""
+    if first_pos % tau:
+        raise ValueError("the timed window must open on a refresh boundary")
     bnd = [t for i, t in enumerate(step_ms) if (first_pos + i) % tau == 0]
     oth = [t for i, t in enumerate(step_ms) if (first_pos + i) % tau != 0]
-    if not bnd or not oth:
-        return sum(step_ms) / len(step_ms), bnd, oth
-    return (sum(bnd) / len(bnd) + (tau - 1) * sum(oth) / len(oth)) / tau, bnd, oth
+    K = len(step_ms)
+    if K >= tau:
+        whole = (K // tau) * tau
+        return sum(step_ms[:whole]) / whole, bnd, oth
+    plain = sorted(oth)[len(oth) // 2] if oth else step_ms[0]
+    return (sum(step_ms) + (tau - K) * plain) / tau, bnd, oth
 
 
 def sample_units(cfg, threads):
@@ -256,9 +267,10 @@ def bench_config(args, cfg, world, preset, custom, start):
         "parallelism": f"seq-shard x{world}", "gqa": "per-head", "tau": cfg.tau,
         "timed_positions": [start, start + K - 1],
         "e2e_positions": [start + K, start + K + E - 1],
-        "tpot_formula": ("per-step device times of the K timed steps; TPOT = (mean refresh-boundary step + "
-                         "(tau - 1) * mean other step) / tau -- the tau-amortised step, K2/K3 included; "
-                         "value = global_batch / TPOT"),
+        "tpot_formula": ("per-step device times of the K timed steps, window opening on a refresh boundary; "
+                         "K >= tau: TPOT = mean over the window's whole tau periods; K < tau: TPOT = (sum of the K "
+                         "steps + (tau - K) * median non-boundary step) / tau -- the tau-amortised step with its "
+                         "eviction waves (boundary + Case-2 anneal) included; value = global_batch / TPOT"),
     }
 
 

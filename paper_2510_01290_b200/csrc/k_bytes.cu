@@ -33,7 +33,8 @@ __global__ void __launch_bounds__(kThreads) bytes_kernel(TkvState st, unsigned l
   const TkvDims& dm = st.dm;
   const int u = tkv_unit_of(st, blockIdx.x);
   const int nwords = (dm.NW + 31) / 32;
-  uint32_t* live_m = win_bits + 2 * nwords;
+  uint32_t* live_m = win_bits + 2 * nwords;                      // live slot mask per block
+  uint8_t* blk_fp8 = reinterpret_cast<uint8_t*>(live_m + dm.P);  // FP8 block flags
   for (int i = threadIdx.x; i < 2 * nwords; i += kThreads) win_bits[i] = 0u;
   unsigned long long live = 0, resident = 0, code = 0, scale = 0, meta = 0;
   // pass 1: one block per thread -- live slot mask, counts, code bytes
@@ -55,17 +56,34 @@ __global__ void __launch_bounds__(kThreads) bytes_kernel(TkvState st, unsigned l
       else if (fmt != TKV_FMT_FP8) scale += (unsigned long long)dm.vchunks * nl;
     }
     live_m[b] = lm;
+    blk_fp8[b] = t >= 0 && dm.band_fmt[t] == TKV_FMT_FP8;
   }
   __syncthreads();
-  // pass 2: slot-parallel, coalesced slot -> window reads of live slots only
+  // pass 2: slot-parallel, coalesced slot -> window reads of live slots only,
+  // kUnroll independent loads in flight per thread (the walk is latency bound)
+  constexpr int kUnroll = 8;
   const int bs = dm.bs;
-  for (int s = threadIdx.x; s < dm.NS; s += kThreads) {
-    const int b = s / bs, sl = s - b * bs;
-    if (!((live_m[b] >> sl) & 1u)) continue;
-    const int w = st.slot_win[(int64_t)u * dm.NS + s];
-    if (w < 0) continue;
-    const bool fp8 = dm.band_fmt[st.blk_thought[(int64_t)u * dm.P + b]] == TKV_FMT_FP8;
-    atomicOr(&win_bits[(fp8 ? nwords : 0) + (w >> 5)], 1u << (w & 31));
+  const int32_t* sw = st.slot_win + (int64_t)u * dm.NS;
+  for (int s0 = threadIdx.x; s0 < dm.NS; s0 += kThreads * kUnroll) {
+    int w[kUnroll];
+    int fp8[kUnroll];
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j) {
+      const int s = s0 + j * kThreads;
+      w[j] = -1;
+      fp8[j] = 0;
+      if (s < dm.NS) {
+        const int b = s / bs;
+        const uint32_t lm = live_m[b];
+        if ((lm >> (s - b * bs)) & 1u) {
+          w[j] = __ldg(sw + s);
+          fp8[j] = blk_fp8[b];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kUnroll; ++j)
+      if (w[j] >= 0) atomicOr(&win_bits[(fp8[j] ? nwords : 0) + (w[j] >> 5)], 1u << (w[j] & 31));
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 2 * nwords; i += kThreads)
@@ -88,7 +106,7 @@ __global__ void __launch_bounds__(kThreads) bytes_kernel(TkvState st, unsigned l
 cudaError_t tkv_launch_bytes(const TkvState& st, unsigned long long* acc, cudaStream_t stream) {
   const int n = tkv_launch_units(st);
   if (n <= 0) return cudaSuccess;
-  const size_t smem = (2 * (size_t)((st.dm.NW + 31) / 32) + st.dm.P) * sizeof(uint32_t);
+  const size_t smem = (2 * (size_t)((st.dm.NW + 31) / 32) + st.dm.P) * sizeof(uint32_t) + st.dm.P;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(bytes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

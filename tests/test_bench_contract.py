@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -37,15 +39,18 @@ def test_reference_arm_does_not_map_the_cuda_library():
 def test_amortised_tpot():
     sys.path.insert(0, ROOT)
     import bench
-    # window of whole tau periods: plain mean
-    steps = [10.0] + [1.0] * 3 + [10.0] + [1.0] * 3
-    assert bench.amortize(steps, 8, 4)[0] == sum(steps) / len(steps)
-    # short window opening on a boundary: the boundary is weighted 1/tau
-    tpot, bnd, oth = bench.amortize([130.0, 1.0, 1.0], 256, 128)
-    assert bnd == [130.0] and oth == [1.0, 1.0] and abs(tpot - (130.0 + 127.0) / 128) < 1e-12
-    # first timed position: a boundary leaving room for K + E steps
+    # windows of whole tau periods: their mean (a trailing partial period is dropped)
+    steps = [10.0, 1.0, 3.0, 1.0] * 2 + [50.0]
+    assert bench.amortize(steps, 8, 4)[0] == 15.0 * 2 / 8
+    # short window opening on a boundary: the rest of the period at the median plain step
+    tpot, bnd, oth = bench.amortize([130.0, 1.0, 1.0, 1.0, 27.0, 1.0], 256, 128)
+    assert bnd == [130.0] and len(oth) == 5 and abs(tpot - (161.0 + 122 * 1.0) / 128) < 1e-12
+    with pytest.raises(ValueError):
+        bench.amortize([1.0, 2.0], 257, 128)
+
     class A:
         ctx, warmup, steps, e2e_steps = None, 5, 20, 128
+
     class Cfg:
         max_gen_len, tau = 32768, 128
     assert bench.positions(A, Cfg) == 32512
