@@ -103,6 +103,8 @@ struct EvSeg {
 struct EventRec {
   int kind = 0;  // 0 emit, 1 evict, 2 refresh
   int64_t step = 0;
+  // emit / evict: one JSON line per unit, layers layer0 .. layer0 + nlayers - 1
+  int layer0 = 0, nlayers = 1;
   // emit
   int fmt = 0, tokens = 0, pad = 0;
   // evict
@@ -114,14 +116,25 @@ struct EventRec {
   int64_t dstep = 0;
   double sparsity = 0.0;
   int band = 0;
+  std::vector<int> bands;  // per-layer labels (per_layer_thought, sim.cpp:713-716, :728-730)
 };
 
+// Units whose segment sizes evolve together: every unit of a sequence
+// (their labels are shared, sim.cpp:717-722), or one unit when labels are
+// per layer (per_layer_thought).  The host plans evictions once per group.
 struct Group {
   int seq = 0, unit0 = 0, nunits = 0;
   std::vector<HSeg> segs;
   int open = -1;
   int next_seg_id = 0;
   int64_t total = 0;
+};
+
+// One reference run (one ThinkvMethod, sim.cpp:494-545): a sequence's units,
+// its event log, step counters and dumps.
+struct SeqRec {
+  int unit0 = 0, nunits = 0;
+  int group0 = 0, ngroups = 0;
   std::vector<EventRec> events;
   int64_t eviction_steps = 0, transition_calls = 0, overflow_calls = 0, infeasible_events = 0;
   std::map<std::string, int64_t> gen_by_thought;
@@ -152,6 +165,8 @@ struct tkv_run {
   TkvState st{};
   cudaStream_t stream = nullptr;
   std::vector<Group> groups;
+  std::vector<SeqRec> seqs;
+  int group_units = 1;  // units per planning group (units_per_seq, or 1 per layer)
   int64_t pos = 0;
   int cur_half = 0;
   int buf_len = 0;
@@ -269,7 +284,6 @@ void validate(const tkv_run_desc& d) {
     if (errs.empty() && d.budget < d.num_thoughts * d.levels[d.num_levels - 1])
       errs.push_back("budget must be >= num_thoughts * retention floor");
   }
-  if (d.per_layer_thought) errs.push_back("per_layer_thought is not supported by this version");
   if (d.scripted) {
     if (d.script_len < 1 || !d.script_bands) errs.push_back("scripted trace has no labels");
     else
@@ -569,7 +583,9 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
       ev.evicted += x.second.m - x.second.K;
     }
     ev.after = g.total;
-    if (r->desc.record_events) g.events.push_back(std::move(ev));
+    ev.layer0 = g.unit0 - r->seqs[g.seq].unit0;
+    ev.nlayers = g.nunits;
+    if (r->desc.record_events) r->seqs[g.seq].events.push_back(std::move(ev));
   }
 }
 
@@ -587,8 +603,7 @@ void flush_all(tkv_run* r, int64_t step) {
   }
   TkvFlushCtl* d_ctl = upload(r, ctl.data(), ctl.size());
   launch(r, CAT_FLUSH, "flush kernel", [&] {
-    return tkv_launch_flush(r->st, r->cur_half, r->buf_len, (int)r->buf_pos0, d_ctl, r->desc.units_per_seq,
-                            r->stream);
+    return tkv_launch_flush(r->st, r->cur_half, r->buf_len, (int)r->buf_pos0, d_ctl, r->group_units, r->stream);
   });
   if (r->desc.record_events) {
     for (size_t gi = 0; gi < r->groups.size(); ++gi) {
@@ -599,7 +614,9 @@ void flush_all(tkv_run* r, int64_t step) {
       ev.fmt = r->st.dm.band_fmt[g.segs[g.open].band];
       ev.tokens = r->buf_len;
       ev.pad = r->desc.group_size - r->buf_len;
-      g.events.push_back(ev);
+      ev.layer0 = g.unit0 - r->seqs[g.seq].unit0;
+      ev.nlayers = g.nunits;
+      r->seqs[g.seq].events.push_back(ev);
     }
   }
   r->cur_half ^= 1;
@@ -618,7 +635,7 @@ void boundary(tkv_run* r, int64_t pos, bool decode) {
   const tkv_run_desc& d = r->desc;
   flush_all(r, pos);
   std::vector<GroupPlan> plans;
-  std::vector<bool> fired(r->groups.size(), false);
+  std::vector<char> fired(r->seqs.size(), 0);
   for (size_t gi = 0; gi < r->groups.size(); ++gi) {
     Group& g = r->groups[gi];
     if (g.open < 0) continue;
@@ -629,41 +646,48 @@ void boundary(tkv_run* r, int64_t pos, bool decode) {
       plans.push_back(plan_transition(r, g, (int)gi, closing));
       bool pred = false;
       for (const HSeg& s : g.segs) pred = pred || s.start < closing;
-      fired[gi] = pred;
+      fired[g.seq] |= pred;
     }
     g.open = -1;
   }
   if (!plans.empty()) execute_plans(r, plans, pos);
-  for (size_t gi = 0; gi < r->groups.size(); ++gi) {
-    if (!fired[gi]) continue;
-    r->groups[gi].transition_calls += 1;
-    r->groups[gi].eviction_steps += 1;
+  for (size_t si = 0; si < r->seqs.size(); ++si) {
+    if (!fired[si]) continue;
+    r->seqs[si].transition_calls += 1;
+    r->seqs[si].eviction_steps += 1;
   }
-  // labels for the next interval
-  const int U = d.units_per_seq;
+  // labels for the next interval: one per sequence (scripted, or classify of
+  // the mean over the calibrated layers), or one per layer (per_layer_thought)
+  const bool per_layer = d.per_layer_thought && !d.scripted;
   std::vector<double> sp;
   const bool need_sp = decode && (!d.scripted || d.record_events);
   if (need_sp) sp = download_sparsity(r);
-  for (size_t gi = 0; gi < r->groups.size(); ++gi) {
-    Group& g = r->groups[gi];
-    int band = prefill_band(d.num_thoughts);
+  for (size_t si = 0; si < r->seqs.size(); ++si) {
+    SeqRec& q = r->seqs[si];
+    std::vector<int> bands(q.ngroups, prefill_band(d.num_thoughts));
     double mean = 0.0;
     if (decode) {
       const int64_t dstep = pos - d.prompt_len;
       const int64_t interval = dstep / d.tau;
+      auto classify = [&](double x) {  // thought.cpp:353-359
+        int band = 0;
+        for (int i = 0; i < d.num_thresholds; ++i)
+          if (x > d.thresholds[i]) ++band;
+        return band;
+      };
       if (d.scripted) {
         const int64_t i = std::min<int64_t>(interval, d.script_len - 1);
-        band = r->script[(size_t)g.seq * d.script_len + i];
+        std::fill(bands.begin(), bands.end(), r->script[(size_t)si * d.script_len + i]);
         if (need_sp) {
-          for (int u = 0; u < U; ++u) mean += sp[(size_t)g.unit0 + u];
-          mean /= (double)U;
+          for (int u = 0; u < q.nunits; ++u) mean += sp[(size_t)q.unit0 + u];
+          mean /= (double)q.nunits;
         }
+      } else if (per_layer) {
+        for (int gi = 0; gi < q.ngroups; ++gi) bands[gi] = classify(sp[(size_t)r->groups[q.group0 + gi].unit0]);
       } else {
-        for (int i = 0; i < std::min(d.num_calib_units, 64); ++i) mean += sp[(size_t)g.unit0 + d.calib_units[i]];
+        for (int i = 0; i < d.num_calib_units; ++i) mean += sp[(size_t)q.unit0 + d.calib_units[i]];
         mean /= (double)d.num_calib_units;
-        band = 0;
-        for (int i = 0; i < d.num_thresholds; ++i)
-          if (mean > d.thresholds[i]) ++band;  // classify (thought.cpp:353-359)
+        std::fill(bands.begin(), bands.end(), classify(mean));
       }
       if (d.record_events) {
         EventRec ev;
@@ -671,22 +695,27 @@ void boundary(tkv_run* r, int64_t pos, bool decode) {
         ev.step = pos;
         ev.dstep = dstep;
         ev.sparsity = mean;
-        ev.band = band;
-        g.events.push_back(ev);
+        ev.band = bands[0];
+        if (per_layer) ev.bands = bands;
+        q.events.push_back(ev);
       }
     }
-    HSeg s;
-    s.id = g.next_seg_id++;
-    s.band = band;
-    s.start = pos;
-    s.open = true;
-    s.dev = (int)g.segs.size();
-    if (s.dev >= r->st.dm.NSEG) throw TkvError(TKV_ERR_UNEXPECTED, "segment capacity exceeded");
-    g.segs.push_back(s);
-    g.open = s.dev;
+    for (int gi = 0; gi < q.ngroups; ++gi) {
+      Group& g = r->groups[q.group0 + gi];
+      HSeg s;
+      s.id = g.next_seg_id++;
+      s.band = bands[gi];
+      s.start = pos;
+      s.open = true;
+      s.dev = (int)g.segs.size();
+      if (s.dev >= r->st.dm.NSEG) throw TkvError(TKV_ERR_UNEXPECTED, "segment capacity exceeded");
+      g.segs.push_back(s);
+      g.open = s.dev;
+    }
   }
 }
 
+// Case-2 budget enforcement (sim.cpp:819-837 in process, :876-883 in finish).
 void overflow_pass(tkv_run* r, int64_t step, bool decode, bool final_pass) {
   std::vector<GroupPlan> plans;
   for (size_t gi = 0; gi < r->groups.size(); ++gi) {
@@ -696,13 +725,23 @@ void overflow_pass(tkv_run* r, int64_t step, bool decode, bool final_pass) {
   }
   if (plans.empty()) return;
   execute_plans(r, plans, step);
+  std::vector<char> any(r->seqs.size(), 0), infeasible(r->seqs.size(), 0);
   for (const GroupPlan& p : plans) {
-    Group& g = r->groups[p.group];
-    // process() counts one infeasible event per step; finish() counts one per
-    // layer whose final plan is infeasible (sim.cpp:835-837 vs :879).
-    if (p.infeasible) g.infeasible_events += final_pass ? g.nunits : 1;
-    g.overflow_calls += 1;  // any_overflow / final_overflow per sequence
-    if (decode && !final_pass) g.eviction_steps += 1;
+    const Group& g = r->groups[p.group];
+    any[g.seq] = 1;
+    if (!p.infeasible) continue;
+    infeasible[g.seq] = 1;
+    // finish() counts one infeasible event per layer whose final plan is
+    // infeasible (sim.cpp:879); process() one per step (:835-837)
+    if (final_pass) r->seqs[g.seq].infeasible_events += g.nunits;
+  }
+  for (size_t si = 0; si < r->seqs.size(); ++si) {
+    if (!any[si]) continue;
+    SeqRec& q = r->seqs[si];
+    q.overflow_calls += 1;
+    if (final_pass) continue;
+    if (decode) q.eviction_steps += 1;
+    if (infeasible[si]) q.infeasible_events += 1;
   }
 }
 
@@ -798,25 +837,29 @@ std::vector<int64_t> members_of(const tkv_run* r, const UnitSnap& s, const HSeg&
   return m;
 }
 
-json segments_json(const tkv_run* r, const Group& g, const std::vector<UnitSnap>& snaps) {  // sim.cpp:919-937
+json segments_json(const tkv_run* r, const SeqRec& q, const std::vector<UnitSnap>& snaps) {  // sim.cpp:919-937
   json units = json::array();
-  for (int i = 0; i < g.nunits; ++i) {
-    json arr = json::array();
-    for (const HSeg& s : g.segs) {
-      const auto mem = members_of(r, snaps[i], s);
-      if ((int64_t)mem.size() != s.size)
-        throw TkvError(TKV_ERR_INTEGRITY, "device member mask disagrees with the host segment size");
-      arr.push_back(json{{"id", s.id},
-                         {"band", s.band},
-                         {"thought", thought_name(s.band, r->desc.num_thoughts)},
-                         {"start", s.start},
-                         {"anneal_level", s.level},
-                         {"open", s.open},
-                         {"initial_size", s.initial},
-                         {"size", s.size},
-                         {"members", mem}});
+  for (int gi = 0; gi < q.ngroups; ++gi) {
+    const Group& g = r->groups[q.group0 + gi];
+    for (int i = 0; i < g.nunits; ++i) {
+      const UnitSnap& snap = snaps[g.unit0 - q.unit0 + i];
+      json arr = json::array();
+      for (const HSeg& s : g.segs) {
+        const auto mem = members_of(r, snap, s);
+        if ((int64_t)mem.size() != s.size)
+          throw TkvError(TKV_ERR_INTEGRITY, "device member mask disagrees with the host segment size");
+        arr.push_back(json{{"id", s.id},
+                           {"band", s.band},
+                           {"thought", thought_name(s.band, r->desc.num_thoughts)},
+                           {"start", s.start},
+                           {"anneal_level", s.level},
+                           {"open", s.open},
+                           {"initial_size", s.initial},
+                           {"size", s.size},
+                           {"members", mem}});
+      }
+      units.push_back(std::move(arr));
     }
-    units.push_back(std::move(arr));
   }
   return units;
 }
@@ -843,7 +886,7 @@ void check_device_errors(tkv_run* r) {
   }
 }
 
-json events_json_lines(tkv_run* r, const Group& g, std::string* out) {
+json events_json_lines(tkv_run* r, const SeqRec& g, std::string* out) {
   // evicted ids come from the device log
   std::vector<uint32_t> log;
   if (r->log_used > 0) {
@@ -853,15 +896,16 @@ json events_json_lines(tkv_run* r, const Group& g, std::string* out) {
   const int W = r->st.dm.W;
   std::string s;
   for (const EventRec& e : g.events) {
-    for (int i = 0; i < g.nunits; ++i) {
-      if (e.kind == 2) {
-        if (i > 0) break;
-        json ev{{"type", "refresh"}, {"step", e.step}, {"dstep", e.dstep}, {"sparsity", e.sparsity}, {"band", e.band}};
-        s += ev.dump() + "\n";
-        continue;
-      }
+    if (e.kind == 2) {
+      json ev{{"type", "refresh"}, {"step", e.step}, {"dstep", e.dstep}, {"sparsity", e.sparsity}};
+      if (e.bands.empty()) ev["band"] = e.band;
+      else ev["bands"] = e.bands;
+      s += ev.dump() + "\n";
+      continue;
+    }
+    for (int i = 0; i < e.nlayers; ++i) {
       if (e.kind == 0) {
-        json ev{{"type", "emit"}, {"step", e.step}, {"layer", i}, {"format", format_name(e.fmt)},
+        json ev{{"type", "emit"}, {"step", e.step}, {"layer", e.layer0 + i}, {"format", format_name(e.fmt)},
                 {"tokens", e.tokens}, {"pad", e.pad}};
         s += ev.dump() + "\n";
         continue;
@@ -884,7 +928,7 @@ json events_json_lines(tkv_run* r, const Group& g, std::string* out) {
       json ev{{"type", "evict"},
               {"trigger", e.trigger == 0 ? "transition_end" : "budget_overflow"},
               {"step", e.step},
-              {"layer", i},
+              {"layer", e.layer0 + i},
               {"segments", segs},
               {"infeasible", e.infeasible},
               {"retained_before", e.after + e.evicted},
@@ -897,7 +941,7 @@ json events_json_lines(tkv_run* r, const Group& g, std::string* out) {
 }
 
 // Metrics (ThinkvMethod::finish, sim.cpp:889-957) from device state.
-json metrics_json(tkv_run* r, const Group& g, const std::vector<UnitSnap>& snaps) {
+json metrics_json(tkv_run* r, const SeqRec& g, const std::vector<UnitSnap>& snaps) {
   const TkvDims& dm = r->st.dm;
   const tkv_run_desc& d = r->desc;
   int64_t bits = 0, slots = 0;
@@ -1040,8 +1084,12 @@ void step_end(tkv_run* r, const StepCtx& c) {
     open.size += 1;
     open.initial += 1;
     g.total += 1;
-    if (c.decode) g.gen_by_thought[thought_name(open.band, d.num_thoughts)] += 1;
   }
+  if (c.decode)  // generated_by_thought counts layer 0's label (sim.cpp:809-812)
+    for (SeqRec& q : r->seqs) {
+      const Group& g0 = r->groups[q.group0];
+      q.gen_by_thought[thought_name(g0.segs[g0.open].band, d.num_thoughts)] += 1;
+    }
   // 4. emission at g tokens
   if (r->buf_len >= d.group_size) flush_all(r, pos);
   // 5. Case-2 budget enforcement
@@ -1049,10 +1097,10 @@ void step_end(tkv_run* r, const StepCtx& c) {
   end_phase(r);
   if (r->dump_at.count(pos)) {
     check_device_errors(r);
-    for (Group& g : r->groups) {
-      const auto snaps = snapshot(r, g.unit0, g.nunits);
-      g.step_dumps[std::to_string(pos)] = json{{"block_tables", tables_json(r, snaps)},
-                                               {"segments", segments_json(r, g, snaps)}};
+    for (SeqRec& q : r->seqs) {
+      const auto snaps = snapshot(r, q.unit0, q.nunits);
+      q.step_dumps[std::to_string(pos)] = json{{"block_tables", tables_json(r, snaps)},
+                                               {"segments", segments_json(r, q, snaps)}};
     }
   }
   r->pos += 1;
@@ -1077,9 +1125,9 @@ void do_finish(tkv_run* r) {
   end_phase(r);
   check_device_errors(r);
   r->metrics.clear();
-  for (Group& g : r->groups) {
-    const auto snaps = snapshot(r, g.unit0, g.nunits);
-    r->metrics.push_back(metrics_json(r, g, snaps));
+  for (SeqRec& q : r->seqs) {
+    const auto snaps = snapshot(r, q.unit0, q.nunits);
+    r->metrics.push_back(metrics_json(r, q, snaps));
   }
   r->finished = true;
 }
@@ -1189,13 +1237,23 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   r->d_scratch = dalloc<double>(r, (size_t)r->scratch_ctas * r->scratch_per_cta);
   r->km_sums_ctas = 2048;  // row blocks at the widest class; narrower classes fit proportionally more
   r->km_sums = dalloc<double>(r, (size_t)r->km_sums_ctas * std::max(1, r->max_m - 1) * (2 * dm.D + 1));  // sums | means (128-point class)
-  // groups = sequences
+  // sequences, and their planning groups: the whole sequence, or one unit
+  // per group when labels are per layer (sizes then evolve per layer)
+  r->group_units = (d.per_layer_thought && !d.scripted) ? 1 : d.units_per_seq;
   for (int s = 0; s < d.num_seqs; ++s) {
-    Group g;
-    g.seq = s;
-    g.unit0 = s * d.units_per_seq;
-    g.nunits = d.units_per_seq;
-    r->groups.push_back(std::move(g));
+    SeqRec q;
+    q.unit0 = s * d.units_per_seq;
+    q.nunits = d.units_per_seq;
+    q.group0 = (int)r->groups.size();
+    q.ngroups = d.units_per_seq / r->group_units;
+    for (int i = 0; i < q.ngroups; ++i) {
+      Group g;
+      g.seq = s;
+      g.unit0 = q.unit0 + i * r->group_units;
+      g.nunits = r->group_units;
+      r->groups.push_back(std::move(g));
+    }
+    r->seqs.push_back(std::move(q));
   }
   CUDA_OK(cudaStreamSynchronize(r->stream));
 }
@@ -1482,10 +1540,10 @@ int64_t tkv_position(const tkv_run* run) { return run->pos; }
 
 int tkv_dump_json(tkv_run* run, int seq, const char* what, char* buf, size_t cap, size_t* needed) {
   try {
-    if (seq < 0 || seq >= (int)run->groups.size()) throw TkvError(TKV_ERR_CONFIG, "no such sequence");
+    if (seq < 0 || seq >= (int)run->seqs.size()) throw TkvError(TKV_ERR_CONFIG, "no such sequence");
     check_device_errors(run);
     const std::string w(what);
-    Group& g = run->groups[seq];
+    SeqRec& g = run->seqs[seq];
     std::string s;
     if (w == "tables") {
       s = tables_json(run, snapshot(run, g.unit0, g.nunits)).dump();

@@ -46,7 +46,7 @@ def _desc(**kw):
     (dict(psi_bits=(4, 3, 2)), "unsupported precision"),
     (dict(scripted=False), "thresholds"),
     (dict(script=[[7]]), "scripted band out of range"),
-    (dict(per_layer_thought=True), "per_layer_thought"),
+    (dict(scripted=False, thresholds=(0.3, 0.6), calib_units=(5,)), "calibration layer index out of range"),
 ])
 def test_config_validation_codes(bad, msg):
     from paper_2510_01290_b200 import _abi

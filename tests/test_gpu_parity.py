@@ -68,6 +68,14 @@ CONFIGS = {
                                       group_size=16, block_size=8, budget=60, levels=(12, 6, 3),
                                       psi_bits=(8, 16, 2), prompt_len=20, max_gen_len=300,
                                       script=script(1, 14, seed=9, pT=300), record_events=True),
+    # per-layer labels (per_layer_thought, sim.cpp:713-716, :728-730): every layer
+    # classifies its own sparsity, so layers of a sequence get different bands,
+    # Case-1 transitions fire per layer and their segment sizes diverge
+    "per_layer_calibrated": ThinkvConfig(num_seqs=2, units_per_seq=4, num_q_heads=4, head_dim=64, tau=32,
+                                         group_size=16, block_size=16, budget=90, levels=(16, 8, 4),
+                                         max_gen_len=400, scripted=False, thresholds=(0.965, 0.978),
+                                         calib_units=(0, 2), per_layer_thought=True, record_events=True,
+                                         dump_positions=(127, 255)),
     # calibrated labels from the fp64 sparsity kernel (refresh steps only)
     "calibrated": ThinkvConfig(num_seqs=2, units_per_seq=3, num_q_heads=4, head_dim=64, tau=32,
                                group_size=16, block_size=16, budget=90, levels=(16, 8, 4),
@@ -81,6 +89,9 @@ def test_parity_synthetic(name):
     cfg = CONFIGS[name]
     res = run_parity(cfg)
     compare_state(res, cfg)
+    if cfg.per_layer_thought:  # the layers really got different labels
+        ev = [json.loads(l) for l in res["run"].events(0).splitlines()]
+        assert any(len(set(e["bands"])) > 1 for e in ev if e["type"] == "refresh")
 
 
 def test_parity_full_tau_kmeans():
