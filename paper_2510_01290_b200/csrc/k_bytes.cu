@@ -18,7 +18,8 @@
 // index of live slots only (coalesced) and marks distinct live windows in a
 // shared-memory bitmap (one bit per window id).  Runs when byte accounting is
 // enabled (tkv_bytes_accounting), right after the attention launch of a step,
-// so every timed K1 launch is matched with its own exact byte count.
+// so every timed K1 launch is matched with its own exact byte count.  Counts
+// accumulate per unit (acc[u][5]); the host sums the rows when it reads them.
 #include <cuda_runtime.h>
 
 #include "tkv_kernels.h"
@@ -88,16 +89,24 @@ __global__ void __launch_bounds__(kThreads) bytes_kernel(TkvState st, unsigned l
   __syncthreads();
   for (int i = threadIdx.x; i < 2 * nwords; i += kThreads)
     scale += (unsigned long long)__popc(win_bits[i]) * (i < nwords ? (unsigned)dm.D : 8u);
+  // block reduce, then one plain add per counter into this unit's own row
+  // (no same-address atomics across the grid)
+  __shared__ unsigned long long red[kThreads / 32][5];
   unsigned long long v[5] = {live, resident, code, scale, meta};
 #pragma unroll
   for (int j = 0; j < 5; ++j) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
   }
-  if ((threadIdx.x & 31) == 0) {
+  if ((threadIdx.x & 31) == 0)
 #pragma unroll
-    for (int j = 0; j < 5; ++j)
-      if (v[j]) atomicAdd(acc + j, v[j]);
+    for (int j = 0; j < 5; ++j) red[threadIdx.x >> 5][j] = v[j];
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    unsigned long long t = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) t += red[w][threadIdx.x];
+    acc[(int64_t)u * 5 + threadIdx.x] += t;
   }
 }
 

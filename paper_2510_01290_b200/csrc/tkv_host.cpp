@@ -208,7 +208,7 @@ struct tkv_run {
   int64_t launches = 0;
   // device byte accounting (tkv_bytes_accounting)
   bool bytes_on = false;
-  unsigned long long* d_bytes_acc = nullptr;  // [5]
+  unsigned long long* d_bytes_acc = nullptr;  // [U][5] per-unit sums
   int64_t bytes_launches = 0, bytes_host = 0;  // accounted launches, host-known bytes (buffer, q, out)
   // host-pointer step staging: two slots, copies on their own stream so the
   // transfers of one step overlap the kernels of its neighbours
@@ -1213,7 +1213,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   st.max_live = st.dm.NS;
   if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 256, 0);
   st.err = dalloc<int32_t>(r, U);
-  r->d_bytes_acc = dalloc<unsigned long long>(r, 5, 0);
+  r->d_bytes_acc = dalloc<unsigned long long>(r, U * 5, 0);
   check_launch(tkv_launch_init(st, r->stream), "init kernel");
   // arenas
   r->arena_cap = 8 << 20;
@@ -1620,7 +1620,7 @@ int tkv_exp_f64(tkv_ctx* ctx, const double* x, double* y, int64_t n) {
 int tkv_bytes_accounting(tkv_run* run, int enable) {
   try {
     if (!run) throw TkvError(TKV_ERR_CONFIG, "null run");
-    CUDA_OK(cudaMemsetAsync(run->d_bytes_acc, 0, 5 * sizeof(unsigned long long), run->stream));
+    CUDA_OK(cudaMemsetAsync(run->d_bytes_acc, 0, (size_t)run->st.dm.U * 5 * sizeof(unsigned long long), run->stream));
     run->bytes_launches = 0;
     run->bytes_host = 0;
     run->bytes_on = enable != 0;
@@ -1635,9 +1635,12 @@ int tkv_bytes_accounting(tkv_run* run, int enable) {
 int tkv_bytes_accumulated(tkv_run* run, tkv_bytes_t* sum, int64_t* launches) {
   try {
     if (!run || !sum) throw TkvError(TKV_ERR_CONFIG, "null argument");
-    unsigned long long acc[5];
-    CUDA_OK(cudaMemcpyAsync(acc, run->d_bytes_acc, sizeof(acc), cudaMemcpyDeviceToHost, run->stream));
+    std::vector<unsigned long long> per_unit((size_t)run->st.dm.U * 5);
+    CUDA_OK(cudaMemcpyAsync(per_unit.data(), run->d_bytes_acc, per_unit.size() * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, run->stream));
     CUDA_OK(cudaStreamSynchronize(run->stream));
+    unsigned long long acc[5] = {0, 0, 0, 0, 0};
+    for (size_t i = 0; i < per_unit.size(); ++i) acc[i % 5] += per_unit[i];
     std::memset(sum, 0, sizeof(*sum));
     sum->live_slots = (int64_t)acc[0];
     sum->resident_slots = (int64_t)acc[1];
