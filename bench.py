@@ -335,10 +335,18 @@ def main():
         return
 
     import torch
+    ndev = torch.cuda.device_count()
+    local = local % max(1, ndev)  # more ranks than GPUs (a 1-GPU rehearsal): ranks share devices
     torch.cuda.set_device(local)
+    coll = None  # device the collectives run on
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if ndev >= world:  # one GPU per rank: NCCL over NVLink / NVSwitch
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            coll = torch.device("cuda", local)
+        else:  # NCCL cannot put two ranks on one GPU; gloo through the host
+            dist.init_process_group("gloo")
+            coll = torch.device("cpu")
     from paper_2510_01290_b200 import DecodeRun
 
     dev = torch.device("cuda", local)
@@ -386,7 +394,7 @@ def main():
         print("[bench] step ms: " + " ".join(f"{x:.3f}" for x in step_ms), file=sys.stderr)
     window_ms = evs[0].elapsed_time(evs[K])
     tpot, bnd, oth = amortize(step_ms, start, cfg.tau)
-    ms_t = torch.tensor([tpot, window_ms / K], device=dev, dtype=torch.float64)
+    ms_t = torch.tensor([tpot, window_ms / K], device=coll or dev, dtype=torch.float64)
     if world > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
     tpot_max, window_max = float(ms_t[0].item()), float(ms_t[1].item())
@@ -409,18 +417,29 @@ def main():
         run.step_host_async(hq, hk, hv, pouts[i % 2])
     run.synchronize()
     e2e_s = time.perf_counter() - t0
-    e2e_t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+    e2e_t = torch.tensor([e2e_s], device=coll or dev, dtype=torch.float64)
     if world > 1:
         torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
     e2e_s = float(e2e_t.item())
     run.synchronize()
     # stats gather over NVLink (the path's only collective)
-    stats = torch.tensor([tpot, tm["attend_ms"], tm["anneal_ms"], float(acc["live_slots"])], device=dev,
+    stats = torch.tensor([tpot, tm["attend_ms"], tm["anneal_ms"], float(acc["live_slots"])], device=coll or dev,
                          dtype=torch.float64)
     gathered = [stats]
+    verify = None
     if world > 1:
         gathered = [torch.zeros_like(stats) for _ in range(world)]
         torch.distributed.all_gather(gathered, stats)
+        # verify mode: the last step's outputs of every rank,
+        # gathered into the global batch (untimed)
+        from paper_2510_01290_b200.shard import gather_outputs
+        last = pouts[(E - 1) % 2].to(dev)
+        t0 = time.perf_counter()
+        allout = gather_outputs(last, global_seqs(args, world), cfg.units_per_seq)
+        torch.cuda.synchronize(dev)
+        verify = {"gathered_outputs": list(allout.shape), "bytes": allout.numel() * 4,
+                  "ms": (time.perf_counter() - t0) * 1e3, "backend": torch.distributed.get_backend(),
+                  "sum": float(allout.double().sum().item())}
 
     parity = None
     cb = None
@@ -475,6 +494,7 @@ def main():
     }
     if world > 1:
         line["per_rank_tpot_ms"] = [float(g[0].item()) for g in gathered]
+        line["verify_gather"] = verify
     if cb is not None:
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         line["parity"] = parity

@@ -55,3 +55,25 @@ def max_over_ranks(x: float, device=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_outputs(out, global_seqs: int, units_per_seq: int):
+    """Verify mode: all-gather every rank's attention outputs
+    [its units, rows, d] into the global batch [global_seqs * units_per_seq,
+    rows, d] on every rank (NCCL over NVLink on the GPU box; gloo needs host
+    tensors, so the gather goes through the CPU there).  Ranks hold
+    contiguous sequence blocks (seq_range), padded to the largest block for
+    the collective."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return out
+    world = dist.get_world_size()
+    sizes = [(e - b) * units_per_seq for b, e in (seq_range(global_seqs, r, world) for r in range(world))]
+    width = max(sizes)
+    dev = out.device if dist.get_backend() == "nccl" else torch.device("cpu")
+    pad = torch.zeros((width,) + tuple(out.shape[1:]), dtype=out.dtype, device=dev)
+    pad[: out.shape[0]] = out.to(dev)
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    return torch.cat([p[:n] for p, n in zip(parts, sizes)]).to(out.device)
