@@ -1552,6 +1552,313 @@ __global__ void __launch_bounds__(32 * kTinyWarps) km_tiny_kernel(TkvState st, c
 }
 
 // ---------------------------------------------------------------------------
+// tiny instances, subset-table form (m <= 8, f16-exact unscaled keys: every
+// band quantised, no FP8 window scale).  Every centroid kmeans_from_seeds
+// ever forms is the mean of a subset S of the m points: a seed is x_s / 1,
+// Lloyd's next[c] is (members summed in index order) / |S|, Hartigan's
+// mean_of(c) is (running sum) / |S| (evictor.cpp:94-251).  With f16-exact
+// keys every such sum is exact (|x| <= 65504, multiples of 2^-24: at most 43
+// significant bits for 8 points), so each is fl(exact subset sum / |S|) --
+// the same bits whichever path built it.  Hence dist2(x_i, mean(S)) for all
+// 2^m - 1 subsets, each the reference's channel-order chain, is one table
+// per instance, built once by all threads; every restart (70 for the
+// 8 -> 4 anneal) then runs Lloyd assignments, empty-cluster repair and
+// Hartigan moves on table lookups, one warp per restart.  Only the Lloyd
+// movement test, the pairwise-swap delta and its filter recompute means, in
+// the reference's operation order.
+// ---------------------------------------------------------------------------
+constexpr int kTabWarps = 8;
+
+struct TabState {  // per warp, warp-uniform
+  int assign[kTinyM];
+  int sizes[kTinyM];
+  unsigned cur[kTinyM];  // subset (point bitmask) whose mean is centroid c
+  int seeds[kTinyM];
+};
+
+// mean(S) channel ch: the exact subset sum / |S| (div_n: the reference's division bits)
+__device__ __forceinline__ double tab_mean(const double* X, int D, unsigned S, int n, int ch) {
+  double acc = 0.0;
+  while (S) {
+    const int i = __ffs(S) - 1;
+    S &= S - 1;
+    acc = __dadd_rn(acc, X[i * D + ch]);
+  }
+  return div_n(acc, n);
+}
+
+__global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops,
+                                                                  int nops, const int32_t* __restrict__ item_prefix,
+                                                                  int nitems, int item0, uint8_t* __restrict__ scratch,
+                                                                  KmGeo geo) {
+  const TkvDims& dm = st.dm;
+  const int item = item0 + blockIdx.x;
+  if (item >= nitems) return;
+  const int oi = find_op(item_prefix, nops, item);
+  const TkvAnnealOp op = ops[oi];
+  uint8_t* base = scratch + (int64_t)blockIdx.x * geo.bytes();
+  const int32_t* misc = reinterpret_cast<const int32_t*>(base + geo.misc_off());
+  if (misc[1]) return;
+  const int m = misc[0], K = op.K, D = dm.D;
+  const int nr = op.nrestart > 0 ? op.nrestart : op.ncombos;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nsub = 1 << m;
+  extern __shared__ __align__(16) uint8_t dyn[];
+  double* X = reinterpret_cast<double*>(dyn);  // [m][D] exact keys
+  __shared__ double T[kTinyM][256];            // dist2(x_i, mean(S))
+  __shared__ double M2[256];                   // |mean(S)|^2 (swap-filter error bound only)
+  __shared__ double pd[kTinyM][kTinyM];
+  __shared__ double tx2[kTinyM];
+  __shared__ double tabA[kTinyM + 1], tabR[kTinyM + 1];  // n / (n + 1.0), -n / (n - 1.0) (evictor.cpp:201, 205)
+  __shared__ TabState ws[kTabWarps];
+  TabState& w = ws[warp];
+  {
+    const float* gX = reinterpret_cast<const float*>(base + geo.x_off());
+    const double* gpd = reinterpret_cast<const double*>(base + geo.pd_off());
+    for (int i = threadIdx.x; i < m * D; i += blockDim.x) X[i] = (double)gX[i];
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) pd[t / m][t % m] = gpd[(int64_t)(t / m) * geo.mmax + t % m];
+    for (int n = threadIdx.x; n <= kTinyM; n += blockDim.x) {
+      const double dn = (double)n;
+      tabA[n] = __ddiv_rn(dn, __dadd_rn(dn, 1.0));
+      tabR[n] = __ddiv_rn(-dn, __dsub_rn(dn, 1.0));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    double acc = 0.0;
+    for (int ch = 0; ch < D; ++ch) acc += X[i * D + ch] * X[i * D + ch];
+    tx2[i] = acc * 1.000001;
+  }
+  // ---- the subset table: one subset per thread, m chains in channel order ----
+  for (int S = threadIdx.x + 1; S < nsub; S += blockDim.x) {
+    const int n = __popc(S);
+    double d[kTinyM];
+#pragma unroll
+    for (int i = 0; i < kTinyM; ++i) d[i] = 0.0;
+    double m2 = 0.0;
+    for (int ch = 0; ch < D; ++ch) {
+      const double mu = tab_mean(X, D, (unsigned)S, n, ch);
+#pragma unroll
+      for (int i = 0; i < kTinyM; ++i) {
+        if (i < m) {
+          const double t = __dsub_rn(X[i * D + ch], mu);
+          d[i] = __dadd_rn(d[i], __dmul_rn(t, t));
+        }
+      }
+      m2 += mu * mu;
+    }
+#pragma unroll
+    for (int i = 0; i < kTinyM; ++i)
+      if (i < m) T[i][S] = d[i];
+    M2[S] = m2;
+  }
+  __syncthreads();
+  const int32_t* ids = reinterpret_cast<const int32_t*>(base + geo.ids_off());
+  for (int r = warp; r < nr; r += kTabWarps) {
+    // ---- seeds: the r-th K-subset in lexicographic order (evictor.cpp:274-283),
+    //      or the prep kernel's farthest-first sets
+    if (lane == 0) {
+      if (op.nrestart > 0) {
+        const int32_t* sd = reinterpret_cast<const int32_t*>(base + geo.seeds_off()) + r * geo.kmax;
+        for (int c = 0; c < K; ++c) w.seeds[c] = sd[c];
+      } else {
+        int rank = r, x = 0;
+        for (int c = 0; c < K; ++c) {
+          while (true) {
+            int cnt = 1;
+            const int n = m - x - 1, k = K - c - 1;
+            for (int t = 0; t < k; ++t) cnt = cnt * (n - t) / (t + 1);
+            if (rank < cnt) break;
+            rank -= cnt;
+            ++x;
+          }
+          w.seeds[c] = x;
+          ++x;
+        }
+      }
+      for (int c = 0; c < K; ++c) w.cur[c] = 1u << w.seeds[c];
+    }
+    __syncwarp();
+    // ---- Lloyd (evictor.cpp:102-159) on table lookups ----------------------------
+    for (int iter = 0; iter < 50; ++iter) {
+      int a = 0;
+      if (lane < m) {  // nearest centroid, ties to the lowest index
+        double bd = T[lane][w.cur[0]];
+        for (int c = 1; c < K; ++c) {
+          const double d = T[lane][w.cur[c]];
+          if (d < bd) { bd = d; a = c; }
+        }
+        w.assign[lane] = a;
+      }
+      unsigned nxt[kTinyM];
+      for (int c = 0; c < K; ++c) {
+        nxt[c] = __ballot_sync(0xffffffffu, lane < m && a == c);
+        if (lane == 0) w.sizes[c] = __popc(nxt[c]);
+      }
+      __syncwarp();
+      if (lane == 0) {  // empty-cluster repair (evictor.cpp:123-141): distances to the current centroids
+        for (int c = 0; c < K; ++c) {
+          if (w.sizes[c] > 0) continue;
+          int donor = 0;
+          for (int dd = 1; dd < K; ++dd)
+            if (w.sizes[dd] > w.sizes[donor]) donor = dd;
+          int steal = m;
+          double steal_d = -1.0;
+          for (int i = 0; i < m; ++i) {
+            if (w.assign[i] != donor) continue;
+            const double d = T[i][w.cur[donor]];
+            if (d > steal_d) { steal = i; steal_d = d; }
+          }
+          w.assign[steal] = c;
+          nxt[donor] &= ~(1u << steal);
+          nxt[c] |= 1u << steal;
+          --w.sizes[donor];
+          ++w.sizes[c];
+        }
+        for (int c = 0; c < K; ++c) w.seeds[c] = (int)nxt[c];  // publish the repaired subsets
+      }
+      __syncwarp();
+      for (int c = 0; c < K; ++c) nxt[c] = (unsigned)w.seeds[c];
+      // movement (evictor.cpp:153-158): an unchanged subset moves exactly 0;
+      // otherwise sum (next - old)^2 across lanes, decide "sqrt < 1e-6" with a
+      // relative margin, redo in channel order within the margin.
+      int code_max = 0;
+      for (int c = 0; c < K; ++c) {
+        if (nxt[c] == w.cur[c] || code_max == 2) continue;  // max: one moving centroid decides
+        const int nn = __popc(nxt[c]), no = __popc(w.cur[c]);
+        double part = 0.0;
+        for (int ch = lane; ch < D; ch += 32) {
+          const double t = __dsub_rn(tab_mean(X, D, nxt[c], nn, ch), tab_mean(X, D, w.cur[c], no, ch));
+          part += __dmul_rn(t, t);
+        }
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        int code;
+        if (part == 0.0) {
+          code = 0;
+        } else if (__dsqrt_rn(part * (1.0 + 1e-12)) < 1e-6) {
+          code = 1;
+        } else if (!(__dsqrt_rn(part * (1.0 - 1e-12)) < 1e-6)) {
+          code = 2;
+        } else {
+          double d = 0.0;
+          if (lane == 0)
+            for (int ch = 0; ch < D; ++ch) {
+              const double t = __dsub_rn(tab_mean(X, D, nxt[c], nn, ch), tab_mean(X, D, w.cur[c], no, ch));
+              d = __dadd_rn(d, __dmul_rn(t, t));
+            }
+          code = __shfl_sync(0xffffffffu, __dsqrt_rn(d) < 1e-6 ? 1 : 2, 0);
+        }
+        code_max = code_max > code ? code_max : code;
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (int c = 0; c < K; ++c) w.cur[c] = nxt[c];
+      __syncwarp();
+      if (code_max < 2) break;
+    }
+    // ---- Hartigan single moves + pairwise swaps (evictor.cpp:167-243) ------------
+    for (int pass = 0; pass < 100; ++pass) {
+      bool moved = false;
+      for (int i = 0; i < m; ++i) {
+        const int from = w.assign[i];
+        const int nfrom = w.sizes[from];
+        if (nfrom <= 1) continue;
+        const double removal = __dmul_rn(tabR[nfrom], T[i][w.cur[from]]);
+        double bd = 0.0;
+        int bt = 0x7fffffff;
+        if (lane < K && lane != from) {
+          const double delta = __dadd_rn(removal, __dmul_rn(tabA[w.sizes[lane]], T[i][w.cur[lane]]));
+          if (delta < -1e-12) { bd = delta; bt = lane; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {  // lowest index among the minimal deltas
+          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+          const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+          if (ot != 0x7fffffff && (bt == 0x7fffffff || od < bd || (od == bd && ot < bt))) { bd = od; bt = ot; }
+        }
+        if (bt == 0x7fffffff) continue;
+        moved = true;
+        __syncwarp();
+        if (lane == 0) {  // apply_move: the two means become other subsets' means
+          w.sizes[from] -= 1;
+          w.sizes[bt] += 1;
+          w.cur[from] &= ~(1u << i);
+          w.cur[bt] |= 1u << i;
+          w.assign[i] = bt;
+        }
+        __syncwarp();
+      }
+      if (moved) continue;
+      // pairwise swaps: pair q = lane in lexicographic order; the first
+      // improving pair is the reference's pick (nothing changes before it)
+      int pi = 0, pj = 0;
+      bool valid = false;
+      for (int i = 0, q = 0; i < m; ++i)
+        for (int j = i + 1; j < m; ++j, ++q)
+          if (q == lane) { pi = i; pj = j; valid = true; }
+      bool improving = false;
+      if (valid && w.assign[pi] != w.assign[pj] && !(w.sizes[w.assign[pi]] == 1 && w.sizes[w.assign[pj]] == 1)) {
+        // (singleton pairs: the swapped means are the two points, delta exactly 0)
+        const int ai = w.assign[pi], aj = w.assign[pj];
+        const int sa = w.sizes[ai], sb = w.sizes[aj];
+        const double na = (double)sa, nb = (double)sb;
+        const unsigned Sa = w.cur[ai], Sb = w.cur[aj];
+        const double wgt = 1.0 / na + 1.0 / nb;
+        const double dja = T[pj][Sa], dia = T[pi][Sa], dib = T[pi][Sb], djb = T[pj][Sb];
+        const double pij = pd[pi][pj];
+        const double approx = dja - dia + dib - djb - wgt * pij;
+        const double margin = 1e-12 * (dja + dia + dib + djb + wgt * pij + 16.0 * (tx2[pi] + tx2[pj]) +
+                                       4.0 * (na * M2[Sa] * 1.000001 + nb * M2[Sb] * 1.000001)) + 1e-12;
+        if (approx < -1e-12 + margin) {
+          double delta = 0.0;
+          for (int ch = 0; ch < D; ++ch) {
+            const double mua = tab_mean(X, D, Sa, sa, ch), mub = tab_mean(X, D, Sb, sb, ch);
+            const double xi = X[pi * D + ch], xj = X[pj * D + ch];
+            const double ma = __dadd_rn(mua, div_n(__dsub_rn(xj, xi), sa));
+            const double mb = __dadd_rn(mub, div_n(__dsub_rn(xi, xj), sb));
+            delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi)),
+                                               __dmul_rn(na, __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua, mua)))));
+            delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj)),
+                                               __dmul_rn(nb, __dsub_rn(__dmul_rn(mb, mb), __dmul_rn(mub, mub)))));
+          }
+          improving = delta < -1e-12;
+        }
+      }
+      const unsigned imp = __ballot_sync(0xffffffffu, improving);
+      if (!imp) break;
+      const int q = __ffs(imp) - 1;
+      const int si = __shfl_sync(0xffffffffu, pi, q), sj = __shfl_sync(0xffffffffu, pj, q);
+      __syncwarp();
+      if (lane == 0) {  // apply_move(i, a, b); apply_move(j, b, a): sizes unchanged
+        const int a = w.assign[si], b = w.assign[sj];
+        w.cur[a] = (w.cur[a] & ~(1u << si)) | (1u << sj);
+        w.cur[b] = (w.cur[b] & ~(1u << sj)) | (1u << si);
+        w.assign[si] = b;
+        w.assign[sj] = a;
+      }
+      __syncwarp();
+    }
+    // ---- cost (point order) and medoids (nearest member, ties to the lowest index)
+    double cst = 0.0;
+    for (int i = 0; i < m; ++i) cst = __dadd_rn(cst, T[i][w.cur[w.assign[i]]]);
+    int med = m;
+    if (lane < K) {
+      double bd = CUDART_INF;
+      for (int i = 0; i < m; ++i) {
+        if (w.assign[i] != lane) continue;
+        const double d = T[i][w.cur[lane]];
+        if (d < bd) { bd = d; med = i; }
+      }
+    }
+    uint32_t* mask = reinterpret_cast<uint32_t*>(base + geo.mask_off()) + (int64_t)r * geo.W;
+    for (int wd = lane; wd < geo.W; wd += 32) mask[wd] = 0;
+    __syncwarp();
+    if (lane < K) atomicOr(mask + (ids[med] >> 5), 1u << (ids[med] & 31));
+    if (lane == 0) reinterpret_cast<double*>(base + geo.cost_off())[r] = cst;
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // final: lowest cost restart -> retained mask, eviction log, segment mask
 // ---------------------------------------------------------------------------
 __global__ void km_final_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
@@ -1623,6 +1930,21 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
   if (e != cudaSuccess) {
     fprintf(stderr, "[kmeans] prep launch failed: items=%d: %s\n", item_count, cudaGetErrorString(e));
     return e;
+  }
+  if (mmax <= kTinyM && x16 && !scaled_any && getenv("TKV_KM_NO_TINY") == nullptr &&
+      getenv("TKV_KM_NO_TABLE") == nullptr) {
+    const size_t tsm = (size_t)kTinyM * st.dm.D * 8;
+    if (tsm > 16 * 1024) {
+      e = cudaFuncSetAttribute(km_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      if (e != cudaSuccess) return e;
+    }
+    km_table_kernel<<<item_count, 32 * kTabWarps, tsm, stream>>>(st, ops, nops, item_prefix, item0 + item_count, item0,
+                                                                  scratch, geo);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    km_final_kernel<<<(item_count + 127) / 128, 128, 0, stream>>>(st, ops, nops, item_prefix, item0 + item_count,
+                                                                   item0, scratch, geo, log);
+    return cudaGetLastError();
   }
   if (mmax <= kTinyM && getenv("TKV_KM_NO_TINY") == nullptr) {
     const int xb = x16 ? 2 : 4;
