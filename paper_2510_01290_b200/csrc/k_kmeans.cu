@@ -1605,6 +1605,7 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
   const int nsub = 1 << m;
   extern __shared__ __align__(16) uint8_t dyn[];
   double* X = reinterpret_cast<double*>(dyn);  // [m][D] exact keys
+  double* terms = X + kTinyM * D + warp * 2 * D;  // per warp: swap-delta terms [2D]
   __shared__ double T[kTinyM][256];            // dist2(x_i, mean(S))
   __shared__ double M2[256];                   // |mean(S)|^2 (swap-filter error bound only)
   __shared__ double pd[kTinyM][kTinyM];
@@ -1624,6 +1625,7 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
     }
   }
   __syncthreads();
+  const long long tb0 = clock64();
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     double acc = 0.0;
     for (int ch = 0; ch < D; ++ch) acc += X[i * D + ch] * X[i * D + ch];
@@ -1653,6 +1655,7 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
     M2[S] = m2;
   }
   __syncthreads();
+  if (st.kstats && threadIdx.x == 0) atomicAdd(st.kstats + 32 + 20, (unsigned long long)(clock64() - tb0));
   const int32_t* ids = reinterpret_cast<const int32_t*>(base + geo.ids_off());
   for (int r = warp; r < nr; r += kTabWarps) {
     // ---- seeds: the r-th K-subset in lexicographic order (evictor.cpp:274-283),
@@ -1679,6 +1682,7 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
       for (int c = 0; c < K; ++c) w.cur[c] = 1u << w.seeds[c];
     }
     __syncwarp();
+    const long long tl0 = clock64();
     // ---- Lloyd (evictor.cpp:102-159) on table lookups ----------------------------
     for (int iter = 0; iter < 50; ++iter) {
       int a = 0;
@@ -1725,6 +1729,15 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
       int code_max = 0;
       for (int c = 0; c < K; ++c) {
         if (nxt[c] == w.cur[c] || code_max == 2) continue;  // max: one moving centroid decides
+        // reverse triangle inequality on the table: |mu' - mu| >= |d(x_i, mu) - d(x_i, mu')|
+        double lb = 0.0;
+        if (lane < m) lb = fabs(__dsqrt_rn(T[lane][nxt[c]]) - __dsqrt_rn(T[lane][w.cur[c]]));
+        for (int o = 16; o > 0; o >>= 1) lb = fmax(lb, __shfl_xor_sync(0xffffffffu, lb, o));
+        if (lb > 2e-6) {  // movement >= 1e-6 whatever the rounding of the bound
+          code_max = 2;
+          continue;
+        }
+        if (st.kstats && lane == 0) atomicAdd(st.kstats + 32 + 25, 1ull);
         const int nn = __popc(nxt[c]), no = __popc(w.cur[c]);
         double part = 0.0;
         for (int ch = lane; ch < D; ch += 32) {
@@ -1756,6 +1769,8 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
       __syncwarp();
       if (code_max < 2) break;
     }
+    const long long th0 = clock64();
+    long long tsw = 0;
     // ---- Hartigan single moves + pairwise swaps (evictor.cpp:167-243) ------------
     for (int pass = 0; pass < 100; ++pass) {
       bool moved = false;
@@ -1788,6 +1803,7 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
         __syncwarp();
       }
       if (moved) continue;
+      const long long ts0 = clock64();
       // pairwise swaps: pair q = lane in lexicographic order; the first
       // improving pair is the reference's pick (nothing changes before it)
       int pi = 0, pj = 0;
@@ -1795,12 +1811,11 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
       for (int i = 0, q = 0; i < m; ++i)
         for (int j = i + 1; j < m; ++j, ++q)
           if (q == lane) { pi = i; pj = j; valid = true; }
-      bool improving = false;
+      bool cand = false;
       if (valid && w.assign[pi] != w.assign[pj] && !(w.sizes[w.assign[pi]] == 1 && w.sizes[w.assign[pj]] == 1)) {
         // (singleton pairs: the swapped means are the two points, delta exactly 0)
         const int ai = w.assign[pi], aj = w.assign[pj];
-        const int sa = w.sizes[ai], sb = w.sizes[aj];
-        const double na = (double)sa, nb = (double)sb;
+        const double na = (double)w.sizes[ai], nb = (double)w.sizes[aj];
         const unsigned Sa = w.cur[ai], Sb = w.cur[aj];
         const double wgt = 1.0 / na + 1.0 / nb;
         const double dja = T[pj][Sa], dia = T[pi][Sa], dib = T[pi][Sb], djb = T[pj][Sb];
@@ -1808,22 +1823,47 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
         const double approx = dja - dia + dib - djb - wgt * pij;
         const double margin = 1e-12 * (dja + dia + dib + djb + wgt * pij + 16.0 * (tx2[pi] + tx2[pj]) +
                                        4.0 * (na * M2[Sa] * 1.000001 + nb * M2[Sb] * 1.000001)) + 1e-12;
-        if (approx < -1e-12 + margin) {
+        cand = approx < -1e-12 + margin;
+      }
+      // Candidates in lexicographic order, each evaluated exactly by the whole
+      // warp: lanes compute the per-channel terms of evictor.cpp:222-225 (the
+      // means' divisions are independent across channels), lane 0 adds them in
+      // the reference's channel order.  The first improving pair is the pick.
+      unsigned cmask = __ballot_sync(0xffffffffu, cand);
+      unsigned imp = 0u;
+      while (cmask) {
+        const int q = __ffs(cmask) - 1;
+        cmask &= cmask - 1;
+        if (st.kstats && lane == 0) atomicAdd(st.kstats + 32 + 26, 1ull);
+        const int ci = __shfl_sync(0xffffffffu, pi, q), cj = __shfl_sync(0xffffffffu, pj, q);
+        const int a = w.assign[ci], b = w.assign[cj];
+        const int sa = w.sizes[a], sb = w.sizes[b];
+        const double na = (double)sa, nb = (double)sb;
+        for (int ch = lane; ch < D; ch += 32) {
+          const double mua = tab_mean(X, D, w.cur[a], sa, ch), mub = tab_mean(X, D, w.cur[b], sb, ch);
+          const double xi = X[ci * D + ch], xj = X[cj * D + ch];
+          const double ma = __dadd_rn(mua, div_n(__dsub_rn(xj, xi), sa));
+          const double mb = __dadd_rn(mub, div_n(__dsub_rn(xi, xj), sb));
+          terms[2 * ch] = __dsub_rn(__dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi)),
+                                    __dmul_rn(na, __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua, mua))));
+          terms[2 * ch + 1] = __dsub_rn(__dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj)),
+                                        __dmul_rn(nb, __dsub_rn(__dmul_rn(mb, mb), __dmul_rn(mub, mub))));
+        }
+        __syncwarp();
+        int better = 0;
+        if (lane == 0) {
           double delta = 0.0;
-          for (int ch = 0; ch < D; ++ch) {
-            const double mua = tab_mean(X, D, Sa, sa, ch), mub = tab_mean(X, D, Sb, sb, ch);
-            const double xi = X[pi * D + ch], xj = X[pj * D + ch];
-            const double ma = __dadd_rn(mua, div_n(__dsub_rn(xj, xi), sa));
-            const double mb = __dadd_rn(mub, div_n(__dsub_rn(xi, xj), sb));
-            delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xj, xj), __dmul_rn(xi, xi)),
-                                               __dmul_rn(na, __dsub_rn(__dmul_rn(ma, ma), __dmul_rn(mua, mua)))));
-            delta = __dadd_rn(delta, __dsub_rn(__dsub_rn(__dmul_rn(xi, xi), __dmul_rn(xj, xj)),
-                                               __dmul_rn(nb, __dsub_rn(__dmul_rn(mb, mb), __dmul_rn(mub, mub)))));
-          }
-          improving = delta < -1e-12;
+          for (int t = 0; t < 2 * D; ++t) delta = __dadd_rn(delta, terms[t]);
+          better = delta < -1e-12;
+        }
+        better = __shfl_sync(0xffffffffu, better, 0);
+        __syncwarp();
+        if (better) {
+          imp = 1u << q;
+          break;
         }
       }
-      const unsigned imp = __ballot_sync(0xffffffffu, improving);
+      tsw += clock64() - ts0;
       if (!imp) break;
       const int q = __ffs(imp) - 1;
       const int si = __shfl_sync(0xffffffffu, pi, q), sj = __shfl_sync(0xffffffffu, pj, q);
@@ -1836,6 +1876,12 @@ __global__ void __launch_bounds__(32 * kTabWarps) km_table_kernel(TkvState st, c
         w.assign[sj] = a;
       }
       __syncwarp();
+    }
+    if (st.kstats && lane == 0) {
+      atomicAdd(st.kstats + 32 + 21, 1ull);
+      atomicAdd(st.kstats + 32 + 22, (unsigned long long)(th0 - tl0));
+      atomicAdd(st.kstats + 32 + 23, (unsigned long long)(clock64() - th0 - tsw));
+      atomicAdd(st.kstats + 32 + 24, (unsigned long long)tsw);
     }
     // ---- cost (point order) and medoids (nearest member, ties to the lowest index)
     double cst = 0.0;
@@ -1933,7 +1979,7 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
   }
   if (mmax <= kTinyM && x16 && !scaled_any && getenv("TKV_KM_NO_TINY") == nullptr &&
       getenv("TKV_KM_NO_TABLE") == nullptr) {
-    const size_t tsm = (size_t)kTinyM * st.dm.D * 8;
+    const size_t tsm = (size_t)(kTinyM + kTabWarps * 2) * st.dm.D * 8;
     if (tsm > 16 * 1024) {
       e = cudaFuncSetAttribute(km_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
       if (e != cudaSuccess) return e;

@@ -1740,6 +1740,10 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
       if (k[32 + 3])
         fprintf(stderr, "[kstats tiny] restarts/warp=%llu cyc_lloyd_phase=%llu refinements=%llu passes=%llu swapscans=%llu "
                 "cyc_refine_phase=%llu\n", k[32 + 3], k[32 + 5], k[32 + 8], k[32 + 7], k[32 + 9], k[32 + 11]);
+      if (k[32 + 21])
+        fprintf(stderr, "[kstats table] cyc_build=%llu restarts=%llu cyc_lloyd=%llu cyc_moves=%llu cyc_swaps=%llu "
+                "exact_movement=%llu exact_swaps=%llu\n", k[32 + 20], k[32 + 21], k[32 + 22], k[32 + 23], k[32 + 24],
+                k[32 + 25], k[32 + 26]);
       for (int c = 1; c < 5; ++c) {
         const unsigned long long* q = k + 32 + 32 * c;
         if (!q[3]) continue;
