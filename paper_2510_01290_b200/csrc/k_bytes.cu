@@ -17,9 +17,15 @@
 // slot mask, counts, code and value-scale bytes), pass 2 reads the window
 // index of live slots only (coalesced) and marks distinct live windows in a
 // shared-memory bitmap (one bit per window id).  Runs when byte accounting is
-// enabled (tkv_bytes_accounting), right after the attention launch of a step,
-// so every timed K1 launch is matched with its own exact byte count.  Counts
-// accumulate per unit (acc[u][5]); the host sums the rows when it reads them.
+// enabled (tkv_bytes_accounting), right after the attention launch of a step
+// whose pager state changed since the previous accounted launch (an emission,
+// an eviction, a layer-by-layer launch): the counts depend only on the block
+// table and the slot -> window map, which K1 does not modify, so a launch on
+// unchanged state reads exactly the bytes of the previous one.  The kernel
+// keeps each unit's latest counts (last[u][5]) and first credits the
+// `repeat` unchanged launches since it last ran; the host credits the tail
+// (last x pending) when it reads.  Counts accumulate per unit (acc[u][5]);
+// the host sums the rows when it reads them.
 #include <cuda_runtime.h>
 
 #include "tkv_kernels.h"
@@ -29,7 +35,8 @@ namespace {
 
 constexpr int kThreads = 128;
 
-__global__ void __launch_bounds__(kThreads) bytes_kernel(TkvState st, unsigned long long* acc) {
+__global__ void __launch_bounds__(kThreads) bytes_kernel(TkvState st, unsigned long long* acc,
+                                                         unsigned long long* last, long long repeat) {
   extern __shared__ uint32_t win_bits[];  // [2][nwords] E4M3-scaled | FP8 windows, then live slot masks [P]
   const TkvDims& dm = st.dm;
   const int u = tkv_unit_of(st, blockIdx.x);
@@ -106,13 +113,30 @@ __global__ void __launch_bounds__(kThreads) bytes_kernel(TkvState st, unsigned l
     unsigned long long t = 0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) t += red[w][threadIdx.x];
-    acc[(int64_t)u * 5 + threadIdx.x] += t;
+    const int64_t i = (int64_t)u * 5 + threadIdx.x;
+    acc[i] += last[i] * (unsigned long long)repeat + t;
+    last[i] = t;
   }
+}
+
+// acc += last * repeat for every unit (before a launch that covers a unit subset)
+__global__ void bytes_repeat_kernel(unsigned long long* acc, const unsigned long long* last, int64_t n,
+                                    long long repeat) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc[i] += last[i] * (unsigned long long)repeat;
 }
 
 }  // namespace
 
-cudaError_t tkv_launch_bytes(const TkvState& st, unsigned long long* acc, cudaStream_t stream) {
+cudaError_t tkv_launch_bytes_repeat(unsigned long long* acc, const unsigned long long* last, int64_t units,
+                                    long long repeat, cudaStream_t stream) {
+  if (repeat <= 0 || units <= 0) return cudaSuccess;
+  bytes_repeat_kernel<<<(int)((units * 5 + 255) / 256), 256, 0, stream>>>(acc, last, units * 5, repeat);
+  return cudaGetLastError();
+}
+
+cudaError_t tkv_launch_bytes(const TkvState& st, unsigned long long* acc, unsigned long long* last,
+                             long long repeat, cudaStream_t stream) {
   const int n = tkv_launch_units(st);
   if (n <= 0) return cudaSuccess;
   const size_t smem = (2 * (size_t)((st.dm.NW + 31) / 32) + st.dm.P) * sizeof(uint32_t) + st.dm.P;
@@ -120,6 +144,6 @@ cudaError_t tkv_launch_bytes(const TkvState& st, unsigned long long* acc, cudaSt
     cudaError_t e = cudaFuncSetAttribute(bytes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  bytes_kernel<<<n, kThreads, smem, stream>>>(st, acc);
+  bytes_kernel<<<n, kThreads, smem, stream>>>(st, acc, last, repeat);
   return cudaGetLastError();
 }

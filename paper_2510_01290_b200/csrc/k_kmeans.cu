@@ -327,7 +327,8 @@ struct RsSmem {
   double xs[MAXM];
   double x2[MAXM];    // |x_i|^2 (swap-filter error bound)
   double m2[MAXM];    // |mean_of(c)|^2 (swap-filter error bound)
-  int flag, move_i, move_to, pair, ncand;
+  int flag, move_i, move_to, pair;
+  int ncand[2];  // per swap window, alternating: a window's reset never races the previous window's reads
   int res[32];
   int cand[WIN];
   double cost;
@@ -955,8 +956,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 
     // in parallel, stop at the first window holding an improving pair.
     const int npairs = m * (m - 1) / 2;
     long long tfilt = 0;
-    for (int p0 = 0; p0 < npairs; p0 += RsSmem<MAXM>::WIN) {
-      if (threadIdx.x == 0) s.ncand = 0;
+    for (int p0 = 0, wi = 0; p0 < npairs; p0 += RsSmem<MAXM>::WIN, wi ^= 1) {
+      int& ncand = s.ncand[wi];
+      if (threadIdx.x == 0) ncand = 0;
       __syncthreads();
       const long long tf0 = clock64();
       for (int p = p0 + threadIdx.x; p < min(npairs, p0 + RsSmem<MAXM>::WIN); p += NT) {
@@ -980,16 +982,16 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 
         const double margin = 1e-12 * (dja + dia + dib + djb + w * pij + 16.0 * (s.x2[i] + s.x2[j]) +
                                        4.0 * (na * s.m2[a] + nb * s.m2[b])) + 1e-12;
         if (approx >= -1e-12 + margin) continue;
-        s.cand[atomicAdd(&s.ncand, 1)] = p;
+        s.cand[atomicAdd(&ncand, 1)] = p;
       }
       __syncthreads();
       tfilt += clock64() - tf0;
-      if (s.ncand == 0) continue;
-      kstm(st, m, 10, (unsigned long long)s.ncand);
+      if (ncand == 0) continue;
+      kstm(st, m, 10, (unsigned long long)ncand);
       // One warp per candidate: lanes evaluate the per-channel terms (the
       // divisions of different channels are independent), then the terms are
       // accumulated in the reference's channel order through shuffles.
-      for (int c = warp; c < s.ncand; c += NT / 32) {
+      for (int c = warp; c < ncand; c += NT / 32) {
         const int p = s.cand[c];
         const int i = pair_row(p, m), j = i + 1 + (p - i * (2 * m - i - 1) / 2);
         const int a = s.assign[i], b = s.assign[j];

@@ -208,8 +208,11 @@ struct tkv_run {
   int64_t launches = 0;
   // device byte accounting (tkv_bytes_accounting)
   bool bytes_on = false;
-  unsigned long long* d_bytes_acc = nullptr;  // [U][5] per-unit sums
+  unsigned long long* d_bytes_acc = nullptr;   // [U][5] per-unit sums
+  unsigned long long* d_bytes_last = nullptr;  // [U][5] counts of the latest accounted launch
   int64_t bytes_launches = 0, bytes_host = 0;  // accounted launches, host-known bytes (buffer, q, out)
+  bool bytes_dirty = true;     // pager state changed since the bytes kernel last ran
+  int64_t bytes_pending = 0;   // full-step launches on unchanged state since then
   // host-pointer step staging: two slots, copies on their own stream so the
   // transfers of one step overlap the kernels of its neighbours
   void* d_q[2] = {nullptr, nullptr};
@@ -365,6 +368,7 @@ void drain_timing(tkv_run* r) {
 template <typename F>
 void launch(tkv_run* r, int cat, const char* what, F&& fn) {
   r->launches += 1;
+  if (cat != CAT_ATTEND && cat != CAT_SCORE) r->bytes_dirty = true;  // block table / windows may change
   if (!r->timing) {
     check_launch(fn(), what);
     return;
@@ -1050,8 +1054,23 @@ void step_attend(tkv_run* r, const StepCtx& c, const void* q, const void* k, con
     return tkv_launch_attend(r->st, q, k, v, out, r->cur_half, r->buf_len, c.put_half, c.put_slot, r->stream);
   });
   if (r->bytes_on) {
-    r->launches += 1;
-    check_launch(tkv_launch_bytes(r->st, r->d_bytes_acc, r->stream), "bytes kernel");
+    // the device counts change only with the pager state (k_bytes.cu): a
+    // full-step launch on unchanged state repeats the previous counts
+    if (lmap_h == 0 && !r->bytes_dirty) {
+      r->bytes_pending += 1;
+    } else {
+      r->launches += 1;
+      if (lmap_h != 0 && r->bytes_pending > 0) {
+        r->launches += 1;
+        check_launch(tkv_launch_bytes_repeat(r->d_bytes_acc, r->d_bytes_last, r->st.dm.U, r->bytes_pending,
+                                             r->stream), "bytes repeat kernel");
+        r->bytes_pending = 0;
+      }
+      check_launch(tkv_launch_bytes(r->st, r->d_bytes_acc, r->d_bytes_last, r->bytes_pending, r->stream),
+                   "bytes kernel");
+      r->bytes_pending = 0;
+      r->bytes_dirty = lmap_h != 0;
+    }
     const TkvDims& dm = r->st.dm;
     const int64_t n = tkv_launch_units(r->st);
     const int rows = dm.maxpool ? 1 : dm.G;
@@ -1214,6 +1233,7 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   if (getenv("TKV_KSTATS")) st.kstats = dalloc<unsigned long long>(r, 256, 0);
   st.err = dalloc<int32_t>(r, U);
   r->d_bytes_acc = dalloc<unsigned long long>(r, U * 5, 0);
+  r->d_bytes_last = dalloc<unsigned long long>(r, U * 5, 0);
   check_launch(tkv_launch_init(st, r->stream), "init kernel");
   // arenas
   r->arena_cap = 8 << 20;
@@ -1621,9 +1641,12 @@ int tkv_bytes_accounting(tkv_run* run, int enable) {
   try {
     if (!run) throw TkvError(TKV_ERR_CONFIG, "null run");
     CUDA_OK(cudaMemsetAsync(run->d_bytes_acc, 0, (size_t)run->st.dm.U * 5 * sizeof(unsigned long long), run->stream));
+    CUDA_OK(cudaMemsetAsync(run->d_bytes_last, 0, (size_t)run->st.dm.U * 5 * sizeof(unsigned long long), run->stream));
     run->bytes_launches = 0;
     run->bytes_host = 0;
     run->bytes_on = enable != 0;
+    run->bytes_dirty = true;
+    run->bytes_pending = 0;
     return 0;
   } catch (const TkvError& e) {
     return fail(e);
@@ -1635,12 +1658,16 @@ int tkv_bytes_accounting(tkv_run* run, int enable) {
 int tkv_bytes_accumulated(tkv_run* run, tkv_bytes_t* sum, int64_t* launches) {
   try {
     if (!run || !sum) throw TkvError(TKV_ERR_CONFIG, "null argument");
-    std::vector<unsigned long long> per_unit((size_t)run->st.dm.U * 5);
+    std::vector<unsigned long long> per_unit((size_t)run->st.dm.U * 5), last(per_unit.size());
     CUDA_OK(cudaMemcpyAsync(per_unit.data(), run->d_bytes_acc, per_unit.size() * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, run->stream));
+    CUDA_OK(cudaMemcpyAsync(last.data(), run->d_bytes_last, last.size() * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, run->stream));
     CUDA_OK(cudaStreamSynchronize(run->stream));
     unsigned long long acc[5] = {0, 0, 0, 0, 0};
-    for (size_t i = 0; i < per_unit.size(); ++i) acc[i % 5] += per_unit[i];
+    // + the launches on unchanged state since the bytes kernel last ran
+    const unsigned long long rep = (unsigned long long)run->bytes_pending;
+    for (size_t i = 0; i < per_unit.size(); ++i) acc[i % 5] += per_unit[i] + last[i] * rep;
     std::memset(sum, 0, sizeof(*sum));
     sum->live_slots = (int64_t)acc[0];
     sum->resident_slots = (int64_t)acc[1];

@@ -20,7 +20,10 @@ cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void*
 // Algorithmic-byte accounting of the state an attention launch reads
 // (k_bytes.cu): adds live slots, resident slots, live code bytes, live scale
 // bytes and metadata bytes of every launched unit to acc[0..5).
-cudaError_t tkv_launch_bytes(const TkvState& st, unsigned long long* acc, cudaStream_t stream);
+cudaError_t tkv_launch_bytes(const TkvState& st, unsigned long long* acc, unsigned long long* last,
+                             long long repeat, cudaStream_t stream);
+cudaError_t tkv_launch_bytes_repeat(unsigned long long* acc, const unsigned long long* last, int64_t units,
+                                    long long repeat, cudaStream_t stream);
 
 // y[i] = tkv_exp(x[i]) (k_math.cu): glibc's exp, bit for bit.
 cudaError_t tkv_launch_exp(const double* x, double* y, int64_t n, cudaStream_t stream);

@@ -105,3 +105,42 @@ def test_device_byte_accounting_matches_host_walk():
             assert n == 1 and got == want, f"step {t}: {got} != {want}"
             checked += 1
     assert checked > 20
+
+
+def test_device_byte_accounting_over_a_long_window():
+    """One accounting window over many steps (emissions, boundaries and
+    evictions inside it, runs of launches on unchanged pager state that reuse
+    the previous counts, k_bytes.cu) == the sum of the host walk before every
+    step; full steps and layer-by-layer launches mixed."""
+    cfg = ThinkvConfig(num_seqs=2, units_per_seq=4, num_q_heads=4, head_dim=128, tau=32, group_size=16,
+                       block_size=16, budget=64, levels=(16, 8, 4), psi_bits=(4, 8, 2), max_gen_len=260,
+                       script=band_script(SEED, 2, 12, 3, 300))
+    run = DecodeRun(cfg)
+    dev = torch.device("cuda:0")
+    L, H = 2, 2  # units_per_seq = layers x kv-heads
+    out = torch.empty((cfg.units, 4, 128), device=dev)
+    lout = torch.empty((cfg.num_seqs * H, 4, 128), device=dev)
+    start = 70
+    for t in range(start):
+        q, k, v = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev)
+                   for x in synth_inputs(cfg, SEED, t))
+        run.step(q, k, v, out)
+    want = None
+    run.bytes_accounting(True)
+    for t in range(start, cfg.max_gen_len):
+        q, k, v = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev)
+                   for x in synth_inputs(cfg, SEED, t))
+        b = run.bytes()
+        want = b if want is None else {f: want[f] + b[f] for f in want}
+        if 150 <= t < 170:  # layer by layer: units [seq][layer][head]
+            qv, kv, vv = (x.view(cfg.num_seqs, L, H, *x.shape[1:]) for x in (q, k, v))
+            for layer in range(L):
+                run.step_layer(layer, L, qv[:, layer].contiguous().view(-1, *q.shape[1:]),
+                               kv[:, layer].contiguous().view(-1, *k.shape[1:]),
+                               vv[:, layer].contiguous().view(-1, *v.shape[1:]), lout)
+        else:
+            run.step(q, k, v, out)
+    got, n = run.bytes_accumulated()
+    run.bytes_accounting(False)
+    assert n == cfg.max_gen_len - start
+    assert got == want
