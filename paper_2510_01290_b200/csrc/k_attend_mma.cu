@@ -676,99 +676,327 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st,
 
 
 // ===========================================================================
-// v3: one warp per unit.  No block-level barriers: the warp builds its own
+// v4: one warp per unit.  No block-level barriers: the warp builds its own
 // live list (u16 slot ids; tail rows are NS + t), walks every tile of its
 // unit, and writes the normalised output itself.  Window indices are not in
 // the list: they are fetched two tiles ahead (slot -> window), so the scale
 // loads of tile t+1 are issued while tile t computes.
+//
+// Instruction economy per 16-token tile (the kernel is issue bound):
+//   * addresses: per-thread, per-format base pointers are formed once per
+//     list; a slot row is one mad.wide.u32 (IMAD.WIDE.U32) of the u16 slot id
+//     and the 32-bit stride -- no 64-bit index arithmetic per load;
+//   * softmax: the running max moves only when some logit exceeds it by more
+//     than 2^8 (lazy rescale), decided by one vote per tile; the max and the
+//     denominator are reduced across lanes only on that rare path and once at
+//     the end (each lane keeps partial denominators of its own tokens);
+//   * PV with R <= 4 output rows: the hi and lo halves of P ride in the
+//     MMA's N dimension (columns h = hi, 4 + h = lo), one mma per m-tile
+//     instead of two; the halves are added once in the epilogue.
 // ===========================================================================
+__device__ __forceinline__ const uint8_t* wide_at(const void* base, uint32_t i, uint32_t stride) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(i), "r"(stride), "l"(reinterpret_cast<uint64_t>(base)));
+  return reinterpret_cast<const uint8_t*>(r);
+}
+
+// Per-thread base pointers of one format's tiles (loop invariant).
 template <int D, int FMT>
-__device__ __forceinline__ void load_wins3(const UnitPtrs& up, const uint16_t* lst, int t0, int gid, int tig,
-                                           int (&wk)[2], int (&wv)[4]) {
+struct Bases {
+  const uint8_t* k;   // slot_k + tig * KBYTES
+  const uint8_t* v;   // slot_v + gid * VBYTES
+  const uint8_t* vs;  // slot_vs + vsel
+  const uint8_t* ks;  // win_ks + tig * CPT
+  __device__ Bases(const UnitPtrs& up, int gid, int tig) {
+    using Gm = Geo<D, FMT>;
+    k = up.k + tig * Gm::KBYTES;
+    v = up.v + gid * Gm::VBYTES;
+    vs = up.vs + up.vsel;
+    ks = up.ks + tig * Gm::CPT;
+  }
+};
+
+template <int D, int FMT>
+__device__ __forceinline__ void load_wins4(const UnitPtrs& up, const uint16_t* lst, int t0, int gid, int tig,
+                                           uint32_t (&wk)[2], uint32_t (&wv)[4]) {
   if constexpr (Geo<D, FMT>::SCALED || FMT == TKV_FMT_FP8) {
 #pragma unroll
-    for (int r = 0; r < 2; ++r) wk[r] = __ldg(up.win + lst[t0 + gid + 8 * r]);  // live quantised slots: >= 0
+    for (int r = 0; r < 2; ++r)  // live quantised slots: >= 0
+      wk[r] = (uint32_t)__ldg(reinterpret_cast<const int32_t*>(wide_at(up.win, lst[t0 + gid + 8 * r], 4)));
   }
   if constexpr (FMT == TKV_FMT_FP8) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) wv[i] = __ldg(up.win + lst[t0 + tig * 2 + (i & 1) + 8 * (i >> 1)]);
+    for (int i = 0; i < 4; ++i)
+      wv[i] = (uint32_t)__ldg(
+          reinterpret_cast<const int32_t*>(wide_at(up.win, lst[t0 + tig * 2 + (i & 1) + 8 * (i >> 1)], 4)));
   }
 }
 
 template <int D, int FMT>
-__device__ __forceinline__ void load_tile3(const UnitPtrs& up, const uint16_t* lst, int t0, int gid, int tig,
-                                           const int (&wk)[2], const int (&wv)[4], Tile<D, FMT>& T) {
+__device__ __forceinline__ void load_tile4(const UnitPtrs& up, const Bases<D, FMT>& B, const uint16_t* lst, int t0,
+                                           int gid, int tig, const uint32_t (&wk)[2], const uint32_t (&wv)[4],
+                                           Tile<D, FMT>& T) {
   using Gm = Geo<D, FMT>;
+  const uint32_t ks = (uint32_t)up.kstride;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int e = lst[t0 + gid + 8 * r];
+    const uint32_t e = lst[t0 + gid + 8 * r];
     const uint8_t* kr;
     if constexpr (FMT == kFmtTail) {
-      if (e < up.NS) kr = up.k + e * up.kstride;
-      else kr = e - up.NS < up.nbuf ? up.bk + (e - up.NS) * (D * 2) : up.kc;
+      if (e < (uint32_t)up.NS) kr = wide_at(B.k, e, ks);
+      else kr = (int)e - up.NS < up.nbuf ? up.bk + ((int)e - up.NS) * (D * 2) + tig * Gm::KBYTES
+                                         : up.kc + tig * Gm::KBYTES;
     } else {
-      kr = up.k + e * up.kstride;
+      kr = wide_at(B.k, e, ks);
     }
-    T.k[r] = ldg_words<Gm::KW>(kr + tig * Gm::KBYTES);
-    if constexpr (FMT == TKV_FMT_FP8) T.kf[r] = __ldg(up.kf + wk[r]);
-    if constexpr (Gm::SCALED) T.ks[r] = ldg_words<Gm::SW>(up.ks + wk[r] * D + tig * Gm::CPT);
+    T.k[r] = ldg_words<Gm::KW>(kr);
+    if constexpr (FMT == TKV_FMT_FP8) T.kf[r] = __ldg(reinterpret_cast<const float*>(wide_at(up.kf, wk[r], 4)));
+    if constexpr (Gm::SCALED) T.ks[r] = ldg_words<Gm::SW>(wide_at(B.ks, wk[r], D));
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int e = lst[t0 + tig * 2 + (i & 1) + 8 * (i >> 1)];
+    const uint32_t e = lst[t0 + tig * 2 + (i & 1) + 8 * (i >> 1)];
     const uint8_t* vr;
     if constexpr (FMT == kFmtTail) {
-      if (e < up.NS) vr = up.v + e * up.kstride;
-      else vr = e - up.NS < up.nbuf ? up.bv + (e - up.NS) * (D * 2) : up.vc;
+      if (e < (uint32_t)up.NS) vr = wide_at(B.v, e, ks);
+      else vr = (int)e - up.NS < up.nbuf ? up.bv + ((int)e - up.NS) * (D * 2) + gid * Gm::VBYTES
+                                         : up.vc + gid * Gm::VBYTES;
     } else {
-      vr = up.v + e * up.kstride;
+      vr = wide_at(B.v, e, ks);
     }
-    vr += gid * Gm::VBYTES;
     if constexpr (Gm::VBYTES >= 4) {
       T.v[i] = ldg_words<Gm::VW>(vr);
     } else {
       T.v[i].w[0] = Gm::VBYTES == 2 ? (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(vr)) : (uint32_t)__ldg(vr);
     }
-    if constexpr (FMT == TKV_FMT_FP8) T.vf[i] = __ldg(up.vf + wv[i]);
-    if constexpr (Gm::SCALED) T.vs[i] = __ldg(up.vs + e * up.vchunks + up.vsel);
+    if constexpr (FMT == TKV_FMT_FP8) T.vf[i] = __ldg(reinterpret_cast<const float*>(wide_at(up.vf, wv[i], 4)));
+    if constexpr (Gm::SCALED) T.vs[i] = __ldg(wide_at(B.vs, e, (uint32_t)up.vchunks));
   }
 }
 
-template <int D, int FMT>
-__device__ __forceinline__ void run_format3(const UnitPtrs& up, const uint16_t* lst, int n,
+template <int D, int FMT, bool PVN>
+__device__ __forceinline__ void compute_tile4(const Tile<D, FMT>& T, const uint32_t (&qb)[D / 16][2],
+                                              const uint32_t* qbb, float qscale, bool maxpool, int nvalid,
+                                              int gid, int tig, float* ps, Acc<D>& A) {
+  using Gm = Geo<D, FMT>;
+  // ---- S = K q^T ----------------------------------------------------------
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  if constexpr (FMT == TKV_FMT_TERNARY) {
+    // 8 codes per 16-bit half -> 8 e2m1 nibbles (one word), 4 k-steps per code word
+#pragma unroll
+    for (int jw = 0; jw < Gm::KW; ++jw) {
+      uint32_t nib[2][2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        nib[r][0] = tern_spread(T.k[r].w[jw]);
+        nib[r][1] = tern_spread(T.k[r].w[jw] >> 16);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = jw * 4 + jj;
+        uint32_t a[4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          uint32_t lo, hi, slo, shi;
+          e2m1x2_b(nib[r][jj >> 1], (jj & 1) * 2, lo);
+          e2m1x2_b(nib[r][jj >> 1], (jj & 1) * 2 + 1, hi);
+          e4m3x4(T.ks[r].w[j], slo, shi);
+          a[r] = hmul2(lo, slo);
+          a[2 + r] = hmul2(hi, shi);
+        }
+        mma16816<false>(s, a[0], a[1], a[2], a[3], qb[j][0], qb[j][1]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < Gm::KT; ++j) {
+      uint32_t a[4];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        uint32_t lo, hi;
+        if constexpr (FMT == TKV_FMT_NVFP4) {
+          e2m1x2_b(T.k[r].w[j >> 1], (j & 1) * 2, lo);
+          e2m1x2_b(T.k[r].w[j >> 1], (j & 1) * 2 + 1, hi);
+          uint32_t slo, shi;
+          e4m3x4(T.ks[r].w[j], slo, shi);
+          lo = hmul2(lo, slo);
+          hi = hmul2(hi, shi);
+        } else if constexpr (FMT == TKV_FMT_FP8) {
+          e4m3x4(T.k[r].w[j], lo, hi);
+        } else {  // raw bf16 words: channels 4j, 4j+1 | 4j+2, 4j+3
+          lo = T.k[r].w[2 * j];
+          hi = T.k[r].w[2 * j + 1];
+        }
+        a[r] = lo;
+        a[2 + r] = hi;
+      }
+      if constexpr (Gm::BF16) mma16816<true>(s, a[0], a[1], a[2], a[3], qbb[j * 2], qbb[j * 2 + 1]);
+      else mma16816<false>(s, a[0], a[1], a[2], a[3], qb[j][0], qb[j][1]);
+    }
+  }
+  // logits (log2 domain); rows: s0,s1 -> token gid, s2,s3 -> token gid+8.
+  // Heads >= G have q = 0: their logits are 0, finite, and never written out.
+  float L[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float x = s[i] * qscale;
+    if constexpr (FMT == TKV_FMT_FP8) x *= T.kf[i >> 1];
+    L[i] = x;
+  }
+  if (nvalid < 16) {  // the list's last tile: padding rows -> -inf (warp-uniform)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (gid + 8 * (i >> 1) >= nvalid) L[i] = -CUDART_INF_F;
+  }
+  if (maxpool) {
+    // one pooled row per token: max over the G heads, kept in column 0
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      float mx = fmaxf(L[2 * r], L[2 * r + 1]);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      L[2 * r] = (PVN ? (tig & 1) == 0 : tig == 0) ? mx : -CUDART_INF_F;  // PVN: column 4 mirrors 0
+      L[2 * r + 1] = -CUDART_INF_F;
+    }
+  }
+  // ---- online softmax per head column, lazy rescale --------------------------
+  const bool grow = L[0] > A.m[0] + kRescale || L[2] > A.m[0] + kRescale || L[1] > A.m[1] + kRescale ||
+                    L[3] > A.m[1] + kRescale;
+  if (__any_sync(0xffffffffu, grow)) {  // rare: a new reference max for some column
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float tmax = fmaxf(L[c], L[2 + c]);
+      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+      if (tmax > A.m[c] + kRescale) {
+        const float corr = A.m[c] == -CUDART_INF_F ? 0.0f : exp2f(A.m[c] - tmax);
+        A.l[c] *= corr;
+#pragma unroll
+        for (int mt = 0; mt < Gm::MT; ++mt) {  // (PVN: lo columns mirror their head's max, same corr)
+          A.o[mt][c] *= corr;
+          A.o[mt][2 + c] *= corr;
+        }
+        A.m[c] = tmax;
+      }
+    }
+  }
+  float p[4];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    // columns that never saw a finite logit (max-pool's unused columns) stay 0
+    const bool live = A.m[c] != -CUDART_INF_F;
+    p[c] = live ? exp2f(L[c] - A.m[c]) : 0.0f;
+    p[2 + c] = live ? exp2f(L[2 + c] - A.m[c]) : 0.0f;
+    A.l[c] += p[c] + p[2 + c];  // this lane's tokens only; reduced across lanes at the end
+  }
+  // ---- P: C layout (token, head) -> B layout (token = k, head = n) -----------
+  ps[gid * 8 + tig * 2] = p[0];
+  ps[gid * 8 + tig * 2 + 1] = p[1];
+  ps[(gid + 8) * 8 + tig * 2] = p[2];
+  ps[(gid + 8) * 8 + tig * 2 + 1] = p[3];
+  __syncwarp();
+  float pb[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    pb[i] = ps[(tig * 2 + (i & 1) + 8 * (i >> 1)) * 8 + (PVN ? (gid & 3) : gid)];
+    if constexpr (FMT == TKV_FMT_FP8) pb[i] *= T.vf[i];
+  }
+  __syncwarp();
+  uint32_t bh0, bh1, bl0, bl1;
+  if constexpr (Gm::BF16) {
+    bh0 = pack_bf16x2(pb[0], pb[1]);
+    bh1 = pack_bf16x2(pb[2], pb[3]);
+    bl0 = pack_bf16x2(pb[0] - bf16lo(bh0), pb[1] - bf16hi(bh0));
+    bl1 = pack_bf16x2(pb[2] - bf16lo(bh1), pb[3] - bf16hi(bh1));
+  } else {
+    bh0 = pack_f16x2(pb[0], pb[1]);
+    bh1 = pack_f16x2(pb[2], pb[3]);
+    bl0 = pack_f16x2(pb[0] - f16lo(bh0), pb[1] - f16hi(bh0));
+    bl1 = pack_f16x2(pb[2] - f16lo(bh1), pb[3] - f16hi(bh1));
+  }
+  if constexpr (PVN) {  // columns 0..3: hi halves of heads 0..3, columns 4..7: lo halves
+    if (gid >= 4) { bh0 = bl0; bh1 = bl1; }
+  }
+  // ---- O^T += V^T P ----------------------------------------------------------
+  uint32_t vsc[4];
+  if constexpr (Gm::SCALED) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) e4m3x2_b(T.vs[i], 0, vsc[i]);
+  }
+  uint32_t tsp[4][(Gm::MT + 3) / 4];  // ternary: e2m1 nibbles of each 8-code half-word
+  if constexpr (FMT == TKV_FMT_TERNARY) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int h = 0; h < (Gm::MT + 3) / 4; ++h) tsp[i][h] = tern_spread(T.v[i].w[0] >> (16 * h));
+  }
+#pragma unroll
+  for (int mt = 0; mt < Gm::MT; ++mt) {
+    uint32_t x[4];  // per PV token: f16x2 / bf16x2 of channels (2mt, 2mt+1) of the thread's range
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if constexpr (FMT == TKV_FMT_NVFP4) {
+        uint32_t h;
+        e2m1x2_b(T.v[i].w[mt >> 2], mt & 3, h);
+        x[i] = hmul2(h, vsc[i]);
+      } else if constexpr (FMT == TKV_FMT_FP8) {
+        uint32_t lo, hi;
+        e4m3x4(T.v[i].w[mt >> 1], lo, hi);
+        x[i] = (mt & 1) ? hi : lo;
+      } else if constexpr (FMT == TKV_FMT_TERNARY) {
+        uint32_t h;
+        e2m1x2_b(tsp[i][mt >> 2], mt & 3, h);
+        x[i] = hmul2(h, vsc[i]);
+      } else {
+        x[i] = T.v[i].w[mt];
+      }
+    }
+    const uint32_t a0 = __byte_perm(x[0], x[1], 0x5410);  // row gid (ch 2mt), tokens tig*2, tig*2+1
+    const uint32_t a1 = __byte_perm(x[0], x[1], 0x7632);  // row gid+8 (ch 2mt+1)
+    const uint32_t a2 = __byte_perm(x[2], x[3], 0x5410);  // row gid, tokens +8, +9
+    const uint32_t a3 = __byte_perm(x[2], x[3], 0x7632);
+    mma16816<Gm::BF16>(A.o[mt], a0, a1, a2, a3, bh0, bh1);
+    if constexpr (!PVN) mma16816<Gm::BF16>(A.o[mt], a0, a1, a2, a3, bl0, bl1);
+  }
+}
+
+template <int D, int FMT, bool PVN>
+__device__ __forceinline__ void run_format4(const UnitPtrs& up, const uint16_t* lst, int n,
                                             const uint32_t (&qb)[D / 16][2], const uint32_t* qbb, float qscale,
-                                            int G, bool maxpool, int gid, int tig, float* ps, Acc<D>& A) {
+                                            bool maxpool, int gid, int tig, float* ps, Acc<D>& A) {
   const int tiles = (n + 15) / 16;
   if (tiles == 0) return;
+  const Bases<D, FMT> B(up, gid, tig);
   if constexpr (FMT == kFmtTail) {  // few tiles, wide rows: no double buffering (registers)
-    int wk[2] = {0, 0}, wv[4] = {0, 0, 0, 0};
+    uint32_t wk[2] = {0, 0}, wv[4] = {0, 0, 0, 0};
     for (int t = 0; t < tiles; ++t) {
       Tile<D, FMT> cur;
-      load_tile3<D, FMT>(up, lst, t * 16, gid, tig, wk, wv, cur);
-      compute_tile<D, FMT>(cur, qb, qbb, qscale, G, maxpool, n - t * 16, gid, tig, ps, A);
+      load_tile4<D, FMT>(up, B, lst, t * 16, gid, tig, wk, wv, cur);
+      compute_tile4<D, FMT, PVN>(cur, qb, qbb, qscale, maxpool, n - t * 16, gid, tig, ps, A);
     }
     return;
   }
-  int wk0[2] = {0, 0}, wv0[4] = {0, 0, 0, 0}, wk1[2] = {0, 0}, wv1[4] = {0, 0, 0, 0};
+  uint32_t wk0[2] = {0, 0}, wv0[4] = {0, 0, 0, 0}, wk1[2] = {0, 0}, wv1[4] = {0, 0, 0, 0};
   Tile<D, FMT> ta, tb;
-  load_wins3<D, FMT>(up, lst, 0, gid, tig, wk0, wv0);
-  load_tile3<D, FMT>(up, lst, 0, gid, tig, wk0, wv0, ta);
-  if (tiles > 1) load_wins3<D, FMT>(up, lst, 16, gid, tig, wk1, wv1);
+  load_wins4<D, FMT>(up, lst, 0, gid, tig, wk0, wv0);
+  load_tile4<D, FMT>(up, B, lst, 0, gid, tig, wk0, wv0, ta);
+  if (tiles > 1) load_wins4<D, FMT>(up, lst, 16, gid, tig, wk1, wv1);
   int t = 0;
   while (true) {
     // ta holds tile t; wk1 the windows of tile t + 1
     if (t + 1 < tiles) {
-      load_tile3<D, FMT>(up, lst, (t + 1) * 16, gid, tig, wk1, wv1, tb);
-      if (t + 2 < tiles) load_wins3<D, FMT>(up, lst, (t + 2) * 16, gid, tig, wk0, wv0);
+      load_tile4<D, FMT>(up, B, lst, (t + 1) * 16, gid, tig, wk1, wv1, tb);
+      if (t + 2 < tiles) load_wins4<D, FMT>(up, lst, (t + 2) * 16, gid, tig, wk0, wv0);
     }
-    compute_tile<D, FMT>(ta, qb, qbb, qscale, G, maxpool, n - t * 16, gid, tig, ps, A);
+    compute_tile4<D, FMT, PVN>(ta, qb, qbb, qscale, maxpool, n - t * 16, gid, tig, ps, A);
     if (++t >= tiles) break;
     // tb holds tile t; wk0 the windows of tile t + 1
     if (t + 1 < tiles) {
-      load_tile3<D, FMT>(up, lst, (t + 1) * 16, gid, tig, wk0, wv0, ta);
-      if (t + 2 < tiles) load_wins3<D, FMT>(up, lst, (t + 2) * 16, gid, tig, wk1, wv1);
+      load_tile4<D, FMT>(up, B, lst, (t + 1) * 16, gid, tig, wk0, wv0, ta);
+      if (t + 2 < tiles) load_wins4<D, FMT>(up, lst, (t + 2) * 16, gid, tig, wk1, wv1);
     }
-    compute_tile<D, FMT>(tb, qb, qbb, qscale, G, maxpool, n - t * 16, gid, tig, ps, A);
+    compute_tile4<D, FMT, PVN>(tb, qb, qbb, qscale, maxpool, n - t * 16, gid, tig, ps, A);
     if (++t >= tiles) break;
   }
 }
@@ -783,7 +1011,11 @@ struct WarpSmem {
   }
 };
 
-template <int D, int MINB>
+// PVN: at most 4 output rows per unit (max-pool, or G <= 4): P's hi/lo halves
+// share one PV mma (compute_tile4).  Without max-pool the q^T operand's
+// columns 4..7 repeat heads 0..3, so the lanes holding the lo columns see their
+// head's own logits and track the same running max and denominator.
+template <int D, int MINB, bool PVN>
 __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st, const void* __restrict__ qin,
                                                                     const void* __restrict__ kin,
                                                                     const void* __restrict__ vin,
@@ -807,11 +1039,12 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
 
   uint32_t qb[D / 16][2];
   {
-    const uint16_t* qq = reinterpret_cast<const uint16_t*>(qin) + ((int64_t)li * G + gid) * D + tig * (D / 4);
+    const int hq = PVN && !dm.maxpool ? (gid & 3) : gid;  // q^T column gid holds head hq
+    const uint16_t* qq = reinterpret_cast<const uint16_t*>(qin) + ((int64_t)li * G + hq) * D + tig * (D / 4);
 #pragma unroll
     for (int j = 0; j < D / 16; ++j) {
       uint2 w = make_uint2(0u, 0u);
-      if (gid < G) w = *reinterpret_cast<const uint2*>(qq + 4 * j);
+      if (hq < G) w = *reinterpret_cast<const uint2*>(qq + 4 * j);
       qbb[2 * j] = w.x;
       qbb[2 * j + 1] = w.y;
       qb[j][0] = pack_f16x2(bf16lo(w.x), bf16hi(w.x));
@@ -910,18 +1143,33 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
   A.m[0] = A.m[1] = -CUDART_INF_F;
   A.l[0] = A.l[1] = 0.f;
   const bool mp = dm.maxpool != 0;
-  run_format3<D, TKV_FMT_NVFP4>(up, list + off[TKV_FMT_NVFP4], cnt[TKV_FMT_NVFP4], qb, qbb, qscale, G, mp, gid, tig,
-                                ps, A);
-  run_format3<D, TKV_FMT_TERNARY>(up, list + off[TKV_FMT_TERNARY], cnt[TKV_FMT_TERNARY], qb, qbb, qscale, G, mp, gid,
-                                  tig, ps, A);
-  run_format3<D, TKV_FMT_FP8>(up, list + off[TKV_FMT_FP8], cnt[TKV_FMT_FP8], qb, qbb, qscale, G, mp, gid, tig, ps,
-                              A);
-  run_format3<D, kFmtTail>(up, list + off[TKV_FMT_RAW], cnt[TKV_FMT_RAW], qb, qbb, qscale, G, mp, gid, tig, ps, A);
+  run_format4<D, TKV_FMT_NVFP4, PVN>(up, list + off[TKV_FMT_NVFP4], cnt[TKV_FMT_NVFP4], qb, qbb, qscale, mp, gid, tig,
+                                     ps, A);
+  run_format4<D, TKV_FMT_TERNARY, PVN>(up, list + off[TKV_FMT_TERNARY], cnt[TKV_FMT_TERNARY], qb, qbb, qscale, mp,
+                                       gid, tig, ps, A);
+  run_format4<D, TKV_FMT_FP8, PVN>(up, list + off[TKV_FMT_FP8], cnt[TKV_FMT_FP8], qb, qbb, qscale, mp, gid, tig, ps,
+                                   A);
+  run_format4<D, kFmtTail, PVN>(up, list + off[TKV_FMT_RAW], cnt[TKV_FMT_RAW], qb, qbb, qscale, mp, gid, tig, ps, A);
   // ---- epilogue: heads tig*2 + cc, channels gid*D/8 + 2mt (+1) ------------------
+  // denominators: each lane summed its own tokens; reduce over the 8 token lanes
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    float l = A.l[cc];
+    l += __shfl_xor_sync(0xffffffffu, l, 4);
+    l += __shfl_xor_sync(0xffffffffu, l, 8);
+    l += __shfl_xor_sync(0xffffffffu, l, 16);
+    A.l[cc] = l;
+  }
+  if constexpr (PVN) {  // head h = hi column h + lo column 4 + h (lane tig + 2)
+#pragma unroll
+    for (int mt = 0; mt < D / 16; ++mt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) A.o[mt][i] += __shfl_xor_sync(0xffffffffu, A.o[mt][i], 2);
+  }
 #pragma unroll
   for (int cc = 0; cc < 2; ++cc) {
     const int h = tig * 2 + cc;
-    if (h >= R) continue;
+    if (h >= R || (PVN && tig >= 2)) continue;
     const float inv = 1.0f / A.l[cc];
     float* o = out + ((int64_t)li * R + h) * D + gid * (D / 8);
 #pragma unroll
@@ -962,17 +1210,17 @@ cudaError_t launch_k1(const TkvState& st, const void* q, const void* k, const vo
   return cudaGetLastError();
 }
 
-template <int D, int MINB>
+template <int D, int MINB, bool PVN>
 cudaError_t launch_k1_warp(const TkvState& st, const void* q, const void* k, const void* v, float* out, int buf_half,
                            int nbuf, int put_half, int put_slot, cudaStream_t s) {
   const size_t smem = (size_t)kWarps * WarpSmem<D>::bytes(st.max_live, st.dm.g, st.dm.P);
   static bool cfg = false;
   if (!cfg) {
-    cudaFuncSetAttribute(attend_warp_kernel<D, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(attend_warp_kernel<D, MINB, PVN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cfg = true;
   }
-  attend_warp_kernel<D, MINB><<<(tkv_launch_units(st) + kWarps - 1) / kWarps, kThreads, smem, s>>>(st, q, k, v, out, buf_half,
-                                                                                     nbuf, put_half, put_slot);
+  attend_warp_kernel<D, MINB, PVN><<<(tkv_launch_units(st) + kWarps - 1) / kWarps, kThreads, smem, s>>>(
+      st, q, k, v, out, buf_half, nbuf, put_half, put_slot);
   return cudaGetLastError();
 }
 
@@ -986,8 +1234,13 @@ cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void*
                                              : WarpSmem<64>::bytes(st.max_live, st.dm.g, st.dm.P)) <= 200 * 1024 &&
                   getenv("TKV_K1_V2") == nullptr;
   if (v3) {
-    if (D == 128) return launch_k1_warp<128, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
-    return launch_k1_warp<64, 3>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+    const bool pvn = st.dm.maxpool || st.dm.G <= 4;
+    if (D == 128) {
+      if (pvn) return launch_k1_warp<128, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+      return launch_k1_warp<128, 3, false>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+    }
+    if (pvn) return launch_k1_warp<64, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+    return launch_k1_warp<64, 3, false>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
   }
   const size_t smem = (size_t)kWarps * 8 * (2 + D) * 4 + (size_t)kWarps * 128 * 4 + (size_t)32 * (D / 8) * 4 +
                       (size_t)(st.dm.NS + st.dm.g + 1 + 4 * 16) * 8 + (size_t)st.dm.P * 8;

@@ -234,9 +234,18 @@ def test_parity_cta_per_unit_attention_variant(monkeypatch):
 
 
 def test_parity_generic_kmeans_for_tiny_instances(monkeypatch):
-    """Instances with m <= 8 normally run the warp-per-restart kernel; the
-    generic restart kernel must give the same (reference) decisions."""
+    """Instances with m <= 8 normally run the subset-table kernel; the generic
+    restart kernel must give the same (reference) decisions."""
     monkeypatch.setenv("TKV_KM_NO_TINY", "1")
+    cfg = CONFIGS["llama_shape"]
+    res = run_parity(cfg, check_every=5)
+    compare_state(res, cfg)
+
+
+def test_parity_warp_per_restart_kmeans_for_tiny_instances(monkeypatch):
+    """TKV_KM_NO_TABLE: the warp-per-restart m <= 8 kernel (km_tiny) instead
+    of the subset-table kernel."""
+    monkeypatch.setenv("TKV_KM_NO_TABLE", "1")
     cfg = CONFIGS["llama_shape"]
     res = run_parity(cfg, check_every=5)
     compare_state(res, cfg)
