@@ -746,6 +746,21 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 
     const long long tl2 = clock64();
     kstm(st, m, 17, (unsigned long long)(tl2 - tl1));
     if constexpr (MAXM > 32) {  // sums rows in global memory: no read-back chains
+    // A cluster whose member set equals the previous iteration's has the same
+    // sum (same members, same order) and so the same mean, bit for bit: its
+    // next centroid is its current one, movement exactly 0 -- skipped.
+    // Changed clusters are flagged in s.ccols (free outside fill_sel); the
+    // previous assignment is kept in s.seeds (dead after the first fill).
+    for (int c = threadIdx.x; c < K; c += NT) s.ccols[c] = iter == 0;
+    __syncthreads();
+    if (iter > 0)
+      for (int i = threadIdx.x; i < m; i += NT)
+        if (s.assign[i] != s.seeds[i]) {
+          s.ccols[s.assign[i]] = 1;
+          s.ccols[s.seeds[i]] = 1;
+        }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += NT) s.seeds[i] = s.assign[i];
     // next centroids (member sums in point order / size, evictor.cpp:143-152)
     // written in place, and the movement terms (next - old)^2 (evictor.cpp:
     // 153-156) summed per column in any order: only "d == 0" (exact for a sum
@@ -756,7 +771,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 
       const bool valid = idx < K * D;
       const int c = valid ? rs.row(idx) : -1, ch = valid ? rs.col(idx) : 0;
       double t2 = 0.0;
-      if (valid) {
+      if (valid && s.ccols[c]) {
         double acc = 0.0;
         for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
         const double nx = div_n(acc, s.sizes[c]);
