@@ -477,6 +477,11 @@ def main():
                    "boundary_step_ms": sum(bnd) / len(bnd) if bnd else None,
                    "between_boundary_step_ms": sum(oth) / len(oth) if oth else None},
         "gpu_launches": tm["total_launches"],
+        "host": {"ms_per_step": tm["host_ms"] / max(1, tm["steps"]),
+                 "wait_ms_per_step": tm["host_wait_ms"] / max(1, tm["steps"]),
+                 "note": "host time inside tkv_step per call (planning + launches; boundary steps include their "
+                         "synchronous planning reads), net of the wait for the step two calls back; the device "
+                         "never starves while this stays below the device step time"},
         "breakdown_ms_per_step": {n: tm[n] / K for n in ("attend_ms", "score_ms", "flush_ms", "anneal_ms", "apply_ms")},
         "roofline": {"kernel": "K1 paged decode attention", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,

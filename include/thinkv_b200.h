@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TKV_ABI_VERSION 1
+#define TKV_ABI_VERSION 2
 
 enum tkv_status {
   TKV_OK = 0,
@@ -187,6 +187,11 @@ typedef struct tkv_timing_t {
   double attend_ms, score_ms, flush_ms, anneal_ms, apply_ms;
   int64_t attend_launches, score_launches, flush_launches, anneal_launches, apply_launches;
   int64_t total_launches;  /* every kernel launched by the run since enable */
+  /* host side of tkv_step / tkv_step_layer / tkv_step_host_async since enable:
+   * host_ms = time in the call minus host_wait_ms, the time blocked waiting
+   * for the step two calls back (pinned staging reuse); steps = calls */
+  double host_ms, host_wait_ms;
+  int64_t steps;
 } tkv_timing_t;
 int tkv_timing_enable(tkv_run* run, int enable);
 int tkv_timing_read(tkv_run* run, tkv_timing_t* out);

@@ -58,7 +58,8 @@ class Bytes(C.Structure):
 class Timing(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("attend_ms", "score_ms", "flush_ms", "anneal_ms", "apply_ms")] + \
                [(n, C.c_int64) for n in ("attend_launches", "score_launches", "flush_launches",
-                                         "anneal_launches", "apply_launches", "total_launches")]
+                                         "anneal_launches", "apply_launches", "total_launches")] + \
+               [("host_ms", C.c_double), ("host_wait_ms", C.c_double), ("steps", C.c_int64)]
 
 
 class GatherDesc(C.Structure):

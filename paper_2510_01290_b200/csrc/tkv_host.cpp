@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -206,6 +207,9 @@ struct tkv_run {
   double acc_ms[5] = {0, 0, 0, 0, 0};
   int64_t acc_n[5] = {0, 0, 0, 0, 0};
   int64_t launches = 0;
+  // host side of the step calls (tkv_timing_t host_ms / host_wait_ms / steps)
+  double host_ms = 0.0, host_wait_ms = 0.0;
+  int64_t host_steps = 0;
   // device byte accounting (tkv_bytes_accounting)
   bool bytes_on = false;
   unsigned long long* d_bytes_acc = nullptr;   // [U][5] per-unit sums
@@ -316,9 +320,29 @@ void validate(const tkv_run_desc& d) {
 // -------------------------------------------------------------------------
 void begin_phase(tkv_run* r) {
   r->phase ^= 1;
-  CUDA_OK(cudaEventSynchronize(r->pinned_ev[r->phase]));
+  if (r->timing) {
+    const auto t0 = std::chrono::steady_clock::now();
+    CUDA_OK(cudaEventSynchronize(r->pinned_ev[r->phase]));
+    r->host_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  } else {
+    CUDA_OK(cudaEventSynchronize(r->pinned_ev[r->phase]));
+  }
   r->arena_used = 0;
 }
+// Host time of one public step call, net of the begin_phase wait (timing on).
+struct HostClock {
+  tkv_run* r;
+  double wait0;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostClock(tkv_run* run) : r(run), wait0(run->host_wait_ms), t0(std::chrono::steady_clock::now()) {}
+  ~HostClock() {
+    if (!r->timing) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    r->host_ms += ms - (r->host_wait_ms - wait0);
+    r->host_steps += 1;
+  }
+};
+
 void end_phase(tkv_run* r) { CUDA_OK(cudaEventRecord(r->pinned_ev[r->phase], r->stream)); }
 
 template <typename T>
@@ -1402,6 +1426,7 @@ int tkv_run_destroy(tkv_run* run) {
 
 int tkv_step(tkv_run* run, const void* q, const void* k, const void* v, float* out, void* stream) {
   try {
+    HostClock hc(run);
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     cudaEvent_t ev = nullptr;
     if (user && user != run->stream) {  // order the run's stream after the caller's
@@ -1465,6 +1490,7 @@ void step_host_async(tkv_run* run, const void* q, const void* k, const void* v, 
 int tkv_step_layer(tkv_run* run, int layer, int num_layers, const void* q, const void* k, const void* v, float* out,
                    void* stream) {
   try {
+    HostClock hc(run);
     const tkv_run_desc& d = run->desc;
     if (num_layers < 1 || d.units_per_seq % num_layers != 0)
       throw TkvError(TKV_ERR_CONFIG, "num_layers must divide units_per_seq");
@@ -1527,6 +1553,7 @@ int tkv_step_host(tkv_run* run, const void* q, const void* k, const void* v, flo
 
 int tkv_step_host_async(tkv_run* run, const void* q, const void* k, const void* v, float* out) {
   try {
+    HostClock hc(run);
     step_host_async(run, q, k, v, out);
     return TKV_OK;
   } catch (const TkvError& e) {
@@ -1750,6 +1777,8 @@ int tkv_timing_enable(tkv_run* run, int enable) {
     run->timing = enable != 0;
     for (int i = 0; i < 5; ++i) { run->acc_ms[i] = 0.0; run->acc_n[i] = 0; }
     run->launches = 0;
+    run->host_ms = run->host_wait_ms = 0.0;
+    run->host_steps = 0;
     return TKV_OK;
   } catch (const TkvError& e) {
     return fail(e);
@@ -1794,6 +1823,9 @@ int tkv_timing_read(tkv_run* run, tkv_timing_t* out) {
     out->anneal_launches = run->acc_n[CAT_ANNEAL];
     out->apply_launches = run->acc_n[CAT_APPLY];
     out->total_launches = run->launches;
+    out->host_ms = run->host_ms;
+    out->host_wait_ms = run->host_wait_ms;
+    out->steps = run->host_steps;
     return TKV_OK;
   } catch (const TkvError& e) {
     return fail(e);

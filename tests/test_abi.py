@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), f"{s} missing from libthinkv_b200.so"
     assert sorted(_abi.EXPORTS) == syms
-    assert lib.tkv_abi_version() == 1
+    assert lib.tkv_abi_version() == 2
 
 
 def test_library_is_sm100a():
