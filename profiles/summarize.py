@@ -50,6 +50,17 @@ def full(path):
         for m in FULL:
             if m in idx:
                 print(f"- {m}: {r[idx[m]]} {units[idx[m]]}")
+        st = {}
+        for h, i in idx.items():
+            if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued"):
+                try:
+                    st[h[len("smsp__pcsamp_warps_issue_stalled_"):]] = float(r[i].replace(",", ""))
+                except ValueError:
+                    pass
+        tot = sum(st.values())
+        if tot > 0:
+            top = sorted(st.items(), key=lambda x: -x[1])[:6]
+            print("- top stall reasons (pc sampling): " + ", ".join(f"{k} {100 * v / tot:.1f}%" for k, v in top))
         print()
 
 

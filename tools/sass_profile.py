@@ -7,9 +7,11 @@ import sys
 
 def main(path, top=40):
     rows = list(csv.reader(open(path)))
-    hdr = rows[1]
+    hi = next(i for i, r in enumerate(rows) if "Instructions Executed" in r)
+    hdr = rows[hi]
     ix = {h: i for i, h in enumerate(hdr)}
-    data = [r for r in rows[2:] if len(r) == len(hdr)]
+    # (multi-kernel exports repeat the header per kernel: skip those rows)
+    data = [r for r in rows[hi + 1:] if len(r) == len(hdr) and r[ix["Instructions Executed"]] != "Instructions Executed"]
     ex = collections.Counter()
     st = collections.Counter()
     tot_e = tot_s = 0
