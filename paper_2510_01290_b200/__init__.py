@@ -164,6 +164,21 @@ class DecodeRun:
         check(lib.tkv_step_layer(self._h, layer, num_layers, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                  out.data_ptr(), s))
 
+    def step_plain(self) -> bool:
+        """True if the next step's only device work is the attention kernel
+        (tkv_step_plain): it may be replayed from a captured CUDA graph."""
+        r = lib.tkv_step_plain(self._h)
+        if r < 0:
+            check(-r)
+        return r == 1
+
+    def graph_step_begin(self, stream=None):
+        """Before each replay of a captured step on `stream`
+        (tkv_graph_step_begin): stages the step's scalars and advances the
+        run by one plain step.  Under stream capture, step()/step_layer()
+        record their launches instead of executing them."""
+        check(lib.tkv_graph_step_begin(self._h, self._stream(stream)))
+
     def step_host(self, q, k, v, out):
         """Same with host (numpy / pinned CPU tensor) buffers, synchronous."""
         ptr = (lambda a: a.ctypes.data) if hasattr(q, "ctypes") else (lambda a: a.data_ptr())

@@ -20,6 +20,7 @@ EXPORTS = (
     "tkv_run_destroy", "tkv_step", "tkv_step_layer", "tkv_step_host", "tkv_finish", "tkv_synchronize",
     "tkv_position", "tkv_dump_json", "tkv_bytes", "tkv_unit_sparsity", "tkv_synth_inputs",
     "tkv_timing_enable", "tkv_timing_read", "tkv_bytes_accounting", "tkv_bytes_accumulated", "tkv_exp_f64", "tkv_step_host_async", "tkv_export_cache",
+    "tkv_step_plain", "tkv_graph_step_begin",
     "tkv_dropin_quantize_window", "tkv_dropin_decode", "tkv_dropin_gqa_attend", "tkv_dropin_sparsity",
     "tkv_dropin_kmeans_select", "tkv_dropin_pager_place", "tkv_dropin_pager_evict",
     "tkv_gather_create", "tkv_gather_destroy", "tkv_gather_step", "tkv_gather_stats", "tkv_gather_ids",
@@ -91,6 +92,8 @@ def _load():
     L.tkv_step_host.argtypes = [vp, vp, vp, vp, vp]
     L.tkv_step_layer.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp]
     L.tkv_step_host_async.argtypes = [vp, vp, vp, vp, vp]
+    L.tkv_step_plain.argtypes = [vp]
+    L.tkv_graph_step_begin.argtypes = [vp, vp]
     L.tkv_finish.argtypes = [vp]
     L.tkv_synchronize.argtypes = [vp]
     L.tkv_position.argtypes = [vp]

@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(kThreads) attend_kernel(TkvState st, const voi
                                                           const void* __restrict__ kin,
                                                           const void* __restrict__ vin, float* __restrict__ out,
                                                           int buf_half, int nbuf, int put_half, int put_slot) {
+  tkv_step_scalars(st, buf_half, nbuf, put_half, put_slot);
   const TkvDims& dm = st.dm;
   const int li = blockIdx.x;             // launch-local index: q/k/v/out rows
   const int u = tkv_unit_of(st, li);     // unit: cache state

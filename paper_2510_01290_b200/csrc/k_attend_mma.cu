@@ -474,6 +474,7 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_mma_kernel(TkvState st,
                                                                   const void* __restrict__ vin,
                                                                   float* __restrict__ out, int buf_half, int nbuf,
                                                                   int put_half, int put_slot) {
+  tkv_step_scalars(st, buf_half, nbuf, put_half, put_slot);
   const TkvDims& dm = st.dm;
   const int li = blockIdx.x;            // launch-local index: q/k/v/out rows
   const int u = tkv_unit_of(st, li);    // unit: cache state
@@ -1021,6 +1022,7 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
                                                                     const void* __restrict__ vin,
                                                                     float* __restrict__ out, int buf_half, int nbuf,
                                                                     int put_half, int put_slot) {
+  tkv_step_scalars(st, buf_half, nbuf, put_half, put_slot);
   const TkvDims& dm = st.dm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int li = blockIdx.x * kWarps + warp;  // launch-local index: q/k/v/out rows
@@ -1236,7 +1238,10 @@ cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void*
   if (v3) {
     const bool pvn = st.dm.maxpool || st.dm.G <= 4;
     if (D == 128) {
-      if (pvn) return launch_k1_warp<128, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+      if (pvn) {
+        if (getenv("TKV_K1_MINB4")) return launch_k1_warp<128, 4, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+        return launch_k1_warp<128, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+      }
       return launch_k1_warp<128, 3, false>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
     }
     if (pvn) return launch_k1_warp<64, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);

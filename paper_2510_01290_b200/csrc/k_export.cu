@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(32 * kWarps) export_kernel(TkvState st, int un
                                                              uint8_t* __restrict__ dst) {
   const TkvDims& dm = st.dm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ui = blockIdx.x * kWarps + warp;
+  const int ui = blockIdx.x * (blockDim.x >> 5) + warp;
   if (ui >= nunits) return;
   const int u = unit0 + ui;
   extern __shared__ int32_t sh[];
@@ -243,17 +243,26 @@ __global__ void __launch_bounds__(32 * kWarps) export_kernel(TkvState st, int un
 
 }  // namespace
 
-size_t tkv_export_smem(const TkvState& st) { return (size_t)kWarps * (2 * st.dm.NS + 2) * sizeof(int32_t); }
+// Warps (units) per CTA: kWarps, fewer when a large pool's per-warp lists
+// would not fit in shared memory.
+static int export_warps(const TkvState& st) {
+  const size_t per = (2 * (size_t)st.dm.NS + 2) * sizeof(int32_t);
+  int w = kWarps;
+  while (w > 1 && (size_t)w * per > 200 * 1024) --w;
+  return w;
+}
+size_t tkv_export_smem(const TkvState& st) { return (size_t)export_warps(st) * (2 * st.dm.NS + 2) * sizeof(int32_t); }
 
 cudaError_t tkv_launch_export(const TkvState& st, int unit0, int nunits, int npos, int pass, int64_t* sizes,
                               const int64_t* offsets, uint8_t* dst, cudaStream_t stream) {
   if (nunits <= 0) return cudaSuccess;
+  const int w = export_warps(st);
   const size_t smem = tkv_export_smem(st);
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // NS > ~25K slots per unit
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(export_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  export_kernel<<<(nunits + kWarps - 1) / kWarps, 32 * kWarps, smem, stream>>>(st, unit0, nunits, npos, pass, sizes,
-                                                                              offsets, dst);
+  export_kernel<<<(nunits + w - 1) / w, 32 * w, smem, stream>>>(st, unit0, nunits, npos, pass, sizes, offsets, dst);
   return cudaGetLastError();
 }

@@ -233,6 +233,19 @@ struct tkv_run {
   int64_t open_pos = -1;
   bool open_decode = false, open_refresh = false;
   int open_put_half = 0, open_put_slot = 0;
+  // CUDA-graph replay of plain steps (tkv_step_plain / tkv_graph_step_begin):
+  // K1 launches recorded under stream capture read {buf_half, nbuf,
+  // put_half, put_slot} from d_stepdesc, staged per replayed step through a
+  // pinned ring on the caller's stream.
+  static constexpr int kDescRing = 64;
+  int32_t* d_stepdesc = nullptr;
+  int32_t* h_stepdesc = nullptr;  // pinned [kDescRing][4]
+  cudaEvent_t desc_ev[kDescRing]{};
+  int desc_next = 0;
+  int cap_next_layer = 0, cap_layers = 0;
+  int64_t cap_launches = 0;    // K1 launches recorded by the capture in progress
+  int64_t graph_launches = 0;  // ... by the last completed capture (per replayed step)
+  int64_t graph_steps = 0;     // steps advanced by tkv_graph_step_begin
   std::vector<void*> allocations;
 };
 
@@ -1156,6 +1169,98 @@ void do_step(tkv_run* r, const void* q, const void* k, const void* v, float* out
   step_end(r, c);
 }
 
+// ---- CUDA-graph replay of plain steps -------------------------
+// A plain step's only device work is K1 (which also buffers the incoming
+// token): no refresh boundary, no emission, no Case-2 anneal, no dump, no
+// sparsity trace, no byte accounting.  Decided with the size arithmetic the
+// step itself runs (plan_overflow on a copy of each over-budget group).
+bool next_step_plain(const tkv_run* r) {
+  const tkv_run_desc& d = r->desc;
+  if (r->finished || r->pos >= r->total_steps || r->next_layer != 0) return false;
+  const bool decode = r->pos >= d.prompt_len;
+  const int64_t bstep = decode ? r->pos - d.prompt_len : r->pos;
+  if (bstep % d.tau == 0 || r->buf_len + 1 >= d.group_size) return false;
+  if (r->dump_at.count(r->pos) || (decode && d.record_sparsity_trace) || r->bytes_on) return false;
+  for (const Group& g : r->groups) {
+    if (g.open < 0) return false;
+    if (g.total + 1 <= d.budget) continue;
+    Group c = g;  // the step buffers one token under the open segment, then enforces the budget
+    c.segs[c.open].size += 1;
+    c.segs[c.open].initial += 1;
+    c.total += 1;
+    if (!plan_overflow(r, c, 0).ops.empty()) return false;
+  }
+  return true;
+}
+
+bool capturing(cudaStream_t s) {
+  if (!s) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CUDA_OK(cudaStreamIsCapturing(s, &cs));
+  return cs == cudaStreamCaptureStatusActive;
+}
+
+// Record one K1 launch on the capturing stream.  The per-step scalars come
+// from d_stepdesc at replay time and the live lists are sized for the whole
+// pool, so the one launch is valid for every plain step it is replayed for.
+void capture_attend(tkv_run* r, cudaStream_t s, const void* q, const void* k, const void* v, float* out,
+                    int lmap_h, int layer) {
+  TkvState st = r->st;
+  st.step_dev = r->d_stepdesc;
+  st.max_live = st.dm.NS;
+  st.lmap_h = lmap_h;
+  st.lmap_ups = r->desc.units_per_seq;
+  st.lmap_off = layer * lmap_h;
+  st.lmap_count = r->desc.num_seqs * lmap_h;
+  check_launch(tkv_launch_attend(st, q, k, v, out, 0, 0, 0, -1, s), "attend kernel (capture)");
+  r->cap_launches += 1;
+}
+
+void capture_layer(tkv_run* r, cudaStream_t s, int layer, int num_layers, const void* q, const void* k,
+                   const void* v, float* out) {
+  if (layer != r->cap_next_layer || (layer > 0 && num_layers != r->cap_layers))
+    throw TkvError(TKV_ERR_CONFIG, "captured layers of a step must be recorded in order 0 .. num_layers-1");
+  if (layer == 0) {
+    r->cap_layers = num_layers;
+    r->cap_launches = 0;
+  }
+  capture_attend(r, s, q, k, v, out, num_layers ? r->desc.units_per_seq / num_layers : 0, layer);
+  if (layer == num_layers - 1 || num_layers == 0) {
+    r->cap_next_layer = 0;
+    r->graph_launches = r->cap_launches;
+  } else {
+    r->cap_next_layer = layer + 1;
+  }
+}
+
+// Before each replay of a captured step on `s`: stage this step's scalars
+// (stream-ordered on s, after the previous replay read them) and advance the
+// run's host state exactly as the eager step would.
+void graph_step_begin(tkv_run* r, cudaStream_t s) {
+  if (r->graph_launches == 0) throw TkvError(TKV_ERR_CONFIG, "no captured step (record one under stream capture)");
+  if (!next_step_plain(r))
+    throw TkvError(TKV_ERR_CONFIG, "the next step is not plain (boundary, emission or eviction): step it eagerly");
+  const StepCtx c = step_begin(r);
+  const int slot = r->desc_next;
+  r->desc_next = (slot + 1) % tkv_run::kDescRing;
+  CUDA_OK(cudaEventSynchronize(r->desc_ev[slot]));
+  int32_t* h = r->h_stepdesc + 4 * slot;
+  h[0] = r->cur_half;
+  h[1] = r->buf_len;
+  h[2] = c.put_half;
+  h[3] = c.put_slot;
+  // order the replay after the run's own stream (eager steps), then stage
+  cudaEvent_t ev = pool_event(r);
+  CUDA_OK(cudaEventRecord(ev, r->stream));
+  CUDA_OK(cudaStreamWaitEvent(s, ev, 0));
+  r->ev_pool.push_back(ev);
+  CUDA_OK(cudaMemcpyAsync(r->d_stepdesc, h, 4 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaEventRecord(r->desc_ev[slot], s));
+  r->launches += r->graph_launches;
+  step_end(r, c);
+  r->graph_steps += 1;
+}
+
 void do_finish(tkv_run* r) {
   if (r->finished) return;
   begin_phase(r);
@@ -1262,6 +1367,9 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   // arenas
   r->arena_cap = 8 << 20;
   r->d_arena = dalloc<uint8_t>(r, r->arena_cap);
+  r->d_stepdesc = dalloc<int32_t>(r, 4, 0);
+  CUDA_OK(cudaMallocHost(&r->h_stepdesc, sizeof(int32_t) * 4 * tkv_run::kDescRing));
+  for (int i = 0; i < tkv_run::kDescRing; ++i) CUDA_OK(cudaEventCreateWithFlags(&r->desc_ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
     CUDA_OK(cudaMallocHost(&r->h_pinned[i], r->arena_cap));
     CUDA_OK(cudaEventCreateWithFlags(&r->pinned_ev[i], cudaEventDisableTiming));
@@ -1317,6 +1425,12 @@ void destroy_run(tkv_run* r) {
   }
   for (void* p : r->allocations) cudaFree(p);
   if (r->km_scratch) cudaFree(r->km_scratch);
+  if (r->h_stepdesc) {
+    for (int i = 0; i < tkv_run::kDescRing; ++i) cudaEventSynchronize(r->desc_ev[i]);
+    cudaFreeHost(r->h_stepdesc);
+  }
+  for (int i = 0; i < tkv_run::kDescRing; ++i)
+    if (r->desc_ev[i]) cudaEventDestroy(r->desc_ev[i]);
   for (auto& t : r->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
@@ -1426,8 +1540,12 @@ int tkv_run_destroy(tkv_run* run) {
 
 int tkv_step(tkv_run* run, const void* q, const void* k, const void* v, float* out, void* stream) {
   try {
-    HostClock hc(run);
     cudaStream_t user = static_cast<cudaStream_t>(stream);
+    if (capturing(user)) {  // record, do not execute (tkv_graph_step_begin replays)
+      capture_layer(run, user, 0, 0, q, k, v, out);
+      return TKV_OK;
+    }
+    HostClock hc(run);
     cudaEvent_t ev = nullptr;
     if (user && user != run->stream) {  // order the run's stream after the caller's
       CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1490,10 +1608,14 @@ void step_host_async(tkv_run* run, const void* q, const void* k, const void* v, 
 int tkv_step_layer(tkv_run* run, int layer, int num_layers, const void* q, const void* k, const void* v, float* out,
                    void* stream) {
   try {
-    HostClock hc(run);
     const tkv_run_desc& d = run->desc;
     if (num_layers < 1 || d.units_per_seq % num_layers != 0)
       throw TkvError(TKV_ERR_CONFIG, "num_layers must divide units_per_seq");
+    if (capturing(static_cast<cudaStream_t>(stream))) {
+      capture_layer(run, static_cast<cudaStream_t>(stream), layer, num_layers, q, k, v, out);
+      return TKV_OK;
+    }
+    HostClock hc(run);
     if (layer != run->next_layer || (layer > 0 && num_layers != run->step_layers))
       throw TkvError(TKV_ERR_CONFIG, "layers of a step must be stepped in order 0 .. num_layers-1");
     cudaStream_t user = static_cast<cudaStream_t>(stream);
@@ -1523,6 +1645,7 @@ int tkv_step_layer(tkv_run* run, int layer, int num_layers, const void* q, const
     if (layer == num_layers - 1) {
       step_end(run, c);
       run->next_layer = 0;
+      run->open_pos = -1;
     } else {
       run->next_layer = layer + 1;
     }
@@ -1555,6 +1678,27 @@ int tkv_step_host_async(tkv_run* run, const void* q, const void* k, const void* 
   try {
     HostClock hc(run);
     step_host_async(run, q, k, v, out);
+    return TKV_OK;
+  } catch (const TkvError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(TkvError(TKV_ERR_UNEXPECTED, e.what()));
+  }
+}
+
+int tkv_step_plain(tkv_run* run) {
+  try {
+    if (!run) throw TkvError(TKV_ERR_CONFIG, "null run");
+    return next_step_plain(run) ? 1 : 0;
+  } catch (const TkvError& e) {
+    return -fail(e);
+  }
+}
+
+int tkv_graph_step_begin(tkv_run* run, void* stream) {
+  try {
+    HostClock hc(run);
+    graph_step_begin(run, static_cast<cudaStream_t>(stream));
     return TKV_OK;
   } catch (const TkvError& e) {
     return fail(e);

@@ -106,7 +106,27 @@ struct TkvState {
   // launch covers i in [0, num_seqs * lmap_h) and
   // u = (i / lmap_h) * lmap_ups + lmap_off + i % lmap_h.  lmap_h == 0: u = i.
   int32_t lmap_h, lmap_ups, lmap_off, lmap_count;
+  // Per-step scalars in device memory (CUDA-graph replay of plain steps,
+  // tkv_graph_step_begin): when non-null, K1 reads {buf_half, nbuf, put_half,
+  // put_slot} from here instead of its launch parameters, so one captured
+  // launch serves every replayed step.  Null on eager launches.
+  const int32_t* step_dev;
 };
+
+// K1's per-step scalars: launch parameters, or the device copy (graph replay).
+__host__ __device__ inline void tkv_step_scalars(const TkvState& st, int& buf_half, int& nbuf, int& put_half,
+                                                 int& put_slot) {
+#ifdef __CUDA_ARCH__
+  if (st.step_dev) {
+    buf_half = st.step_dev[0];
+    nbuf = st.step_dev[1];
+    put_half = st.step_dev[2];
+    put_slot = st.step_dev[3];
+  }
+#else
+  (void)st; (void)buf_half; (void)nbuf; (void)put_half; (void)put_slot;
+#endif
+}
 
 __host__ __device__ inline int tkv_unit_of(const TkvState& st, int i) {
   return st.lmap_h ? (i / st.lmap_h) * st.lmap_ups + st.lmap_off + i % st.lmap_h : i;
