@@ -409,6 +409,18 @@ def main():
         run.synth_inputs(SEED, start + K + i, q, k, v, unit0=unit0)
         host_inputs.append((q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()))
     torch.cuda.synchronize(dev)
+    # the host link the e2e copies ride on (untimed): one step's upload and
+    # download alone, pinned buffers, CUDA events
+    link = {}
+    for name, (dst, src) in {"h2d": (q, host_inputs[0][0]), "d2h": (pouts[0], out.view(pouts[0].shape))}.items():
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dst.copy_(src, non_blocking=True)
+        a.record()
+        for _ in range(5):
+            dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize(dev)
+        link[name + "_GBps"] = 5 * src.numel() * src.element_size() / (a.elapsed_time(b) / 1e3) / 1e9
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
@@ -486,14 +498,16 @@ def main():
         "roofline": {"kernel": "K1 paged decode attention", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                     "traffic_source": traffic.get("source") if traffic else None,
+                     "traffic_source": traffic.get("capture") if traffic else None,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "algorithmic_bytes_source": "k_bytes.cu, computed on the device for every timed K1 launch",
                      "launch_ms": k1_ms, "live_tokens_per_unit": acc["live_slots"] / max(1, acc_launches) / U},
         "e2e": {"value": global_seqs(args, world) * E / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in host_inputs[0])),
                 "d2h_bytes_per_step": int(pouts[0].numel() * 4), "steps": E,
-                "api": "tkv_step_host_async (pinned host buffers, copies overlapped with kernels)"},
+                "api": "tkv_step_host_async (pinned host buffers, copies overlapped with kernels)",
+                "host_link": {**link, "note": "one step's q+k+v-sized upload / output download alone on this box; "
+                              "between boundaries the e2e step is bound by max(device step, copy time)"}},
         "clocks": clk.summary(),
         "context_build_s": t_ctx,
     }

@@ -1238,10 +1238,7 @@ cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void*
   if (v3) {
     const bool pvn = st.dm.maxpool || st.dm.G <= 4;
     if (D == 128) {
-      if (pvn) {
-        if (getenv("TKV_K1_MINB4")) return launch_k1_warp<128, 4, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
-        return launch_k1_warp<128, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
-      }
+      if (pvn) return launch_k1_warp<128, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
       return launch_k1_warp<128, 3, false>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
     }
     if (pvn) return launch_k1_warp<64, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
