@@ -78,9 +78,23 @@ __device__ __forceinline__ void kstm(const TkvState& st, int m, int i, unsigned 
 // x / n for a cluster size n >= 1.  For n = 2^k the multiply by the exact
 // reciprocal 2^-k is the same correctly rounded real x / 2^k as the
 // division, so both produce identical bits; other sizes divide.
+// Other sizes up to kInvN: Markstein's correction from the correctly rounded
+// reciprocal r = RN(1/n) (c_inv_n, written once per device by the host):
+// q0 = RN(x r) lies within one ulp of x/n, the residual x - q0 n is exact in
+// one fma, and RN(q0 + residual * r) is the correctly rounded quotient
+// (Markstein 1990; Muller et al., Handbook of Floating-Point Arithmetic,
+// division by fma) -- the bits of __ddiv_rn(x, n) in 3 fp64 operations
+// instead of the division's reciprocal iteration.  A zero quotient keeps the
+// sign of x (q0).
+constexpr int kInvN = 1024;
+__constant__ double c_inv_n[kInvN + 1];
 __device__ __forceinline__ double div_n(double x, int n) {
   if ((n & (n - 1)) == 0) return __dmul_rn(x, __longlong_as_double((long long)(1024 - __ffs(n)) << 52));
-  return __ddiv_rn(x, (double)n);
+  if (n > kInvN) return __ddiv_rn(x, (double)n);
+  const double r = c_inv_n[n];
+  const double q0 = __dmul_rn(x, r);
+  const double rem = __fma_rn(-q0, (double)n, x);
+  return q0 == 0.0 ? q0 : __fma_rn(rem, r, q0);
 }
 // Out-of-line form for the warp-per-restart kernel: one copy of the division
 // sequence keeps its many concurrent warps inside the instruction cache
@@ -161,8 +175,8 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
   int32_t* ids = reinterpret_cast<int32_t*>(base + geo.ids_off());
   int32_t* seeds = reinterpret_cast<int32_t*>(base + geo.seeds_off());
   int32_t* misc = reinterpret_cast<int32_t*>(base + geo.misc_off());
-  __shared__ int sids[kMaxM];
-  __shared__ int sm_m, sm_bad;
+  __shared__ int sids[kMaxM], sslot[kMaxM];
+  __shared__ int sm_m, sm_bad, sm_found;
   __shared__ double dmean[kMaxM];
   __shared__ int anchors[4];
   const uint32_t* segm = st.seg_mask + ((int64_t)u * dm.NSEG + op.seg) * dm.W;
@@ -171,10 +185,15 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
     for (int b = 0; b < op.span && m < kMaxM; ++b)
       if ((segm[b >> 5] >> (b & 31)) & 1u) sids[m++] = b;
     sm_m = m;
-    int bad = (m != op.m) || st.err[u] != 0;
-    for (int i = 0; i < m && !bad; ++i) bad |= st.tok_slot[(int64_t)u * dm.T + op.seg_start + sids[i]] < 0;
+    sm_found = 0;
+  }
+  __syncthreads();
+  if (sm_m == op.m && op.m <= kMaxM) tkv_member_slots(st, u, op.seg_start, op.span, segm, sslot, &sm_found);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int bad = (sm_m != op.m) || sm_found != sm_m || st.err[u] != 0;
     sm_bad = bad;
-    misc[0] = m;
+    misc[0] = sm_m;
     misc[1] = bad;
   }
   __syncthreads();
@@ -188,7 +207,7 @@ __global__ void __launch_bounds__(256) km_prep_kernel(TkvState st, const TkvAnne
   __shared__ double sxs[kMaxM];
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     ids[i] = sids[i];
-    decode_point(st, u, st.tok_slot[(int64_t)u * dm.T + op.seg_start + sids[i]], sX + (int64_t)i * XS, sxs + i);
+    decode_point(st, u, sslot[i], sX + (int64_t)i * XS, sxs + i);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < m * D; i += blockDim.x) X[i] = (float)sX[(i / D) * XS + i % D];
@@ -1977,6 +1996,19 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
                               int nitems, const int32_t* run_prefix, int nruns, int item0, int item_count,
                               int run0, int run_count, int mmax, int kmax, int R, uint8_t* scratch, double* gsums,
                               int gsums_ctas, uint32_t* log, int scaled_any, int x16, cudaStream_t stream) {
+  {  // RN(1/n) table for div_n, once per device
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+      double inv[kInvN + 1];
+      inv[0] = 0.0;
+      for (int n = 1; n <= kInvN; ++n) inv[n] = 1.0 / (double)n;  // IEEE division: correctly rounded
+      const cudaError_t e = cudaMemcpyToSymbol(c_inv_n, inv, sizeof(inv));
+      if (e != cudaSuccess) return e;
+      done[dev] = true;
+    }
+  }
   KmGeo geo{mmax, kmax, st.dm.D, st.dm.W, R};
   const size_t psmem = x16 ? (size_t)mmax * (st.dm.D + 2) * 2 : (size_t)mmax * (st.dm.D + 1) * 4;
   if (psmem > 160 * 1024) return cudaErrorInvalidConfiguration;
