@@ -376,7 +376,6 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
     if (threadIdx.x == 0) {
       st.slot_win[slot] = w;
       st.slot_id[slot] = pos0 + i;
-      st.tok_slot[(int64_t)u * dm.T + pos0 + i] = sm.claim[i];
     }
   }
   if (w >= 0) {

@@ -462,10 +462,15 @@ __global__ void __launch_bounds__(kThreads) anneal_kernel(TkvState st, const Tkv
       for (int b = 0; b < op.span && m < kMaxM; ++b)
         if ((segm[b >> 5] >> (b & 31)) & 1u) s.ids[m++] = b;
       s.flag = m;
+      s.pair = 0;
     }
     __syncthreads();
     const int m = s.flag;
     bool bad = m != op.m || st.err[u] != 0;
+    // member slots (s.taken is free until the seeds are chosen)
+    if (!bad) tkv_member_slots(st, u, op.seg_start, op.span, segm, s.taken, &s.pair);
+    __syncthreads();
+    bad = bad || s.pair != m;
     Km km;
     km.m = m;
     km.K = op.K;
@@ -482,13 +487,10 @@ __global__ void __launch_bounds__(kThreads) anneal_kernel(TkvState st, const Tkv
       // Decoded fp64 keys (BlockPager::key_of, pager.cpp:280-287; exact products).
       for (int idx = threadIdx.x; idx < m * D; idx += kThreads) {
         const int i = idx / D, ch = idx % D;
-        const int slot = st.tok_slot[(int64_t)u * dm.T + op.seg_start + s.ids[i]];
-        km.X[idx] = slot < 0 ? CUDART_NAN : decode_key(st, u, slot, ch);
+        km.X[idx] = decode_key(st, u, s.taken[i], ch);
       }
       if (threadIdx.x == 0) {
-        int missing = 0;
-        for (int i = 0; i < m; ++i) missing |= st.tok_slot[(int64_t)u * dm.T + op.seg_start + s.ids[i]] < 0;
-        s.flag = missing;
+        s.flag = 0;
         s.have_best = 0;
       }
       __syncthreads();
@@ -557,8 +559,8 @@ __global__ void __launch_bounds__(32) apply_kernel(TkvState st, const TkvAnnealO
                                                    const int32_t* __restrict__ prefix, int nitems,
                                                    const uint32_t* __restrict__ log) {
   const TkvDims& dm = st.dm;
-  const int item = blockIdx.x;
-  if (item >= nitems || threadIdx.x != 0) return;
+  const int item = blockIdx.x, lane = threadIdx.x;
+  if (item >= nitems) return;
   int gi = 0;
   {
     int lo = 0, hi = ngroups - 1;
@@ -571,7 +573,8 @@ __global__ void __launch_bounds__(32) apply_kernel(TkvState st, const TkvAnnealO
   const TkvApplyGroup grp = groups[gi];
   const int urel = item - prefix[gi];
   const int u = grp.unit0 + urel;
-  if (st.err[u] != 0) return;
+  if (st.err[u] != 0) return;  // (uniform: read by every lane before any write)
+  __syncwarp();
   const int P = dm.P, bs = dm.bs, W = dm.W;
   int8_t* th = st.blk_thought + (int64_t)u * P;
   uint8_t* fl = st.blk_filled + (int64_t)u * P;
@@ -579,38 +582,57 @@ __global__ void __launch_bounds__(32) apply_kernel(TkvState st, const TkvAnnealO
   uint8_t* ns = st.blk_nstart + (int64_t)u * P;
   uint32_t touched[64];  // P <= 2048
   for (int i = 0; i < 64; ++i) touched[i] = 0;
-  for (int oi = grp.op_begin; oi < grp.op_end; ++oi) {
+  extern __shared__ int rel_slot[];  // [W * 32]: slot of each live id of the op's segment window
+  const int32_t* sid = st.slot_id + (int64_t)u * dm.NS;
+  bool failed = false;
+  for (int oi = grp.op_begin; oi < grp.op_end && !failed; ++oi) {
     const TkvAnnealOp op = ops[oi];
     const uint32_t* lm = log + op.log_off + (int64_t)urel * W;
-    for (int w = 0; w < W; ++w) {
-      uint32_t bits = lm[w];
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int id = op.seg_start + w * 32 + b;
-        int32_t* ts = st.tok_slot + (int64_t)u * dm.T + id;
-        const int slot = *ts;
-        if (slot < 0) {
-          st.err[u] = TKV_E_INTEGRITY;
-          return;
-        }
-        const int blk = slot / bs, sl = slot % bs;
-        ev[blk] |= 1u << sl;
-        *ts = -1;
-        const int64_t gs = (int64_t)u * dm.NS + slot;
-        const int win = st.slot_win[gs];
-        if (win >= 0) {
-          const int64_t wi = (int64_t)u * dm.NW + win;
-          if (--st.win_refs[wi] <= 0) {
-            st.win_refs[wi] = 0;
-            st.win_free[(int64_t)u * dm.NW + st.win_nfree[u]] = win;
-            st.win_nfree[u] += 1;
+    // The warp maps the window's live ids to slots (slot_id, skipping evicted
+    // slots -- including those of earlier ops of this call); lane 0 then
+    // applies the evictions in id order, so window records return to the free
+    // stack in the reference's order (release_slot_groups, pager.cpp:72-87).
+    __syncwarp();
+    for (int r = lane; r < W * 32; r += 32) rel_slot[r] = -1;
+    __syncwarp();
+    for (int s = lane; s < dm.NS; s += 32) {
+      const int rel = sid[s] - op.seg_start;
+      const int blk = s / bs, sl = s % bs;
+      if (rel >= 0 && rel < op.span && !((ev[blk] >> sl) & 1u) && th[blk] >= 0 && sl < fl[blk]) rel_slot[rel] = s;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (int w = 0; w < W && !failed; ++w) {
+        uint32_t bits = lm[w];
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int slot = rel_slot[w * 32 + b];
+          if (slot < 0) {
+            st.err[u] = TKV_E_INTEGRITY;
+            failed = true;
+            break;
           }
+          const int blk = slot / bs, sl = slot % bs;
+          ev[blk] |= 1u << sl;
+          const int64_t gs = (int64_t)u * dm.NS + slot;
+          const int win = st.slot_win[gs];
+          if (win >= 0) {
+            const int64_t wi = (int64_t)u * dm.NW + win;
+            if (--st.win_refs[wi] <= 0) {
+              st.win_refs[wi] = 0;
+              st.win_free[(int64_t)u * dm.NW + st.win_nfree[u]] = win;
+              st.win_nfree[u] += 1;
+            }
+          }
+          touched[blk >> 5] |= 1u << (blk & 31);
         }
-        touched[blk >> 5] |= 1u << (blk & 31);
       }
     }
+    failed = __shfl_sync(0xffffffffu, failed, 0);
   }
+  if (failed) return;
+  if (lane != 0) return;
   for (int w = 0; w < 64; ++w) {
     uint32_t bits = touched[w];
     while (bits) {
@@ -652,6 +674,7 @@ cudaError_t tkv_launch_apply(const TkvState& st, const TkvAnnealOp* ops, const T
                              int ngroups, const int32_t* unit_prefix, int nitems, const uint32_t* log,
                              cudaStream_t stream) {
   if (nitems <= 0) return cudaSuccess;
-  apply_kernel<<<nitems, 32, 0, stream>>>(st, ops, groups, ngroups, unit_prefix, nitems, log);
+  apply_kernel<<<nitems, 32, (size_t)st.dm.W * 32 * sizeof(int), stream>>>(st, ops, groups, ngroups, unit_prefix,
+                                                                          nitems, log);
   return cudaGetLastError();
 }

@@ -27,7 +27,7 @@
 //
 // Two launches: pass 0 sizes every unit, the host scans the sizes into
 // offsets, pass 1 writes.  One warp per unit; live tokens are compacted in id
-// order from tok_slot with ballots into shared memory.
+// order: the block table's live slots, sorted by token id in shared memory.
 #include <cuda_runtime.h>
 
 #include "tkv_codec.cuh"
@@ -120,18 +120,55 @@ __global__ void __launch_bounds__(32 * kWarps) export_kernel(TkvState st, int un
   // per warp: slot[NS] then record starts[NS + 1]
   int32_t* lslot = sh + (int64_t)warp * (2 * dm.NS + 2);
   int32_t* rstart = lslot + dm.NS;
-  const int32_t* ts = st.tok_slot + (int64_t)u * dm.T;
   const unsigned below = (1u << lane) - 1u;
-  // 1. live tokens in ascending id (tok_slot[id] >= 0); ids are recovered from slot_id.
+  // 1. live tokens in ascending id: the live slots of the block table
+  //    (BlockPager::read_active, pager.cpp:261-271) as (id, slot) keys, then a
+  //    bitonic sort by id in place (implicit +inf padding to a power of two:
+  //    every compare-exchange is ascending, so partners beyond n are no-ops).
+  uint64_t* key = reinterpret_cast<uint64_t*>(lslot);  // NS + 1 keys fit in the warp's 2 NS + 2 words
   int n = 0;
-  for (int b = 0; b < npos; b += 32) {
-    const int id = b + lane;
-    const int s = id < npos ? ts[id] : -1;
-    const unsigned bal = __ballot_sync(0xffffffffu, s >= 0);
-    if (s >= 0) lslot[n + __popc(bal & below)] = s;
-    n += __popc(bal);
+  {
+    const int8_t* th = st.blk_thought + (int64_t)u * dm.P;
+    const uint8_t* fl = st.blk_filled + (int64_t)u * dm.P;
+    const uint32_t* ev = st.blk_evict + (int64_t)u * dm.P;
+    const int32_t* sid = st.slot_id + (int64_t)u * dm.NS;
+    for (int b = 0; b < dm.NS; b += 32) {
+      const int s = b + lane;
+      bool live = false;
+      if (s < dm.NS) {
+        const int blk = s / dm.bs, sl = s % dm.bs;
+        live = th[blk] >= 0 && sl < fl[blk] && !((ev[blk] >> sl) & 1u);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, live);
+      if (live) key[n + __popc(bal & below)] = ((uint64_t)(uint32_t)sid[s] << 32) | (uint32_t)s;
+      n += __popc(bal);
+    }
   }
   __syncwarp();
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  for (int k = 2; k <= p2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = lane; t < p2 / 2; t += 32) {
+        // pair t of this stage: i < partner, both in one block of size 2j
+        const int i = (t / j) * 2 * j + (t % j);
+        const int partner = j == (k >> 1) ? (i | (2 * j - 1)) - (i & (2 * j - 1)) : i + j;  // flip, then half-cleaners
+        if (partner < n) {
+          const uint64_t a = key[i], c = key[partner];
+          if (a > c) { key[i] = c; key[partner] = a; }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  // keys -> slots in place: chunk c's slots overwrite keys of chunks <= c / 2, already read
+  for (int b = 0; b < n; b += 32) {
+    const int i = b + lane;
+    const int s = i < n ? (int)(uint32_t)key[i] : 0;
+    __syncwarp();
+    if (i < n) lslot[i] = s;
+    __syncwarp();
+  }
   // 2. record starts: kind/band change, or (quantised) a different window
   int nrec = 0;
   for (int b = 0; b < n; b += 32) {

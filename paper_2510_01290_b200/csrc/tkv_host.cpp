@@ -1351,7 +1351,6 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   st.win_refs = dalloc<int32_t>(r, U * dm.NW, 0);
   st.win_free = dalloc<int32_t>(r, U * dm.NW);
   st.win_nfree = dalloc<int32_t>(r, U);
-  st.tok_slot = dalloc<int32_t>(r, U * (size_t)dm.T, 0xFF);
   st.seg_mask = dalloc<uint32_t>(r, U * dm.NSEG * dm.W, 0xFF);
   st.buf = dalloc<uint8_t>(r, U * 4 * (size_t)dm.g * dm.D * dm.in_bytes, 0);
   st.sparsity = dalloc<double>(r, U);

@@ -24,7 +24,6 @@
 //                 one 16-token emission), kscale_f32[NW], vscale_f32[NW] (FP8
 //                 per-window scales), refs[NW] (live slots referencing it),
 //                 free stack[NW] + nfree.
-//   tokens        tok_slot[T] i32: slot of each live token id (-1 otherwise).
 //   segments      segmask[NSEG][W] u32: member bitmask relative to start_step.
 //   buffer        buf_k/buf_v[2][g][d] input dtype (double-buffered emission window).
 #pragma once
@@ -89,8 +88,7 @@ struct TkvState {
   int32_t* win_refs;
   int32_t* win_free;
   int32_t* win_nfree;
-  // tokens / segments / buffer
-  int32_t* tok_slot;
+  // segments / buffer
   uint32_t* seg_mask;
   uint8_t* buf;          // [U][2][2 (k,v)][g][D] * in_bytes
   // per-unit outputs of the score kernel and sticky device errors
@@ -127,6 +125,35 @@ __host__ __device__ inline void tkv_step_scalars(const TkvState& st, int& buf_ha
   (void)st; (void)buf_half; (void)nbuf; (void)put_half; (void)put_slot;
 #endif
 }
+
+#ifdef __CUDACC__
+// Slots of a closed segment's members (BlockPager::key_of, pager.cpp:280-287)
+// without a token-id index: a live slot holds a member iff its token id lies
+// in the segment's window [seg_start, seg_start + span) and the id's member
+// bit is set.  A token is written to exactly one slot and its member bit is
+// cleared when it is evicted, so every member is found exactly once; evicted
+// slots are skipped as well.  Block-cooperative: rank_slot[r] = the slot of the
+// r-th member in id order; *found (shared, zeroed by the caller) counts them.
+__device__ inline void tkv_member_slots(const TkvState& st, int u, int seg_start, int span, const uint32_t* segm,
+                                        int* rank_slot, int* found) {
+  const TkvDims& dm = st.dm;
+  const int32_t* sid = st.slot_id + (int64_t)u * dm.NS;
+  const uint32_t* ev = st.blk_evict + (int64_t)u * dm.P;
+  for (int s = threadIdx.x; s < dm.NS; s += blockDim.x) {
+    const int rel = sid[s] - seg_start;
+    if (rel < 0 || rel >= span) continue;
+    const uint32_t w = segm[rel >> 5];
+    const int blk = s / dm.bs, sl = s % dm.bs;
+    if (!((w >> (rel & 31)) & 1u) || ((ev[blk] >> sl) & 1u) || st.blk_thought[(int64_t)u * dm.P + blk] < 0 ||
+        sl >= st.blk_filled[(int64_t)u * dm.P + blk])
+      continue;
+    int rank = __popc(w & ((1u << (rel & 31)) - 1u));
+    for (int k = 0; k < (rel >> 5); ++k) rank += __popc(segm[k]);
+    rank_slot[rank] = s;
+    atomicAdd(found, 1);
+  }
+}
+#endif
 
 __host__ __device__ inline int tkv_unit_of(const TkvState& st, int i) {
   return st.lmap_h ? (i / st.lmap_h) * st.lmap_ups + st.lmap_off + i % st.lmap_h : i;
