@@ -58,3 +58,34 @@ def test_gather_fast_scores_run():
     assert st["eviction_steps"] == 80 - budget
     assert len(gpu.ids(0)) == budget and st["moved_token_slots"] >= 0
     assert torch.isfinite(out).all()
+
+
+def test_gather_fast_scores_victim_disagreement_rate():
+    """Pins how often the fp32-score mode (the config-5 sweep's mode) evicts a
+    different victim than the reference's fp64 scores: every unit runs
+    against the oracle on identical inputs until its kept ids first differ;
+    the disagreement rate is diverged units / evictions compared."""
+    units, G, D, budget, steps = 16, 4, 128, 32, 200
+    dev = torch.device("cuda:0")
+    gpu = GatherRun(units, G, D, budget, exact=False)
+    orc = O.GatherOracle(units, G, D, budget)
+    out = torch.empty((units, G, D), device=dev)
+    diverged = {}
+    compared = 0
+    for t in range(steps):
+        q, k, v = O.synth_step(SEED, units, 32, units, G, D, t)
+        orc.step(O.bf16_to_f64(q), O.bf16_to_f64(k), O.bf16_to_f64(v))
+        tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev) for x in (q, k, v))
+        gpu.step(tq, tk, tv, out)
+        if t < budget:
+            continue
+        for u in range(units):
+            if u in diverged:
+                continue
+            compared += 1
+            if not np.array_equal(gpu.ids(u), orc.ids(u)):
+                diverged[u] = t
+    rate = len(diverged) / max(1, compared)
+    print(f"gather fast scores: {len(diverged)} of {units} units diverged over {compared} compared evictions "
+          f"(rate {rate:.4f}); first divergence steps {sorted(diverged.values())}")
+    assert rate < 0.02, rate
