@@ -99,7 +99,7 @@ def main():
         del th0
     if args.out:
         with open(os.path.join(ROOT, args.out), "w") as f:
-            json.dump({"what": "BASELINE config 5 sweep (sweep_config5.py)", "points": results}, f, indent=1)
+            json.dump({"what": "BASELINE config 5 sweep (tools/sweep_config5.py)", "points": results}, f, indent=1)
 
 
 if __name__ == "__main__":
