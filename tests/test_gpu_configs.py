@@ -61,6 +61,21 @@ def test_baseline_config2_units_over_the_whole_32k():
     compare_units_state(res)
 
 
+@pytest.mark.parametrize("n", [3, 4])
+def test_baseline_configs_3_and_4_units_over_the_whole_generation(n):
+    """configs[2] (GPT-OSS-20B shape: d=64, G=8 per-head, 24 layers, 32K
+    generated, budget 1024) and configs[3] (R1-Distill-Qwen-14B shape: G=5,
+    48 layers, 16K generated, budget 819 = 5%): 8 units spread over each
+    batch decoded over the whole generation against the oracle -- the head
+    shapes of the bench lines, at their full lengths and budgets."""
+    cfg = baseline_config(n)
+    assert (cfg.head_dim, cfg.num_q_heads) == ((64, 8) if n == 3 else (128, 5))
+    units = [i * (cfg.units // 8) + (i * 29) % cfg.units_per_seq for i in range(8)]
+    check = set(range(0, cfg.max_gen_len, 211)) | set(range(cfg.max_gen_len - 130, cfg.max_gen_len))
+    res = run_parity_units(cfg, units, check=check)
+    compare_units_state(res)
+
+
 def test_f64_inputs_with_raw16_band():
     """f64 inputs with a 16-bit passthrough band: the raw fp64 keys take the
     fp64-key anneal kernel (k_evict.cu anneal_kernel) -- the configuration a
