@@ -186,7 +186,8 @@ struct tkv_run {
   uint8_t* km_scratch = nullptr;   // K-means v2 per-instance scratch (grown on demand)
   int64_t km_scratch_bytes = 0;
   double* km_sums = nullptr;       // per restart-CTA sums rows
-  int km_sums_ctas = 0;
+  int64_t km_sums_doubles = 0;     // capacity
+  double* km_sums_grown = nullptr; // (owned) replacement when a wave needs more row blocks
   int scratch_ctas = 0;
   int64_t scratch_per_cta = 0;
   int max_m = 0;
@@ -570,12 +571,24 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
       };
       const int run0 = run_of_item(i0);
       const int run1 = i0 + cnt < items ? run_of_item(i0 + cnt) : runs;
+      // One restart launch per chunk: the global sums row blocks (one per
+      // restart CTA of the m > 32 classes) grow to hold every run, so the
+      // wave has a single tail instead of one per sub-launch (<= 16 GB).
+      const int64_t block = (int64_t)std::max(1, kmax) * (2 * dm.D + 1);
+      if (mmax > 32) {
+        const int64_t need = std::min<int64_t>((int64_t)(run1 - run0) * block, (int64_t)2 << 30);
+        if (need > r->km_sums_doubles) {
+          CUDA_OK(cudaStreamSynchronize(r->stream));
+          if (r->km_sums_grown) CUDA_OK(cudaFree(r->km_sums_grown));
+          CUDA_OK(cudaMalloc(&r->km_sums_grown, (size_t)need * sizeof(double)));
+          r->km_sums = r->km_sums_grown;
+          r->km_sums_doubles = need;
+        }
+      }
+      const int gctas = (int)std::max<int64_t>(1, std::min<int64_t>(1 << 30, r->km_sums_doubles / block));
       launch(r, CAT_ANNEAL, "kmeans kernels", [&] {
         return tkv_launch_kmeans(r->st, d_ops, (int)wv.size(), d_pre, items, d_rpre, runs, i0, cnt, run0,
-                                 run1 - run0, mmax, kmax, R, r->km_scratch, r->km_sums,
-                                 (int)std::min<int64_t>(1 << 20, (int64_t)r->km_sums_ctas * std::max(1, r->max_m - 1) /
-                                                                    std::max(1, kmax)),
-                                 r->d_log,
+                                 run1 - run0, mmax, kmax, R, r->km_scratch, r->km_sums, gctas, r->d_log,
                                  fp8 ? 1 : 0, raw ? 0 : 1, r->stream);
       });
     }
@@ -1386,8 +1399,9 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   r->scratch_per_cta = f64_raw ? (int64_t)6 * r->max_m * dm.D : 1;
   r->scratch_ctas = f64_raw ? (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, U)) : 1;
   r->d_scratch = dalloc<double>(r, (size_t)r->scratch_ctas * r->scratch_per_cta);
-  r->km_sums_ctas = 2048;  // row blocks at the widest class; narrower classes fit proportionally more
-  r->km_sums = dalloc<double>(r, (size_t)r->km_sums_ctas * std::max(1, r->max_m - 1) * (2 * dm.D + 1));  // sums | means (128-point class)
+  // sums | means row blocks of the m > 32 restart classes (grown per wave in execute_plans)
+  r->km_sums_doubles = (int64_t)2048 * std::max(1, r->max_m - 1) * (2 * dm.D + 1);
+  r->km_sums = dalloc<double>(r, (size_t)r->km_sums_doubles);
   // sequences, and their planning groups: the whole sequence, or one unit
   // per group when labels are per layer (sizes then evolve per layer)
   r->group_units = (d.per_layer_thought && !d.scripted) ? 1 : d.units_per_seq;
@@ -1424,6 +1438,7 @@ void destroy_run(tkv_run* r) {
   }
   for (void* p : r->allocations) cudaFree(p);
   if (r->km_scratch) cudaFree(r->km_scratch);
+  if (r->km_sums_grown) cudaFree(r->km_sums_grown);
   if (r->h_stepdesc) {
     for (int i = 0; i < tkv_run::kDescRing; ++i) cudaEventSynchronize(r->desc_ev[i]);
     cudaFreeHost(r->h_stepdesc);
