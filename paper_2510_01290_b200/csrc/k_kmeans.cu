@@ -785,27 +785,44 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 
     // 153-156) summed per column in any order: only "d == 0" (exact for a sum
     // of non-negative terms) and "sqrt(d) < 1e-6" (decided with a relative
     // margin, else by the channel-order sum from the saved old centroid) are used.
-    for (int base = 0; base < K * D; base += NT) {
-      const int idx = base + threadIdx.x;
-      const bool valid = idx < K * D;
-      const int c = valid ? rs.row(idx) : -1, ch = valid ? rs.col(idx) : 0;
-      double t2 = 0.0;
-      if (valid && s.ccols[c]) {
-        double acc = 0.0;
-        for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
-        const double nx = div_n(acc, s.sizes[c]);
-        const double old = Mn[(int64_t)c * MS + ch];
-        const double t = __dsub_rn(nx, old);
-        t2 = __dmul_rn(t, t);
-        S[idx] = old;
-        Mn[(int64_t)c * MS + ch] = nx;
+    // Four items per thread at a time, their old centroid values loaded
+    // first (independent loads in flight instead of one dependent chain per
+    // item); warps whose centroid row is unchanged skip the reduction.
+    constexpr int kU = (NT == 256 && MAXM == 128) ? 4 : 1;  // (the 64-point classes spill with more)
+    for (int base = 0; base < K * D; base += kU * NT) {
+      int cc[kU];
+      bool act[kU];
+      double old[kU];
+#pragma unroll
+      for (int k = 0; k < kU; ++k) {
+        const int idx = base + k * NT + threadIdx.x;
+        const bool valid = idx < K * D;
+        cc[k] = valid ? rs.row(idx) : -1;
+        act[k] = valid && s.ccols[cc[k]];
+        old[k] = act[k] ? Mn[(int64_t)cc[k] * MS + rs.col(idx)] : 0.0;
       }
-      const int c0 = __shfl_sync(0xffffffffu, c, 0);
-      if (__all_sync(0xffffffffu, c == c0)) {
-        for (int o = 16; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-        if ((threadIdx.x & 31) == 0 && c0 >= 0) atomicAdd(&s.mv[c0], t2);
-      } else if (valid) {
-        atomicAdd(&s.mv[c], t2);
+#pragma unroll
+      for (int k = 0; k < kU; ++k) {
+        const int idx = base + k * NT + threadIdx.x;
+        double t2 = 0.0;
+        if (act[k]) {
+          const int c = cc[k], ch = rs.col(idx);
+          double acc = 0.0;
+          for (int q = s.offs[c]; q < s.offs[c + 1]; ++q) acc = __dadd_rn(acc, xval(X, xs, s.order[q], ch, XS, scaled));
+          const double nx = div_n(acc, s.sizes[c]);
+          const double t = __dsub_rn(nx, old[k]);
+          t2 = __dmul_rn(t, t);
+          S[idx] = old[k];
+          Mn[(int64_t)c * MS + ch] = nx;
+        }
+        if (!__any_sync(0xffffffffu, act[k])) continue;
+        const int c0 = __shfl_sync(0xffffffffu, cc[k], 0);
+        if (__all_sync(0xffffffffu, cc[k] == c0)) {
+          for (int o = 16; o > 0; o >>= 1) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+          if ((threadIdx.x & 31) == 0 && c0 >= 0) atomicAdd(&s.mv[c0], t2);
+        } else if (act[k]) {
+          atomicAdd(&s.mv[cc[k]], t2);
+        }
       }
     }
     __syncthreads();

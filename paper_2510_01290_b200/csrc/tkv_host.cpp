@@ -1399,9 +1399,22 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   r->scratch_per_cta = f64_raw ? (int64_t)6 * r->max_m * dm.D : 1;
   r->scratch_ctas = f64_raw ? (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, U)) : 1;
   r->d_scratch = dalloc<double>(r, (size_t)r->scratch_ctas * r->scratch_per_cta);
-  // sums | means row blocks of the m > 32 restart classes (grown per wave in execute_plans)
-  r->km_sums_doubles = (int64_t)2048 * std::max(1, r->max_m - 1) * (2 * dm.D + 1);
-  r->km_sums = dalloc<double>(r, (size_t)r->km_sums_doubles);
+  // K-means scratch sized up front for the largest wave the schedule can
+  // produce (every unit annealing a tau-token segment to the first level,
+  // 4 restarts each), so no timed step pays a synchronising re-allocation;
+  // execute_plans still grows either buffer if a wave exceeds it.
+  {
+    const int kmax = (int)std::min<int64_t>(std::max(1, r->max_m - 1), d.num_levels > 0 ? d.levels[0] : 1);
+    const int64_t items = std::min<int64_t>(U, 16384);
+    r->km_sums_doubles = std::max<int64_t>((int64_t)2048 * std::max(1, r->max_m - 1),
+                                           4 * items * std::max(1, kmax)) * (2 * dm.D + 1);
+    r->km_sums_doubles = std::min<int64_t>(r->km_sums_doubles, (int64_t)2 << 30);
+    r->km_sums = dalloc<double>(r, (size_t)r->km_sums_doubles);
+    if (r->max_m > 8) {
+      r->km_scratch_bytes = tkv_km_instance_bytes(r->max_m, kmax, dm.D, dm.W, 4) * items;
+      CUDA_OK(cudaMalloc(&r->km_scratch, (size_t)r->km_scratch_bytes));
+    }
+  }
   // sequences, and their planning groups: the whole sequence, or one unit
   // per group when labels are per layer (sizes then evolve per layer)
   r->group_units = (d.per_layer_thought && !d.scripted) ? 1 : d.units_per_seq;
