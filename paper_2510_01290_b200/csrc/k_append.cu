@@ -159,9 +159,19 @@ __device__ void tkv_record_placements(uint8_t* fl, uint32_t* ev, uint8_t* ns, in
   }
 }
 
+// Claimed blocks staged in shared memory for the placement bookkeeping (a
+// 16-token window touches at most 16 blocks; more falls back to global memory).
+constexpr int kStageBlocks = 24;
+
 struct FlushSmem {
   int32_t claim[64];
   int8_t reuse[64];
+  int32_t nb;                                   // staged blocks
+  int32_t sb[kStageBlocks];                     // their ids
+  uint8_t fl_t[kStageBlocks], ns_t[kStageBlocks];
+  uint32_t ev_t[kStageBlocks];
+  int32_t st_t[kStageBlocks][TKV_STARTS_PER_BLOCK(32)];
+  uint32_t mk_t[kStageBlocks][TKV_MASKS_PER_BLOCK(32)];
   int32_t win;
   int32_t abort_code;
   int32_t bad;
@@ -330,11 +340,87 @@ __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n
         }
       }
       sm.win = w;
-      if (sm.abort_code == 0) tkv_record_placements(fl, ev, ns, sstart, smask, bs, c.seg_start, n, sm.claim, sm.reuse);
+      // distinct claimed blocks, in first-claim order
+      int nb = 0;
+      for (int i = 0; i < n; ++i) {
+        const int b = sm.claim[i] / bs;
+        int k = 0;
+        while (k < nb && sm.sb[k] != b) ++k;
+        if (k == nb) {
+          if (nb == kStageBlocks) { nb = -1; break; }
+          sm.sb[nb++] = b;
+        }
+      }
+      sm.nb = nb;
+      if (nb < 0) tkv_record_placements(fl, ev, ns, sstart, smask, bs, c.seg_start, n, sm.claim, sm.reuse);
     }
   }
   __syncthreads();
   if (sm.abort_code != 0) return;
+  // Placement bookkeeping (tkv_record_placements, pager.cpp:166-216) on
+  // shared-memory copies of the claimed blocks: the warp stages them, one
+  // thread applies the claims in order, the warp writes them back -- the
+  // serial part no longer waits on dependent global loads.
+  if (sm.nb >= 0) {
+    const int nb = sm.nb, SP = TKV_STARTS_PER_BLOCK(bs), MP = TKV_MASKS_PER_BLOCK(bs);
+    uint8_t* fl = st.blk_filled + (int64_t)u * P;
+    uint32_t* ev = st.blk_evict + (int64_t)u * P;
+    uint8_t* ns = st.blk_nstart + (int64_t)u * P;
+    int32_t* sstart = st.blk_start + (int64_t)u * P * SP;
+    uint32_t* smask = st.blk_segmask + (int64_t)u * P * MP;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      const int b = sm.sb[k];
+      sm.fl_t[k] = fl[b];
+      sm.ev_t[k] = ev[b];
+      sm.ns_t[k] = ns[b];
+    }
+    for (int t = threadIdx.x; t < nb * SP; t += blockDim.x) sm.st_t[t / SP][t % SP] = sstart[(int64_t)sm.sb[t / SP] * SP + t % SP];
+    for (int t = threadIdx.x; t < nb * MP; t += blockDim.x) sm.mk_t[t / MP][t % MP] = smask[(int64_t)sm.sb[t / MP] * MP + t % MP];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < n; ++i) {
+        const int b = sm.claim[i] / bs, sl = sm.claim[i] % bs;
+        int k = 0;
+        while (sm.sb[k] != b) ++k;
+        const uint32_t bit = 1u << sl;
+        int32_t* starts = sm.st_t[k];
+        uint32_t* masks = sm.mk_t[k];
+        int nsb = sm.ns_t[k];
+        if (sm.reuse[i]) {
+          sm.ev_t[k] &= ~bit;
+          for (int q = 0; q + 1 < nsb; ++q) masks[q] &= ~bit;
+        } else {
+          sm.fl_t[k] += 1;
+        }
+        int found = -1;
+        for (int q = 0; q < nsb; ++q)
+          if (starts[q] == c.seg_start) { found = q; break; }
+        if (found < 0) {
+          starts[nsb] = c.seg_start;
+          if (nsb > 0) masks[nsb - 1] = bit;
+          nsb += 1;
+        } else if (found > 0) {
+          masks[found - 1] |= bit;
+        }
+        for (int q = nsb - 2; q >= 0; --q) {
+          if (masks[q] != 0) continue;
+          for (int j = q; j + 1 < nsb - 1; ++j) masks[j] = masks[j + 1];
+          for (int j = q + 1; j + 1 < nsb; ++j) starts[j] = starts[j + 1];
+          nsb -= 1;
+        }
+        sm.ns_t[k] = (uint8_t)nsb;
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+      const int b = sm.sb[k];
+      fl[b] = sm.fl_t[k];
+      ev[b] = sm.ev_t[k];
+      ns[b] = sm.ns_t[k];
+    }
+    for (int t = threadIdx.x; t < nb * SP; t += blockDim.x) sstart[(int64_t)sm.sb[t / SP] * SP + t % SP] = sm.st_t[t / SP][t % SP];
+    for (int t = threadIdx.x; t < nb * MP; t += blockDim.x) smask[(int64_t)sm.sb[t / MP] * MP + t % MP] = sm.mk_t[t / MP][t % MP];
+  }
 
   // ---- phase C: slot payload stores ----------------------------------------
   const int w = sm.win;

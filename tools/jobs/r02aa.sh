@@ -1,0 +1,7 @@
+# K2 placement bookkeeping on staged blocks: parity + bench
+set -x
+TAG=r02aa
+timeout 1800 python -m pytest -x -q -p no:cacheprovider tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_dropin.py > gpurun_out/${TAG}_parity.log 2>&1; echo "parity rc=$?"
+tail -2 gpurun_out/${TAG}_parity.log
+timeout 900 python bench.py --no-cpu > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
+python -c "import json; d=json.load(open('gpurun_out/${TAG}_bench.json')); print(round(d['value']), round(d['tpot_ms'],4), d['breakdown_ms_per_step'], round(d['roofline']['frac'],3), round(d['e2e']['value']))"
