@@ -636,7 +636,7 @@ __device__ void assign_nearest(SM& s, const double* D2, int m, int K) {
 }
 
 template <int NT, int MAXM, typename XT>
-__global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 128 ? (MAXM == 64 ? 6 : 4) : NT == 64 ? 8 : 1)
+__global__ void __launch_bounds__(NT, NT == 256 ? (MAXM == 128 ? 2 : 3) : NT == 128 ? (MAXM == 64 ? 5 : 4) : NT == 64 ? 8 : 1)
     km_restart_kernel(TkvState st, const TkvAnnealOp* __restrict__ ops, int nops,
                                                         const int32_t* __restrict__ rprefix, int nruns, int run0,
                                                         const int32_t* __restrict__ item_prefix, int item0,
@@ -2098,7 +2098,7 @@ cudaError_t tkv_launch_kmeans(const TkvState& st, const TkvAnnealOp* ops, int no
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km_restart_kernel<128, 64, __half>, 128, dyn) !=
             cudaSuccess)
       cudaGetLastError(), nb = 0;
-    mg64 = nb >= 6;
+    mg64 = nb >= 5;
   }
   const size_t smem = tkv_km_restart_smem(mmax, kmax, st.dm.D, x16 ? 2 : 4, mg || mg64);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;  // tau x d beyond the smem design point
