@@ -2,7 +2,7 @@
 set -x
 for tool in memcheck racecheck synccheck; do
   timeout 1500 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 \
-      python tools/sanitize_run.py > gpurun_out/sanitize_$tool.log 2>&1
+      python tools/sanitize_run.py > gpurun_out/r02_sanitize_$tool.log 2>&1
   echo "$tool rc=$?"
-  tail -12 gpurun_out/sanitize_$tool.log
+  tail -12 gpurun_out/r02_sanitize_$tool.log
 done

@@ -75,12 +75,56 @@ def run_gather():
     print("gather: ok", run.stats(), flush=True)
 
 
+def run_graph():
+    """CUDA-graph replay of plain steps (tkv_step_plain / tkv_graph_step_begin),
+    2 layers, final state against the oracle."""
+    import torch
+    from harness import oracle_config
+    from paper_2510_01290_b200 import DecodeRun
+    cfg = CONFIGS["smoke"]
+    L, S, H, G, D = 2, 1, 1, 4, 128
+    run = DecodeRun(cfg)
+    orc = O.OracleRun(oracle_config(cfg))
+    dev = torch.device("cuda:0")
+    qs = [torch.empty((S, H, G, D), dtype=torch.bfloat16, device=dev) for _ in range(L)]
+    ks = [torch.empty((S, H, D), dtype=torch.bfloat16, device=dev) for _ in range(L)]
+    vs = [torch.empty((S, H, D), dtype=torch.bfloat16, device=dev) for _ in range(L)]
+    os_ = [torch.empty((S, H, G, D), dtype=torch.float32, device=dev) for _ in range(L)]
+    stream, graph, replays = torch.cuda.Stream(), None, 0
+    with torch.cuda.stream(stream):
+        for t in range(cfg.max_gen_len):
+            q, k, v = synth_inputs(cfg, 0x71534B56, t)
+            orc.step(O.bf16_to_f64(q), O.bf16_to_f64(k), O.bf16_to_f64(v))
+            tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev) for x in (q, k, v))
+            for l in range(L):
+                qs[l].copy_(tq.view(S, L, H, G, D)[:, l])
+                ks[l].copy_(tk.view(S, L, H, D)[:, l])
+                vs[l].copy_(tv.view(S, L, H, D)[:, l])
+            if run.step_plain():
+                if graph is None:
+                    graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(graph):
+                        for l in range(L):
+                            run.step_layer(l, L, qs[l], ks[l], vs[l], os_[l])
+                run.graph_step_begin()
+                graph.replay()
+                replays += 1
+            else:
+                for l in range(L):
+                    run.step_layer(l, L, qs[l], ks[l], vs[l], os_[l])
+    torch.cuda.synchronize()
+    compare_state({"run": run, "oracle": orc}, cfg)
+    print(f"graph: ok ({replays} replayed steps of {cfg.max_gen_len})", flush=True)
+
+
 if __name__ == "__main__":
-    names = sys.argv[1:] or ["smoke", "tau128", "d64", "f32raw", "tiny", "gather"]
+    names = sys.argv[1:] or ["smoke", "tau128", "d64", "f32raw", "tiny", "gather", "graph"]
     for n in names:
         if n == "tiny":
             run_tiny()
         elif n == "gather":
             run_gather()
+        elif n == "graph":
+            run_graph()
         else:
             run_config(n)
