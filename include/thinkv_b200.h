@@ -132,25 +132,30 @@ int tkv_step_host(tkv_run* run, const void* q, const void* k, const void* v, flo
  * tkv_synchronize returns (use page-locked host memory for overlap). */
 int tkv_step_host_async(tkv_run* run, const void* q, const void* k, const void* v, float* out);
 
-/* CUDA-graph replay of plain steps (the real-model caller).
- * A *plain* step is one whose only device work is the attention (K1, which
- * also buffers the incoming token): no refresh boundary, no emission, no
- * Case-2 anneal, no dump, no sparsity trace, no byte accounting.  Between
- * emissions (g - 1 of every g decode steps) most steps are plain.
+/* CUDA-graph replay of plain and emission steps (the
+ * real-model caller).  Two step kinds are capturable: 1 = *plain* (the only
+ * device work is the attention, K1, which also buffers the incoming token)
+ * and 2 = *emission* (K1, then K2 quantising the full g-token window into
+ * reclaimed slots).  Neither may hold a refresh boundary, a Case-2 anneal, a
+ * dump, a sparsity trace or byte accounting.  At g = 16, 15 of every 16
+ * decode steps are plain and the 16th an emission, except at boundaries.
  *
  * Capture: while `stream` is capturing (cudaStreamBeginCapture), tkv_step /
- * tkv_step_layer RECORD the step's K1 launches on `stream` and leave the run
+ * tkv_step_layer RECORD the next step's launches on `stream` (K1 per call,
+ * and K2 after the last layer of an emission step) and leave the run
  * unchanged; the recorded launches read the per-step scalars (buffer half,
- * buffered tokens, put slot) from device memory, so a graph holding one
- * model decode step (projections, tkv_step_layer for every layer, ...) can be
- * replayed for every plain step.
+ * buffered tokens, put slot, window position) and K2's per-sequence controls
+ * from device memory, so one graph per kind holding a model decode step
+ * (projections, tkv_step_layer for every layer, ...) can be replayed for
+ * every step of that kind.
  * Replay: call tkv_graph_step_begin(run, stream) before each
- * cudaGraphLaunch(exec, stream).  It fails with TKV_ERR_CONFIG unless
- * tkv_step_plain(run) == 1, stages the step's scalars (stream-ordered on
- * `stream`) and advances the run's host state by one step exactly as the
- * eager step would.  Non-plain steps run eagerly (tkv_step / tkv_step_layer
- * with the same stream).
- * tkv_step_plain: 1 if the next step is plain, 0 if not, < 0 on error. */
+ * cudaGraphLaunch(exec, stream) of the graph of kind tkv_step_plain(run).
+ * It fails with TKV_ERR_CONFIG unless that kind is 1 or 2 and was captured,
+ * stages the step's scalars (stream-ordered on `stream`) and advances the
+ * run's host state by one step exactly as the eager step would.  Other steps
+ * run eagerly (tkv_step / tkv_step_layer with the same stream).
+ * tkv_step_plain: the next step's kind (1 plain, 2 emission, 0 neither),
+ * < 0 on error. */
 int tkv_step_plain(tkv_run* run);
 int tkv_graph_step_begin(tkv_run* run, void* stream);
 

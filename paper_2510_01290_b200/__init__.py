@@ -164,19 +164,25 @@ class DecodeRun:
         check(lib.tkv_step_layer(self._h, layer, num_layers, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                  out.data_ptr(), s))
 
-    def step_plain(self) -> bool:
-        """True if the next step's only device work is the attention kernel
-        (tkv_step_plain): it may be replayed from a captured CUDA graph."""
+    def step_kind(self) -> int:
+        """The next step's capturable kind (tkv_step_plain): 1 plain (only the
+        attention kernel), 2 emission (attention + the window's quantisation),
+        0 neither (boundary / eviction: step eagerly).  Keep one captured CUDA
+        graph per kind."""
         r = lib.tkv_step_plain(self._h)
         if r < 0:
             check(-r)
-        return r == 1
+        return r
+
+    def step_plain(self) -> bool:
+        return self.step_kind() == 1
 
     def graph_step_begin(self, stream=None):
-        """Before each replay of a captured step on `stream`
-        (tkv_graph_step_begin): stages the step's scalars and advances the
-        run by one plain step.  Under stream capture, step()/step_layer()
-        record their launches instead of executing them."""
+        """Before each replay of the captured graph of kind step_kind() on
+        `stream` (tkv_graph_step_begin): stages the step's scalars and
+        advances the run by one step.  Under stream capture, step() /
+        step_layer() record the next step's launches instead of executing
+        them."""
         check(lib.tkv_graph_step_begin(self._h, self._stream(stream)))
 
     def step_host(self, q, k, v, out):

@@ -182,6 +182,7 @@ struct FlushSmem {
 __global__ void __launch_bounds__(128) flush_kernel(TkvState st, int half, int n, int pos0,
                                                     const TkvFlushCtl* __restrict__ ctl,
                                                     int units_per_group) {
+  tkv_flush_scalars(st, half, pos0);
   const TkvDims& dm = st.dm;
   const int u = blockIdx.x;
   if (u >= dm.U) return;

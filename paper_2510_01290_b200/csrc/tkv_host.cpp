@@ -239,13 +239,18 @@ struct tkv_run {
   // put_half, put_slot} from d_stepdesc, staged per replayed step through a
   // pinned ring on the caller's stream.
   static constexpr int kDescRing = 64;
+  static constexpr int kDescInts = 8;  // K1: buf_half, nbuf, put_half, put_slot; K2: half, pos0
   int32_t* d_stepdesc = nullptr;
-  int32_t* h_stepdesc = nullptr;  // pinned [kDescRing][4]
+  int32_t* h_stepdesc = nullptr;  // pinned [kDescRing][kDescInts]
+  TkvFlushCtl* d_ctl_graph = nullptr;  // K2's per-group controls for replayed emission steps
+  TkvFlushCtl* h_ctl_ring = nullptr;   // pinned [kDescRing][groups]
+  bool replaying = false;              // step_end of a replayed step: host bookkeeping only
   cudaEvent_t desc_ev[kDescRing]{};
   int desc_next = 0;
   int cap_next_layer = 0, cap_layers = 0;
-  int64_t cap_launches = 0;    // K1 launches recorded by the capture in progress
-  int64_t graph_launches = 0;  // ... by the last completed capture (per replayed step)
+  int cap_kind = 0;            // kind of step being captured (1 plain, 2 emission)
+  int64_t cap_launches = 0;    // launches recorded by the capture in progress
+  int64_t graph_launches[3] = {0, 0, 0};  // ... by the last completed capture of each kind
   int64_t graph_steps = 0;     // steps advanced by tkv_graph_step_begin
   std::vector<void*> allocations;
 };
@@ -646,19 +651,25 @@ void execute_plans(tkv_run* r, std::vector<GroupPlan>& plans, int64_t step) {
 // -------------------------------------------------------------------------
 // emission (flush_layer, sim.cpp:565-650) for every unit
 // -------------------------------------------------------------------------
-void flush_all(tkv_run* r, int64_t step) {
-  if (r->buf_len <= 0) return;
-  std::vector<TkvFlushCtl> ctl(r->groups.size());
+void flush_ctl(const tkv_run* r, TkvFlushCtl* ctl) {
   for (size_t gi = 0; gi < r->groups.size(); ++gi) {
     const Group& g = r->groups[gi];
     const HSeg& s = g.segs[g.open];
     ctl[gi].band = s.band;
     ctl[gi].seg_start = (int32_t)s.start;
   }
-  TkvFlushCtl* d_ctl = upload(r, ctl.data(), ctl.size());
-  launch(r, CAT_FLUSH, "flush kernel", [&] {
-    return tkv_launch_flush(r->st, r->cur_half, r->buf_len, (int)r->buf_pos0, d_ctl, r->group_units, r->stream);
-  });
+}
+
+void flush_all(tkv_run* r, int64_t step) {
+  if (r->buf_len <= 0) return;
+  if (!r->replaying) {  // (a replayed emission step's K2 is in the graph)
+    std::vector<TkvFlushCtl> ctl(r->groups.size());
+    flush_ctl(r, ctl.data());
+    TkvFlushCtl* d_ctl = upload(r, ctl.data(), ctl.size());
+    launch(r, CAT_FLUSH, "flush kernel", [&] {
+      return tkv_launch_flush(r->st, r->cur_half, r->buf_len, (int)r->buf_pos0, d_ctl, r->group_units, r->stream);
+    });
+  }
   if (r->desc.record_events) {
     for (size_t gi = 0; gi < r->groups.size(); ++gi) {
       Group& g = r->groups[gi];
@@ -1182,28 +1193,31 @@ void do_step(tkv_run* r, const void* q, const void* k, const void* v, float* out
   step_end(r, c);
 }
 
-// ---- CUDA-graph replay of plain steps -------------------------
-// A plain step's only device work is K1 (which also buffers the incoming
-// token): no refresh boundary, no emission, no Case-2 anneal, no dump, no
-// sparsity trace, no byte accounting.  Decided with the size arithmetic the
-// step itself runs (plan_overflow on a copy of each over-budget group).
-bool next_step_plain(const tkv_run* r) {
+// ---- CUDA-graph replay of plain and emission steps ------------
+// Capturable step kinds: 1 = plain (the only device work is K1, which also
+// buffers the incoming token), 2 = emission (K1, then K2 flushing the full
+// window).  Neither may hold a refresh boundary, a Case-2 anneal, a dump, a
+// sparsity trace or byte accounting; decided with the size arithmetic the
+// step itself runs (plan_overflow on a copy of each over-budget group; an
+// emission moves tokens from the buffer into the pager without changing
+// segment sizes).  0 = step eagerly.
+int next_step_kind(const tkv_run* r) {
   const tkv_run_desc& d = r->desc;
-  if (r->finished || r->pos >= r->total_steps || r->next_layer != 0) return false;
+  if (r->finished || r->pos >= r->total_steps || r->next_layer != 0) return 0;
   const bool decode = r->pos >= d.prompt_len;
   const int64_t bstep = decode ? r->pos - d.prompt_len : r->pos;
-  if (bstep % d.tau == 0 || r->buf_len + 1 >= d.group_size) return false;
-  if (r->dump_at.count(r->pos) || (decode && d.record_sparsity_trace) || r->bytes_on) return false;
+  if (bstep % d.tau == 0 || r->buf_len + 1 > d.group_size) return 0;
+  if (r->dump_at.count(r->pos) || (decode && d.record_sparsity_trace) || r->bytes_on) return 0;
   for (const Group& g : r->groups) {
-    if (g.open < 0) return false;
+    if (g.open < 0) return 0;
     if (g.total + 1 <= d.budget) continue;
     Group c = g;  // the step buffers one token under the open segment, then enforces the budget
     c.segs[c.open].size += 1;
     c.segs[c.open].initial += 1;
     c.total += 1;
-    if (!plan_overflow(r, c, 0).ops.empty()) return false;
+    if (!plan_overflow(r, c, 0).ops.empty()) return 0;
   }
-  return true;
+  return r->buf_len + 1 == d.group_size ? 2 : 1;
 }
 
 bool capturing(cudaStream_t s) {
@@ -1213,14 +1227,19 @@ bool capturing(cudaStream_t s) {
   return cs == cudaStreamCaptureStatusActive;
 }
 
-// Record one K1 launch on the capturing stream.  The per-step scalars come
-// from d_stepdesc at replay time and the live lists are sized for the whole
-// pool, so the one launch is valid for every plain step it is replayed for.
-void capture_attend(tkv_run* r, cudaStream_t s, const void* q, const void* k, const void* v, float* out,
-                    int lmap_h, int layer) {
+TkvState replay_state(const tkv_run* r) {
   TkvState st = r->st;
   st.step_dev = r->d_stepdesc;
   st.max_live = st.dm.NS;
+  return st;
+}
+
+// Record one K1 launch on the capturing stream.  The per-step scalars come
+// from d_stepdesc at replay time and the live lists are sized for the whole
+// pool, so the one launch is valid for every step it is replayed for.
+void capture_attend(tkv_run* r, cudaStream_t s, const void* q, const void* k, const void* v, float* out,
+                    int lmap_h, int layer) {
+  TkvState st = replay_state(r);
   st.lmap_h = lmap_h;
   st.lmap_ups = r->desc.units_per_seq;
   st.lmap_off = layer * lmap_h;
@@ -1234,43 +1253,69 @@ void capture_layer(tkv_run* r, cudaStream_t s, int layer, int num_layers, const 
   if (layer != r->cap_next_layer || (layer > 0 && num_layers != r->cap_layers))
     throw TkvError(TKV_ERR_CONFIG, "captured layers of a step must be recorded in order 0 .. num_layers-1");
   if (layer == 0) {
+    r->cap_kind = next_step_kind(r);
+    if (r->cap_kind == 0)
+      throw TkvError(TKV_ERR_CONFIG, "the next step cannot be captured (boundary or eviction): step it eagerly");
     r->cap_layers = num_layers;
     r->cap_launches = 0;
   }
   capture_attend(r, s, q, k, v, out, num_layers ? r->desc.units_per_seq / num_layers : 0, layer);
   if (layer == num_layers - 1 || num_layers == 0) {
+    if (r->cap_kind == 2) {  // the emission: K2 over the full window, controls staged per replay
+      check_launch(tkv_launch_flush(replay_state(r), 0, r->desc.group_size, 0, r->d_ctl_graph, r->group_units, s),
+                   "flush kernel (capture)");
+      r->cap_launches += 1;
+    }
     r->cap_next_layer = 0;
-    r->graph_launches = r->cap_launches;
+    r->graph_launches[r->cap_kind] = r->cap_launches;
   } else {
     r->cap_next_layer = layer + 1;
   }
 }
 
 // Before each replay of a captured step on `s`: stage this step's scalars
-// (stream-ordered on s, after the previous replay read them) and advance the
-// run's host state exactly as the eager step would.
+// (and, for an emission, K2's per-group controls), stream-ordered on s after
+// the previous replay read them, and advance the run's host state exactly as
+// the eager step would.
 void graph_step_begin(tkv_run* r, cudaStream_t s) {
-  if (r->graph_launches == 0) throw TkvError(TKV_ERR_CONFIG, "no captured step (record one under stream capture)");
-  if (!next_step_plain(r))
-    throw TkvError(TKV_ERR_CONFIG, "the next step is not plain (boundary, emission or eviction): step it eagerly");
+  const int kind = next_step_kind(r);
+  if (kind == 0)
+    throw TkvError(TKV_ERR_CONFIG, "the next step cannot be replayed (boundary or eviction): step it eagerly");
+  if (r->graph_launches[kind] == 0)
+    throw TkvError(TKV_ERR_CONFIG, kind == 1 ? "no captured plain step (record one under stream capture)"
+                                             : "no captured emission step (record one under stream capture)");
   const StepCtx c = step_begin(r);
   const int slot = r->desc_next;
   r->desc_next = (slot + 1) % tkv_run::kDescRing;
   CUDA_OK(cudaEventSynchronize(r->desc_ev[slot]));
-  int32_t* h = r->h_stepdesc + 4 * slot;
+  int32_t* h = r->h_stepdesc + tkv_run::kDescInts * slot;
   h[0] = r->cur_half;
   h[1] = r->buf_len;
   h[2] = c.put_half;
   h[3] = c.put_slot;
+  h[4] = r->cur_half;                             // K2: the buffer half the window fills
+  h[5] = (int)(r->buf_len == 0 ? c.pos : r->buf_pos0);  // K2: position of the window's first token
   // order the replay after the run's own stream (eager steps), then stage
   cudaEvent_t ev = pool_event(r);
   CUDA_OK(cudaEventRecord(ev, r->stream));
   CUDA_OK(cudaStreamWaitEvent(s, ev, 0));
   r->ev_pool.push_back(ev);
-  CUDA_OK(cudaMemcpyAsync(r->d_stepdesc, h, 4 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpyAsync(r->d_stepdesc, h, tkv_run::kDescInts * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (kind == 2) {
+    TkvFlushCtl* hc = r->h_ctl_ring + (size_t)slot * r->groups.size();
+    flush_ctl(r, hc);
+    CUDA_OK(cudaMemcpyAsync(r->d_ctl_graph, hc, r->groups.size() * sizeof(TkvFlushCtl), cudaMemcpyHostToDevice, s));
+  }
   CUDA_OK(cudaEventRecord(r->desc_ev[slot], s));
-  r->launches += r->graph_launches;
-  step_end(r, c);
+  r->launches += r->graph_launches[kind];
+  r->replaying = true;
+  try {
+    step_end(r, c);
+  } catch (...) {
+    r->replaying = false;
+    throw;
+  }
+  r->replaying = false;
   r->graph_steps += 1;
 }
 
@@ -1379,8 +1424,8 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
   // arenas
   r->arena_cap = 8 << 20;
   r->d_arena = dalloc<uint8_t>(r, r->arena_cap);
-  r->d_stepdesc = dalloc<int32_t>(r, 4, 0);
-  CUDA_OK(cudaMallocHost(&r->h_stepdesc, sizeof(int32_t) * 4 * tkv_run::kDescRing));
+  r->d_stepdesc = dalloc<int32_t>(r, tkv_run::kDescInts, 0);
+  CUDA_OK(cudaMallocHost(&r->h_stepdesc, sizeof(int32_t) * tkv_run::kDescInts * tkv_run::kDescRing));
   for (int i = 0; i < tkv_run::kDescRing; ++i) CUDA_OK(cudaEventCreateWithFlags(&r->desc_ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
     CUDA_OK(cudaMallocHost(&r->h_pinned[i], r->arena_cap));
@@ -1433,6 +1478,8 @@ void create_run(tkv_ctx* ctx, const tkv_run_desc* desc, tkv_run* r) {
     }
     r->seqs.push_back(std::move(q));
   }
+  r->d_ctl_graph = dalloc<TkvFlushCtl>(r, r->groups.size());
+  CUDA_OK(cudaMallocHost(&r->h_ctl_ring, sizeof(TkvFlushCtl) * r->groups.size() * tkv_run::kDescRing));
   CUDA_OK(cudaStreamSynchronize(r->stream));
 }
 
@@ -1456,6 +1503,7 @@ void destroy_run(tkv_run* r) {
     for (int i = 0; i < tkv_run::kDescRing; ++i) cudaEventSynchronize(r->desc_ev[i]);
     cudaFreeHost(r->h_stepdesc);
   }
+  if (r->h_ctl_ring) cudaFreeHost(r->h_ctl_ring);
   for (int i = 0; i < tkv_run::kDescRing; ++i)
     if (r->desc_ev[i]) cudaEventDestroy(r->desc_ev[i]);
   for (auto& t : r->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
@@ -1716,7 +1764,7 @@ int tkv_step_host_async(tkv_run* run, const void* q, const void* k, const void* 
 int tkv_step_plain(tkv_run* run) {
   try {
     if (!run) throw TkvError(TKV_ERR_CONFIG, "null run");
-    return next_step_plain(run) ? 1 : 0;
+    return next_step_kind(run);
   } catch (const TkvError& e) {
     return -fail(e);
   }

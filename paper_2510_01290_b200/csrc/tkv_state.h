@@ -104,12 +104,25 @@ struct TkvState {
   // launch covers i in [0, num_seqs * lmap_h) and
   // u = (i / lmap_h) * lmap_ups + lmap_off + i % lmap_h.  lmap_h == 0: u = i.
   int32_t lmap_h, lmap_ups, lmap_off, lmap_count;
-  // Per-step scalars in device memory (CUDA-graph replay of plain steps,
-  // tkv_graph_step_begin): when non-null, K1 reads {buf_half, nbuf, put_half,
-  // put_slot} from here instead of its launch parameters, so one captured
-  // launch serves every replayed step.  Null on eager launches.
+  // Per-step scalars in device memory (CUDA-graph replay of plain and
+  // emission steps, tkv_graph_step_begin): when non-null, K1 reads
+  // {buf_half, nbuf, put_half, put_slot} = step_dev[0..3] and K2 its
+  // {half, pos0} = step_dev[4..5] instead of their launch parameters, so one
+  // captured launch serves every replayed step.  Null on eager launches.
   const int32_t* step_dev;
 };
+
+// K2's per-step scalars: launch parameters, or the device copy (graph replay).
+__host__ __device__ inline void tkv_flush_scalars(const TkvState& st, int& half, int& pos0) {
+#ifdef __CUDA_ARCH__
+  if (st.step_dev) {
+    half = st.step_dev[4];
+    pos0 = st.step_dev[5];
+  }
+#else
+  (void)st; (void)half; (void)pos0;
+#endif
+}
 
 // K1's per-step scalars: launch parameters, or the device copy (graph replay).
 __host__ __device__ inline void tkv_step_scalars(const TkvState& st, int& buf_half, int& nbuf, int& put_half,

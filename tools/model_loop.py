@@ -11,8 +11,8 @@ Keys arrive post-RoPE in the reference (apply_rotary is outside the path), so
 no rotary is applied.  The decode context is built with the synthetic inputs
 (tkv_synth_inputs, the bench's own path) up to --ctx, then the model drives
 the run: K steps eagerly (every launch from Python), then K steps where each
-plain step replays one CUDA graph of the whole model step
-(tkv_graph_step_begin + graph.replay()) and boundary / emission / eviction
+plain or emission step replays the CUDA graph of its kind holding the whole
+model step (tkv_graph_step_begin + graph.replay()) and boundary / eviction
 steps run eagerly.  Both windows open on a refresh boundary and span whole
 tau periods.  Prints one JSON line.
 
@@ -46,7 +46,7 @@ def main():
 
     S, L, H, G, D, HID = args.seqs, args.layers, 8, 4, 128, 4096
     tau = 128
-    max_gen = args.ctx + 2 * (args.steps + args.warmup + tau) + 16
+    max_gen = args.ctx + 2 * (args.steps + args.warmup + 16 + tau) + 16
     cfg = ThinkvConfig(num_seqs=S, units_per_seq=L * H, num_q_heads=G, head_dim=D, tau=tau, group_size=16,
                        block_size=16, budget=1024, levels=(64, 32, 16, 8, 4), psi_bits=(4, 4, 2),
                        max_gen_len=max_gen, script=band_script(SEED, S, max_gen // tau + 2, 3, 100))
@@ -103,13 +103,15 @@ def main():
                 h.add_(torch.matmul(torch.nn.functional.silu(y @ Wg[l]) * (y @ Wu[l]), Wd[l]))
 
     stream = torch.cuda.Stream()
-    graph = None
+    graphs = {}  # one per capturable step kind (1 plain, 2 emission)
     res = {}
     with torch.cuda.stream(stream):
         for mode in ("eager", "graph"):
             pos0 = run.position
-            # align the window to a refresh boundary (warmup steps before it)
-            lead = (-(pos0 + args.warmup)) % tau + args.warmup
+            # align the window to a refresh boundary; the warmup before it
+            # holds at least one emission, so both graphs are captured untimed
+            pre = args.warmup + 16
+            lead = (-(pos0 + pre)) % tau + pre
             replays = eager = 0
             for i in range(lead + args.steps):
                 if i == lead:
@@ -119,13 +121,14 @@ def main():
                     ev0.record(stream)
                     h0 = time.perf_counter()
                 h.copy_(emb[(run.position) % 64])
-                if mode == "graph" and run.step_plain():
-                    if graph is None:
-                        graph = torch.cuda.CUDAGraph()
-                        with torch.cuda.graph(graph):
+                kind = run.step_kind() if mode == "graph" else 0
+                if kind:
+                    if kind not in graphs:
+                        graphs[kind] = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(graphs[kind]):
                             model_step()
                     run.graph_step_begin()
-                    graph.replay()
+                    graphs[kind].replay()
                     replays += i >= lead
                 else:
                     model_step()
@@ -142,7 +145,7 @@ def main():
                          "graph_replayed_steps": replays, "eager_steps": eager,
                          "tkv_launches": tm["total_launches"]}
     line = {"what": "R1-Distill-Llama-8B-shaped bf16 decoder (random weights) with ThinKV attention via "
-                    "tkv_step_layer; eager vs CUDA-graph replay of plain steps",
+                    "tkv_step_layer; eager vs CUDA-graph replay of plain and emission steps",
             "seqs": S, "layers": L, "mlp": args.mlp, "context_build_s": ctx_s, **res,
             "graph_speedup": res["eager"]["ms_per_step"] / res["graph"]["ms_per_step"]}
     print(json.dumps(line), flush=True)

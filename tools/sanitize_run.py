@@ -90,7 +90,7 @@ def run_graph():
     ks = [torch.empty((S, H, D), dtype=torch.bfloat16, device=dev) for _ in range(L)]
     vs = [torch.empty((S, H, D), dtype=torch.bfloat16, device=dev) for _ in range(L)]
     os_ = [torch.empty((S, H, G, D), dtype=torch.float32, device=dev) for _ in range(L)]
-    stream, graph, replays = torch.cuda.Stream(), None, 0
+    stream, graphs, replays = torch.cuda.Stream(), {}, 0
     with torch.cuda.stream(stream):
         for t in range(cfg.max_gen_len):
             q, k, v = synth_inputs(cfg, 0x71534B56, t)
@@ -100,14 +100,15 @@ def run_graph():
                 qs[l].copy_(tq.view(S, L, H, G, D)[:, l])
                 ks[l].copy_(tk.view(S, L, H, D)[:, l])
                 vs[l].copy_(tv.view(S, L, H, D)[:, l])
-            if run.step_plain():
-                if graph is None:
-                    graph = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(graph):
+            kind = run.step_kind()
+            if kind:
+                if kind not in graphs:
+                    graphs[kind] = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(graphs[kind]):
                         for l in range(L):
                             run.step_layer(l, L, qs[l], ks[l], vs[l], os_[l])
                 run.graph_step_begin()
-                graph.replay()
+                graphs[kind].replay()
                 replays += 1
             else:
                 for l in range(L):
