@@ -733,12 +733,17 @@ __device__ __forceinline__ void load_wins4(const UnitPtrs& up, const uint16_t* l
   }
 }
 
-template <int D, int FMT>
+template <int D, int FMT, int KS>
 __device__ __forceinline__ void load_tile4(const UnitPtrs& up, const Bases<D, FMT>& B, const uint16_t* lst, int t0,
                                            int gid, int tig, const uint32_t (&wk)[2], const uint32_t (&wv)[4],
                                            Tile<D, FMT>& T) {
   using Gm = Geo<D, FMT>;
-  const uint32_t ks = (uint32_t)up.kstride;
+  // KS > 0: the slot-row stride is a compile-time constant (and the value
+  // chunks per slot D / 16), so each row address is one IMAD.WIDE.U32 with an
+  // immediate; a runtime stride makes ptxas split it into a product plus a
+  // 64-bit add (three instructions per load address).
+  const uint32_t ks = KS > 0 ? (uint32_t)KS : (uint32_t)up.kstride;
+  const uint32_t vc = KS > 0 ? (uint32_t)(D / 16) : (uint32_t)up.vchunks;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const uint32_t e = lst[t0 + gid + 8 * r];
@@ -771,7 +776,7 @@ __device__ __forceinline__ void load_tile4(const UnitPtrs& up, const Bases<D, FM
       T.v[i].w[0] = Gm::VBYTES == 2 ? (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(vr)) : (uint32_t)__ldg(vr);
     }
     if constexpr (FMT == TKV_FMT_FP8) T.vf[i] = __ldg(reinterpret_cast<const float*>(wide_at(up.vf, wv[i], 4)));
-    if constexpr (Gm::SCALED) T.vs[i] = __ldg(wide_at(B.vs, e, (uint32_t)up.vchunks));
+    if constexpr (Gm::SCALED) T.vs[i] = __ldg(wide_at(B.vs, e, vc));
   }
 }
 
@@ -962,7 +967,7 @@ __device__ __forceinline__ void compute_tile4(const Tile<D, FMT>& T, const uint3
   }
 }
 
-template <int D, int FMT, bool PVN>
+template <int D, int FMT, bool PVN, int KS>
 __device__ __forceinline__ void run_format4(const UnitPtrs& up, const uint16_t* lst, int n,
                                             const uint32_t (&qb)[D / 16][2], const uint32_t* qbb, float qscale,
                                             bool maxpool, int gid, int tig, float* ps, Acc<D>& A) {
@@ -973,7 +978,7 @@ __device__ __forceinline__ void run_format4(const UnitPtrs& up, const uint16_t* 
     uint32_t wk[2] = {0, 0}, wv[4] = {0, 0, 0, 0};
     for (int t = 0; t < tiles; ++t) {
       Tile<D, FMT> cur;
-      load_tile4<D, FMT>(up, B, lst, t * 16, gid, tig, wk, wv, cur);
+      load_tile4<D, FMT, KS>(up, B, lst, t * 16, gid, tig, wk, wv, cur);
       compute_tile4<D, FMT, PVN>(cur, qb, qbb, qscale, maxpool, n - t * 16, gid, tig, ps, A);
     }
     return;
@@ -981,20 +986,20 @@ __device__ __forceinline__ void run_format4(const UnitPtrs& up, const uint16_t* 
   uint32_t wk0[2] = {0, 0}, wv0[4] = {0, 0, 0, 0}, wk1[2] = {0, 0}, wv1[4] = {0, 0, 0, 0};
   Tile<D, FMT> ta, tb;
   load_wins4<D, FMT>(up, lst, 0, gid, tig, wk0, wv0);
-  load_tile4<D, FMT>(up, B, lst, 0, gid, tig, wk0, wv0, ta);
+  load_tile4<D, FMT, KS>(up, B, lst, 0, gid, tig, wk0, wv0, ta);
   if (tiles > 1) load_wins4<D, FMT>(up, lst, 16, gid, tig, wk1, wv1);
   int t = 0;
   while (true) {
     // ta holds tile t; wk1 the windows of tile t + 1
     if (t + 1 < tiles) {
-      load_tile4<D, FMT>(up, B, lst, (t + 1) * 16, gid, tig, wk1, wv1, tb);
+      load_tile4<D, FMT, KS>(up, B, lst, (t + 1) * 16, gid, tig, wk1, wv1, tb);
       if (t + 2 < tiles) load_wins4<D, FMT>(up, lst, (t + 2) * 16, gid, tig, wk0, wv0);
     }
     compute_tile4<D, FMT, PVN>(ta, qb, qbb, qscale, maxpool, n - t * 16, gid, tig, ps, A);
     if (++t >= tiles) break;
     // tb holds tile t; wk0 the windows of tile t + 1
     if (t + 1 < tiles) {
-      load_tile4<D, FMT>(up, B, lst, (t + 1) * 16, gid, tig, wk0, wv0, ta);
+      load_tile4<D, FMT, KS>(up, B, lst, (t + 1) * 16, gid, tig, wk0, wv0, ta);
       if (t + 2 < tiles) load_wins4<D, FMT>(up, lst, (t + 2) * 16, gid, tig, wk1, wv1);
     }
     compute_tile4<D, FMT, PVN>(tb, qb, qbb, qscale, maxpool, n - t * 16, gid, tig, ps, A);
@@ -1016,7 +1021,7 @@ struct WarpSmem {
 // share one PV mma (compute_tile4).  Without max-pool the q^T operand's
 // columns 4..7 repeat heads 0..3, so the lanes holding the lo columns see their
 // head's own logits and track the same running max and denominator.
-template <int D, int MINB, bool PVN>
+template <int D, int MINB, bool PVN, int KS>
 __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st, const void* __restrict__ qin,
                                                                     const void* __restrict__ kin,
                                                                     const void* __restrict__ vin,
@@ -1145,13 +1150,13 @@ __global__ void __launch_bounds__(kThreads, MINB) attend_warp_kernel(TkvState st
   A.m[0] = A.m[1] = -CUDART_INF_F;
   A.l[0] = A.l[1] = 0.f;
   const bool mp = dm.maxpool != 0;
-  run_format4<D, TKV_FMT_NVFP4, PVN>(up, list + off[TKV_FMT_NVFP4], cnt[TKV_FMT_NVFP4], qb, qbb, qscale, mp, gid, tig,
+  run_format4<D, TKV_FMT_NVFP4, PVN, KS>(up, list + off[TKV_FMT_NVFP4], cnt[TKV_FMT_NVFP4], qb, qbb, qscale, mp, gid, tig,
                                      ps, A);
-  run_format4<D, TKV_FMT_TERNARY, PVN>(up, list + off[TKV_FMT_TERNARY], cnt[TKV_FMT_TERNARY], qb, qbb, qscale, mp,
+  run_format4<D, TKV_FMT_TERNARY, PVN, KS>(up, list + off[TKV_FMT_TERNARY], cnt[TKV_FMT_TERNARY], qb, qbb, qscale, mp,
                                        gid, tig, ps, A);
-  run_format4<D, TKV_FMT_FP8, PVN>(up, list + off[TKV_FMT_FP8], cnt[TKV_FMT_FP8], qb, qbb, qscale, mp, gid, tig, ps,
+  run_format4<D, TKV_FMT_FP8, PVN, KS>(up, list + off[TKV_FMT_FP8], cnt[TKV_FMT_FP8], qb, qbb, qscale, mp, gid, tig, ps,
                                    A);
-  run_format4<D, kFmtTail, PVN>(up, list + off[TKV_FMT_RAW], cnt[TKV_FMT_RAW], qb, qbb, qscale, mp, gid, tig, ps, A);
+  run_format4<D, kFmtTail, PVN, KS>(up, list + off[TKV_FMT_RAW], cnt[TKV_FMT_RAW], qb, qbb, qscale, mp, gid, tig, ps, A);
   // ---- epilogue: heads tig*2 + cc, channels gid*D/8 + 2mt (+1) ------------------
   // denominators: each lane summed its own tokens; reduce over the 8 token lanes
 #pragma unroll
@@ -1212,16 +1217,16 @@ cudaError_t launch_k1(const TkvState& st, const void* q, const void* k, const vo
   return cudaGetLastError();
 }
 
-template <int D, int MINB, bool PVN>
+template <int D, int MINB, bool PVN, int KS>
 cudaError_t launch_k1_warp(const TkvState& st, const void* q, const void* k, const void* v, float* out, int buf_half,
                            int nbuf, int put_half, int put_slot, cudaStream_t s) {
   const size_t smem = (size_t)kWarps * WarpSmem<D>::bytes(st.max_live, st.dm.g, st.dm.P);
   static bool cfg = false;
   if (!cfg) {
-    cudaFuncSetAttribute(attend_warp_kernel<D, MINB, PVN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(attend_warp_kernel<D, MINB, PVN, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cfg = true;
   }
-  attend_warp_kernel<D, MINB, PVN><<<(tkv_launch_units(st) + kWarps - 1) / kWarps, kThreads, smem, s>>>(
+  attend_warp_kernel<D, MINB, PVN, KS><<<(tkv_launch_units(st) + kWarps - 1) / kWarps, kThreads, smem, s>>>(
       st, q, k, v, out, buf_half, nbuf, put_half, put_slot);
   return cudaGetLastError();
 }
@@ -1237,12 +1242,18 @@ cudaError_t tkv_launch_attend_mma(const TkvState& st, const void* q, const void*
                   getenv("TKV_K1_V2") == nullptr;
   if (v3) {
     const bool pvn = st.dm.maxpool || st.dm.G <= 4;
-    if (D == 128) {
-      if (pvn) return launch_k1_warp<128, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
-      return launch_k1_warp<128, 3, false>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
-    }
-    if (pvn) return launch_k1_warp<64, 3, true>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
-    return launch_k1_warp<64, 3, false>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s);
+    // 4-bit widest band with 16-channel value groups (BASELINE configs 2-4):
+    // slot-row stride D / 2 as an immediate; any other layout: runtime stride.
+    const bool imm = st.dm.kstride == D / 2 && st.dm.vchunks == D / 16 && getenv("TKV_K1_RUNTIME_STRIDE") == nullptr;
+#define TKV_K1(DD, MB, PV)                                                                                    \
+  (imm ? launch_k1_warp<DD, MB, PV, DD / 2>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s)         \
+       : launch_k1_warp<DD, MB, PV, 0>(st, q, k, v, out, buf_half, nbuf, put_half, put_slot, s))
+    if (D == 128) return pvn ? TKV_K1(128, 3, true) : TKV_K1(128, 3, false);
+    // d = 64 fits 128 registers without spills: 4 CTAs (16 warps) per SM.
+    // Measured at config 3: 3 CTAs/SM 0.287 ms, 4: 0.249 ms, 5 (96 registers,
+    // 48 B spilled): 0.308 ms (profiles/r02_c3_k1_minb*.json).
+    return pvn ? TKV_K1(64, 4, true) : TKV_K1(64, 4, false);
+#undef TKV_K1
   }
   const size_t smem = (size_t)kWarps * 8 * (2 + D) * 4 + (size_t)kWarps * 128 * 4 + (size_t)32 * (D / 8) * 4 +
                       (size_t)(st.dm.NS + st.dm.g + 1 + 4 * 16) * 8 + (size_t)st.dm.P * 8;
