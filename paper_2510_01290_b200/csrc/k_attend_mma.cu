@@ -925,43 +925,69 @@ __device__ __forceinline__ void compute_tile4(const Tile<D, FMT>& T, const uint3
     if (gid >= 4) { bh0 = bl0; bh1 = bl1; }
   }
   // ---- O^T += V^T P ----------------------------------------------------------
+  // Grouped formats (NVFP4, ternary): the code words of a PV token pair are
+  // interleaved nibble-wise before conversion -- byte k of lo[p] holds channel
+  // 2k of tokens (2p, 2p+1), byte k of hi[p] channel 2k+1 -- so one F2FP yields
+  // an A-fragment register directly (no byte_perm transpose per m-tile), and the
+  // pair's two value-chunk scales form one f16x2 multiplier.
+  constexpr bool kPair = FMT == TKV_FMT_NVFP4 || FMT == TKV_FMT_TERNARY;
   uint32_t vsc[4];
-  if constexpr (Gm::SCALED) {
+  if constexpr (kPair) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) e4m3x2_b(T.vs[i], 0, vsc[i]);
+    for (int pp = 0; pp < 2; ++pp) {
+      const uint32_t b = __byte_perm(T.vs[2 * pp], T.vs[2 * pp + 1], 0x0040);  // (s_2p, s_2p+1)
+      asm("{\n .reg .b16 h0, h1;\n mov.b32 {h0, h1}, %1;\n cvt.rn.f16x2.e4m3x2 %0, h0;\n}" : "=r"(vsc[pp]) : "r"(b));
+    }
   }
-  uint32_t tsp[4][(Gm::MT + 3) / 4];  // ternary: e2m1 nibbles of each 8-code half-word
-  if constexpr (FMT == TKV_FMT_TERNARY) {
+  constexpr int kVW = FMT == TKV_FMT_TERNARY ? (Gm::MT + 3) / 4 : Gm::VW;  // nibble words per token
+  uint32_t vlo[2][kVW], vhi[2][kVW];
+  if constexpr (kPair) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int w = 0; w < kVW; ++w)
 #pragma unroll
-      for (int h = 0; h < (Gm::MT + 3) / 4; ++h) tsp[i][h] = tern_spread(T.v[i].w[0] >> (16 * h));
+      for (int pp = 0; pp < 2; ++pp) {
+        uint32_t wa, wb;
+        if constexpr (FMT == TKV_FMT_TERNARY) {
+          wa = tern_spread(T.v[2 * pp].w[0] >> (16 * w));
+          wb = tern_spread(T.v[2 * pp + 1].w[0] >> (16 * w));
+        } else {
+          wa = T.v[2 * pp].w[w];
+          wb = T.v[2 * pp + 1].w[w];
+        }
+        vlo[pp][w] = (wa & 0x0f0f0f0fu) | ((wb << 4) & 0xf0f0f0f0u);
+        vhi[pp][w] = ((wa >> 4) & 0x0f0f0f0fu) | (wb & 0xf0f0f0f0u);
+      }
   }
 #pragma unroll
   for (int mt = 0; mt < Gm::MT; ++mt) {
-    uint32_t x[4];  // per PV token: f16x2 / bf16x2 of channels (2mt, 2mt+1) of the thread's range
+    uint32_t a0, a1, a2, a3;
+    if constexpr (kPair) {
+      uint32_t c0, c1, c2, c3;
+      e2m1x2_b(vlo[0][mt >> 2], mt & 3, c0);  // row gid (ch 2mt), tokens tig*2, tig*2+1
+      e2m1x2_b(vhi[0][mt >> 2], mt & 3, c1);  // row gid+8 (ch 2mt+1)
+      e2m1x2_b(vlo[1][mt >> 2], mt & 3, c2);  // row gid, tokens +8, +9
+      e2m1x2_b(vhi[1][mt >> 2], mt & 3, c3);
+      a0 = hmul2(c0, vsc[0]);
+      a1 = hmul2(c1, vsc[0]);
+      a2 = hmul2(c2, vsc[1]);
+      a3 = hmul2(c3, vsc[1]);
+    } else {
+      uint32_t x[4];  // per PV token: f16x2 / bf16x2 of channels (2mt, 2mt+1) of the thread's range
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if constexpr (FMT == TKV_FMT_NVFP4) {
-        uint32_t h;
-        e2m1x2_b(T.v[i].w[mt >> 2], mt & 3, h);
-        x[i] = hmul2(h, vsc[i]);
-      } else if constexpr (FMT == TKV_FMT_FP8) {
-        uint32_t lo, hi;
-        e4m3x4(T.v[i].w[mt >> 1], lo, hi);
-        x[i] = (mt & 1) ? hi : lo;
-      } else if constexpr (FMT == TKV_FMT_TERNARY) {
-        uint32_t h;
-        e2m1x2_b(tsp[i][mt >> 2], mt & 3, h);
-        x[i] = hmul2(h, vsc[i]);
-      } else {
-        x[i] = T.v[i].w[mt];
+      for (int i = 0; i < 4; ++i) {
+        if constexpr (FMT == TKV_FMT_FP8) {
+          uint32_t lo, hi;
+          e4m3x4(T.v[i].w[mt >> 1], lo, hi);
+          x[i] = (mt & 1) ? hi : lo;
+        } else {
+          x[i] = T.v[i].w[mt];
+        }
       }
+      a0 = __byte_perm(x[0], x[1], 0x5410);  // row gid (ch 2mt), tokens tig*2, tig*2+1
+      a1 = __byte_perm(x[0], x[1], 0x7632);  // row gid+8 (ch 2mt+1)
+      a2 = __byte_perm(x[2], x[3], 0x5410);  // row gid, tokens +8, +9
+      a3 = __byte_perm(x[2], x[3], 0x7632);
     }
-    const uint32_t a0 = __byte_perm(x[0], x[1], 0x5410);  // row gid (ch 2mt), tokens tig*2, tig*2+1
-    const uint32_t a1 = __byte_perm(x[0], x[1], 0x7632);  // row gid+8 (ch 2mt+1)
-    const uint32_t a2 = __byte_perm(x[2], x[3], 0x5410);  // row gid, tokens +8, +9
-    const uint32_t a3 = __byte_perm(x[2], x[3], 0x7632);
     mma16816<Gm::BF16>(A.o[mt], a0, a1, a2, a3, bh0, bh1);
     if constexpr (!PVN) mma16816<Gm::BF16>(A.o[mt], a0, a1, a2, a3, bl0, bl1);
   }
