@@ -344,3 +344,31 @@ def test_export_edge_cases():
     small = torch.empty(8, dtype=torch.uint8, device=dev)
     rc = _abi.lib.tkv_export_cache(run._h, 0, cfg.units, small.data_ptr(), 8, None, C.byref(need))
     assert rc == 2 and need.value > 8
+
+
+@pytest.mark.parametrize("D,maxpool", [(128, False), (64, True)])
+def test_immediate_and_runtime_slot_stride_k1_agree(monkeypatch, D, maxpool):
+    """K1's immediate slot-row stride instantiation (widest band 4-bit, the
+    BASELINE configs 2-4) and its runtime-stride form (TKV_K1_RUNTIME_STRIDE)
+    compute bit-identical outputs and leave identical cache state."""
+    S, U, G = 2, 3, 8 if maxpool else 4
+    cfg = ThinkvConfig(num_seqs=S, units_per_seq=U, num_q_heads=G, gqa_maxpool=maxpool, head_dim=D, tau=32,
+                       group_size=16, block_size=16, budget=80, levels=(16, 8, 4), psi_bits=(4, 4, 2),
+                       max_gen_len=260, script=script(S, 10, seed=5), record_events=True)
+    dev = torch.device("cuda:0")
+    a, b = DecodeRun(cfg), DecodeRun(cfg)
+    out_a = torch.empty((cfg.units, cfg.out_rows, D), device=dev)
+    out_b = torch.empty_like(out_a)
+    for t in range(cfg.max_gen_len):
+        q, k, v = O.synth_step(0x71534B56, cfg.units_per_seq, cfg.tau, cfg.units, G, D, t)
+        tq, tk, tv = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(dev) for x in (q, k, v))
+        monkeypatch.delenv("TKV_K1_RUNTIME_STRIDE", raising=False)
+        a.step(tq, tk, tv, out_a)
+        monkeypatch.setenv("TKV_K1_RUNTIME_STRIDE", "1")
+        b.step(tq, tk, tv, out_b)
+        assert torch.equal(out_a, out_b), f"step {t}"
+    a.finish()
+    b.finish()
+    for s in range(S):
+        assert b.tables(s) == a.tables(s)
+        assert b.segments(s) == a.segments(s)
