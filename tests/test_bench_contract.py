@@ -23,6 +23,10 @@ def test_reference_arm_line():
     assert line["e2e"] == {"value": line["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert line["config"]["global_batch"] == 1 and line["scaling"] == "weak"
+    # the GPU arm prints the same config object (bench_config), incl. the L2 statement
+    assert line["config"]["l2"].startswith("working set fits in L2")
+    assert set(line["config"]) == {"workload", "global_batch", "units_per_gpu", "parallelism", "gqa", "tau",
+                                   "timed_positions", "e2e_positions", "tpot_formula", "l2"}
 
 
 def test_reference_arm_does_not_map_the_cuda_library():
